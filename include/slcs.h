@@ -1,0 +1,175 @@
+/*
+ * slcs.h -- C ABI of the B200-native SLCS/ImgQL primitive layer.
+ *
+ * This is the drop-in boundary below the reference executor's opcode dispatch
+ * `evalTask` (proj/src/executor.cpp:74-115, declared proj/include/pixlog/executor.hpp:54-55).
+ * Every entry point is plain C: opaque handles, plain pointers and sizes, int
+ * status codes, no C++ or torch types.  INTEGRATION.md shows the C++ shim a
+ * reference maintainer adds (a device variant of `Value`, a rethrowing
+ * wrapper) and the ctypes binding used by this repository's Python host.
+ *
+ * Semantics are bit-exact with the reference CPU path.
+ *
+ * Threading: all entry points are safe to call concurrently from several host
+ * threads (the reference evaluates independent DAG nodes on WorkerPool
+ * threads, executor.cpp:220,259).  Work is enqueued in call order on the
+ * context's stream; only volume/download/program outputs synchronise.
+ *
+ * Errors: a non-zero status plus a thread-local message (slcs_last_error)
+ * that reuses the reference's RunError texts, e.g. "dimension mismatch"
+ * (kernels.cpp:16-21), "expects a boolean image, got u16" (kernels.cpp:10-14),
+ * "reach expects boolean images" (reach.cpp:13-14), "image too large for
+ * packed coordinate labels" (image.cpp:26-28).
+ */
+#ifndef SLCS_H
+#define SLCS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLCS_ABI_VERSION 1
+
+typedef struct slcs_ctx slcs_ctx;         /* one device + one stream + memory pool */
+typedef struct slcs_image slcs_image;     /* refcounted immutable device image      */
+typedef struct slcs_program slcs_program; /* a whole task DAG compiled for replay   */
+
+/* PixelKind, proj/include/pixlog/image.hpp:16 */
+typedef enum { SLCS_BOOL = 0, SLCS_U16 = 1, SLCS_LABEL = 2 } slcs_kind;
+
+/* kernels::CmpOp, proj/include/pixlog/kernels.hpp:10 (">." ">=." "<." "<=." "=.") */
+typedef enum { SLCS_GT = 0, SLCS_GE = 1, SLCS_LT = 2, SLCS_LE = 3, SLCS_EQ = 4 } slcs_cmp;
+
+typedef enum {
+  SLCS_OK = 0,
+  SLCS_ERR_KIND = 1,      /* wrong pixel kind (RunError "expects a ... image")        */
+  SLCS_ERR_SHAPE = 2,     /* dimension mismatch / bad dimensions                      */
+  SLCS_ERR_TOO_LARGE = 3, /* labels need W*H < 0xFFFFFFFE (image.cpp:26-28)           */
+  SLCS_ERR_OOM = 4,       /* device allocation failed                                 */
+  SLCS_ERR_CUDA = 5,      /* CUDA runtime error                                       */
+  SLCS_ERR_NCCL = 6,      /* collective failure (multi-GPU)                           */
+  SLCS_ERR_ARG = 7,       /* invalid argument (null handle, bad enum, ...)            */
+  SLCS_ERR_RUN = 8,       /* evaluation error (division by zero, unknown opcode, ...) */
+  SLCS_ERR_NOGPU = 9      /* no CUDA device: the product path has no CPU fallback     */
+} slcs_status;
+
+/* ---- library / context --------------------------------------------------- */
+
+int slcs_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* slcs_last_error(void);
+
+/* Creates a context on `device`.  `cuda_stream` is a cudaStream_t to enqueue
+ * on (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a private
+ * non-blocking stream. */
+int slcs_ctx_create(int device, void* cuda_stream, slcs_ctx** out);
+int slcs_ctx_destroy(slcs_ctx* ctx);
+int slcs_ctx_synchronize(slcs_ctx* ctx);
+void* slcs_ctx_stream(slcs_ctx* ctx);
+/* Number of kernels this context has launched (for bench gpu_launches). */
+int64_t slcs_ctx_launch_count(slcs_ctx* ctx);
+
+/* ---- device images (refcounted, mirror shared_ptr<const ImageBuffer>) ----
+ * Host layout is the reference ImageBuffer layout (image.hpp:36-75): row-major,
+ * Bool = 1 byte/pixel (0 or nonzero), U16 = 2 bytes, LABEL = uint32 idx+1.
+ * `batch` stacks same-shape slices (slice s at offset s*W*H in host memory);
+ * the single-image reference API uses batch = 1.
+ * Device layout: Bool is bit-packed, 32 px per uint32 word,
+ * LSB = lowest column, row pitch padded to 16 B, padding bits zero; U16 rows
+ * are padded to 32 pixels; labels are dense uint32. */
+int slcs_image_upload(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batch,
+                      const void* host, slcs_image** out);
+/* Same, from DEVICE memory already in the reference dense layout. */
+int slcs_image_from_device(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batch,
+                           const void* dev, slcs_image** out);
+/* Copies into host memory in the reference layout (Bool -> bytes 0/1).
+ * `bytes` must be >= W*H*batch*sizeof(pixel).  Synchronises. */
+int slcs_image_download(slcs_ctx* ctx, const slcs_image* img, void* host, size_t bytes);
+/* Device-to-device copy into the reference dense layout (no sync). */
+int slcs_image_to_device(slcs_ctx* ctx, const slcs_image* img, void* dev, size_t bytes);
+int slcs_image_retain(slcs_image* img);
+int slcs_image_release(slcs_image* img);
+int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch);
+/* Raw device storage (bit-packed for Bool) for zero-copy interop. */
+int slcs_image_storage(const slcs_image* img, void** dev, size_t* row_pitch_bytes,
+                       size_t* slice_bytes);
+
+/* ---- primitives: each returns a NEW image (*out, refcount 1) --------------
+ * Boolean operands that are U16 are coerced by `p > 0` (boolArg,
+ * executor.cpp:43-50).  Label images are rejected. */
+
+/* kernels::threshold (kernels.cpp:75-97): U16 -> Bool, double(p) op n. */
+int slcs_threshold(slcs_ctx* ctx, slcs_cmp op, const slcs_image* img, double n,
+                   slcs_image** out);
+/* kernels::logicalNot / logicalAnd / logicalOr (kernels.cpp:36-73). */
+int slcs_not(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
+int slcs_and(slcs_ctx* ctx, const slcs_image* a, const slcs_image* b, slcs_image** out);
+int slcs_or(slcs_ctx* ctx, const slcs_image* a, const slcs_image* b, slcs_image** out);
+/* kernels::dilate = near (kernels.cpp:99-124); near_k = near applied k times
+ * (one launch, (2k+1)^2 clipped box). */
+int slcs_near(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
+int slcs_near_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out);
+/* stdlib interior = !near(!a) (stdlib.imgql:5) as one erosion launch. */
+int slcs_interior(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
+int slcs_interior_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out);
+/* kernels::countTrue = volume (kernels.cpp:126-136).  `out` holds `batch`
+ * counts (one per slice).  Synchronises. */
+int slcs_volume(slcs_ctx* ctx, const slcs_image* a, int64_t* out);
+/* ccl::label (ccl.cpp:127-165): 8-connected labels, each component labelled
+ * with its max row-major index + 1 (ccl.hpp:52-60), background 0. */
+int slcs_ccl(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
+/* reach(target, through) (reach.cpp:10-50). */
+int slcs_reach(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+               slcs_image** out);
+/* NEW opcode maxvol: union of the 8-connected components of maximal pixel
+ * count (ties keep all maxima; per slice for batches).  No reference pin. */
+int slcs_maxvol(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
+
+/* ---- host-in / host-out wrappers with the reference signatures -----------
+ * kernels::threshold / logicalNot / logicalAnd / logicalOr / dilate /
+ * countTrue, ccl::label, reach -- for callers holding host ImageBuffers. */
+int slcs_h_threshold(slcs_ctx* ctx, slcs_cmp op, const uint16_t* img, int w, int h, double n,
+                     uint8_t* out);
+int slcs_h_not(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint8_t* out);
+int slcs_h_and(slcs_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, uint8_t* out);
+int slcs_h_or(slcs_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, uint8_t* out);
+int slcs_h_dilate(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint8_t* out);
+int slcs_h_count_true(slcs_ctx* ctx, const uint8_t* a, int w, int h, int64_t* out);
+int slcs_h_ccl_label(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint32_t* out);
+int slcs_h_reach(slcs_ctx* ctx, const uint8_t* target, const uint8_t* through, int w, int h,
+                 uint8_t* out);
+
+/* ---- programs: a whole TaskGraph evaluated device-resident ----------------
+ * Replaces executor::run's per-node scheduling (executor.cpp:117-282) below
+ * the same Task contract (task_graph.hpp:20-24): tasks in id order (deps have
+ * smaller ids, task_graph.cpp:64-70), opcode strings from the builtin table
+ * (task_graph.cpp:131-139) plus "const", "load", "save", "print", and the new
+ * "maxvol".  payload_num is used by "const"; payload_str by load/save/print.
+ * deps of task i are deps[dep_off[i] .. dep_off[i+1]).
+ * The program binds "load" names to images, plans device memory by liveness,
+ * fuses elementwise/threshold chains and near runs, and records the whole
+ * evaluation into a CUDA graph that is replayed by slcs_program_run. */
+int slcs_program_create(slcs_ctx* ctx, int n_tasks, const char* const* opcodes,
+                        const double* payload_num, const char* const* payload_str,
+                        const int* dep_off, const int* deps, slcs_program** out);
+int slcs_program_destroy(slcs_program* prog);
+/* Binds the image loaded by `load` tasks with payload `name`. */
+int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* img);
+/* flags: bit 0 = capture/replay as a CUDA graph, bit 1 = disable fusion. */
+int slcs_program_run(slcs_program* prog, int flags);
+/* Result of task `task` (an image; *out gets a new reference) or a number
+ * (synchronises).  kind_out: 0 image, 1 number. */
+int slcs_program_result(slcs_program* prog, int task, int* kind_out, slcs_image** img_out,
+                        double* num_out);
+/* Kernel launches issued by one run (after fusion). */
+int slcs_program_launches(slcs_program* prog, int* out);
+/* Human-readable execution plan (fused groups, buffer slots). */
+const char* slcs_program_plan(slcs_program* prog);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLCS_H */

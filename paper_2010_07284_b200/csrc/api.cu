@@ -1,0 +1,627 @@
+// api.cu -- the C ABI (include/slcs.h): contexts, refcounted device images,
+// primitive entry points with the reference's argument checks and error
+// texts, and host-in/host-out wrappers with the kernels::/ccl::/reach
+// signatures.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "slcs_internal.h"
+
+namespace slcs {
+int launch_pack_u16_mask(const uint16_t* dense, uint32_t* bits, const Geo& g, cudaStream_t st);
+}
+
+using namespace slcs;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SLCS_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SLCS_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SLCS_ERR_RUN;
+  }
+}
+
+const char* kind_name(int k) {
+  switch (k) {
+    case SLCS_BOOL: return "bool";
+    case SLCS_U16: return "u16";
+    case SLCS_LABEL: return "label";
+  }
+  return "?";
+}
+
+size_t unit_bytes(int kind) { return kind == SLCS_U16 ? 2 : 4; }
+
+Geo geo_for(int kind, int w, int h, int batch) {
+  switch (kind) {
+    case SLCS_BOOL: return bool_geo(w, h, batch);
+    case SLCS_U16: return u16_geo(w, h, batch);
+    case SLCS_LABEL: return label_geo(w, h, batch);
+  }
+  fail(SLCS_ERR_ARG, "unknown pixel kind");
+}
+
+void check_dims(int w, int h, int batch) {
+  if (w < 1 || h < 1)
+    fail(SLCS_ERR_SHAPE, "image dimensions must be at least 1x1, got " + std::to_string(w) +
+                             "x" + std::to_string(h));
+  if (batch < 1) fail(SLCS_ERR_SHAPE, "batch must be at least 1");
+}
+
+struct DeviceGuard {
+  explicit DeviceGuard(int dev) { cuda_check(cudaSetDevice(dev), "cudaSetDevice"); }
+};
+
+}  // namespace
+
+void* slcs_ctx::alloc(size_t bytes) {
+  void* p = nullptr;
+  cuda_check(cudaMallocAsync(&p, bytes ? bytes : 16, stream), "cudaMallocAsync");
+  return p;
+}
+
+void slcs_ctx::release(void* p) {
+  if (p) cudaFreeAsync(p, stream);
+}
+
+namespace slcs {
+
+slcs_image* new_image(slcs_ctx* ctx, int kind, int w, int h, int batch) {
+  check_dims(w, h, batch);
+  auto* img = new slcs_image;
+  img->ctx = ctx;
+  img->kind = kind;
+  img->geo = geo_for(kind, w, h, batch);
+  img->bytes = img->geo.slice * size_t(batch) * unit_bytes(kind);
+  try {
+    img->data = ctx->alloc(img->bytes);
+  } catch (...) {
+    delete img;
+    throw;
+  }
+  return img;
+}
+
+void drop_image(slcs_image* img) {
+  if (img && img->refs.fetch_sub(1) == 1) {
+    DeviceGuard dg(img->ctx->device);
+    img->ctx->release(img->data);
+    delete img;
+  }
+}
+
+// RAII holder for intermediate images
+struct Ref {
+  slcs_image* p = nullptr;
+  Ref() = default;
+  explicit Ref(slcs_image* q) : p(q) {}
+  Ref(const Ref&) = delete;
+  ~Ref() { drop_image(p); }
+  slcs_image* release() {
+    slcs_image* q = p;
+    p = nullptr;
+    return q;
+  }
+};
+
+const uint32_t* words(const slcs_image* img) { return static_cast<const uint32_t*>(img->data); }
+uint32_t* words(slcs_image* img) { return static_cast<uint32_t*>(img->data); }
+
+void need_ctx(slcs_ctx* ctx) {
+  if (!ctx) fail(SLCS_ERR_ARG, "null context");
+}
+void need_img(const slcs_image* img) {
+  if (!img) fail(SLCS_ERR_ARG, "null image");
+}
+
+// boolArg (executor.cpp:43-50): Bool passes through, U16 coerces by p > 0,
+// anything else is a type error.  Returns a NEW reference.
+slcs_image* bool_arg(slcs_ctx* ctx, const slcs_image* v, const char* op) {
+  need_img(v);
+  if (v->kind == SLCS_BOOL) {
+    const_cast<slcs_image*>(v)->refs.fetch_add(1);
+    return const_cast<slcs_image*>(v);
+  }
+  if (v->kind == SLCS_U16) {
+    slcs_image* out = new_image(ctx, SLCS_BOOL, v->geo.w, v->geo.h, v->geo.batch);
+    ctx->launches += launch_threshold(static_cast<const uint16_t*>(v->data), words(out), v->geo,
+                                      out->geo, 1, 65535, ctx->stream);
+    return out;
+  }
+  fail(SLCS_ERR_KIND, std::string("'") + op + "' expects a boolean image, got " +
+                          kind_name(v->kind));
+}
+
+void same_shape(const slcs_image* a, const slcs_image* b, const char* op) {
+  if (a->geo.w != b->geo.w || a->geo.h != b->geo.h || a->geo.batch != b->geo.batch)
+    fail(SLCS_ERR_SHAPE, std::string(op) + ": dimension mismatch (" + std::to_string(a->geo.w) +
+                             "x" + std::to_string(a->geo.h) + " vs " + std::to_string(b->geo.w) +
+                             "x" + std::to_string(b->geo.h) + ")");
+}
+
+// threshold interval of SURVEY.md Appendix A #5 (host side)
+void threshold_interval(int op, double n, int& lo, int& hi) {
+  lo = 1;
+  hi = 0;
+  if (std::isnan(n)) return;
+  double l = 0.0, u = 65535.0;
+  switch (op) {
+    case SLCS_GT: l = std::floor(n) + 1.0; break;
+    case SLCS_GE: l = std::ceil(n); break;
+    case SLCS_LT: u = std::ceil(n) - 1.0; break;
+    case SLCS_LE: u = std::floor(n); break;
+    case SLCS_EQ:
+      if (std::floor(n) != n) return;
+      l = u = n;
+      break;
+    default: fail(SLCS_ERR_ARG, "unknown comparison operator");
+  }
+  if (l < 0.0) l = 0.0;
+  if (u > 65535.0) u = 65535.0;
+  if (l > u) return;
+  lo = int(l);
+  hi = int(u);
+}
+
+const char* cmp_symbol(int op) {
+  switch (op) {
+    case SLCS_GT: return ">.";
+    case SLCS_GE: return ">=.";
+    case SLCS_LT: return "<.";
+    case SLCS_LE: return "<=.";
+    case SLCS_EQ: return "=.";
+  }
+  return "?";
+}
+
+slcs_image* op_threshold(slcs_ctx* ctx, int op, const slcs_image* img, double n) {
+  need_img(img);
+  if (op < 0 || op > 4) fail(SLCS_ERR_ARG, "unknown comparison operator");
+  if (img->kind != SLCS_U16)
+    fail(SLCS_ERR_KIND, std::string(cmp_symbol(op)) + " expects a numeric image, got " +
+                            kind_name(img->kind));
+  int lo, hi;
+  threshold_interval(op, n, lo, hi);
+  slcs_image* out = new_image(ctx, SLCS_BOOL, img->geo.w, img->geo.h, img->geo.batch);
+  ctx->launches += launch_threshold(static_cast<const uint16_t*>(img->data), words(out), img->geo,
+                                    out->geo, lo, hi, ctx->stream);
+  return out;
+}
+
+slcs_image* op_not(slcs_ctx* ctx, const slcs_image* a0) {
+  Ref a(bool_arg(ctx, a0, "!"));
+  slcs_image* out = new_image(ctx, SLCS_BOOL, a.p->geo.w, a.p->geo.h, a.p->geo.batch);
+  ctx->launches += launch_not(words(a.p), words(out), a.p->geo, ctx->stream);
+  return out;
+}
+
+slcs_image* op_binary(slcs_ctx* ctx, const slcs_image* a0, const slcs_image* b0, bool is_and) {
+  const char* name = is_and ? "&" : "|";
+  Ref a(bool_arg(ctx, a0, name));
+  Ref b(bool_arg(ctx, b0, name));
+  same_shape(a.p, b.p, name);
+  slcs_image* out = new_image(ctx, SLCS_BOOL, a.p->geo.w, a.p->geo.h, a.p->geo.batch);
+  if (is_and)
+    ctx->launches += launch_and(words(a.p), words(b.p), words(out), a.p->geo, ctx->stream);
+  else
+    ctx->launches += launch_or(words(a.p), words(b.p), words(out), a.p->geo, ctx->stream);
+  return out;
+}
+
+slcs_image* op_near(slcs_ctx* ctx, const slcs_image* a0, int k, bool erode) {
+  if (k < 1) fail(SLCS_ERR_ARG, "near/interior: k must be >= 1");
+  Ref a(bool_arg(ctx, a0, erode ? "interior" : "near"));
+  const Geo& g = a.p->geo;
+  Ref cur;
+  const slcs_image* src = a.p;
+  while (k > 0) {
+    int step = k > 8 ? 8 : k;
+    slcs_image* out = new_image(ctx, SLCS_BOOL, g.w, g.h, g.batch);
+    ctx->launches += launch_near(words(src), words(out), g, step, erode, ctx->stream);
+    k -= step;
+    drop_image(cur.p);
+    cur.p = out;
+    src = out;
+  }
+  return cur.release();
+}
+
+void op_volume(slcs_ctx* ctx, const slcs_image* a0, int64_t* out) {
+  Ref a(bool_arg(ctx, a0, "volume"));
+  int b = a.p->geo.batch;
+  if (ctx->counts_cap < b) {
+    if (ctx->d_counts) cudaFree(ctx->d_counts);
+    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+    ctx->d_counts = nullptr;
+    ctx->h_counts = nullptr;
+    cuda_check(cudaMalloc(&ctx->d_counts, sizeof(unsigned long long) * b), "cudaMalloc");
+    cuda_check(cudaMallocHost(&ctx->h_counts, sizeof(unsigned long long) * b), "cudaMallocHost");
+    ctx->counts_cap = b;
+  }
+  ctx->launches += launch_volume(words(a.p), ctx->d_counts, a.p->geo, ctx->stream);
+  cuda_check(cudaMemcpyAsync(ctx->h_counts, ctx->d_counts, sizeof(unsigned long long) * b,
+                             cudaMemcpyDeviceToHost, ctx->stream),
+             "volume readback");
+  cuda_check(cudaStreamSynchronize(ctx->stream), "volume sync");
+  for (int i = 0; i < b; ++i) out[i] = int64_t(ctx->h_counts[i]);
+}
+
+struct Scratch {
+  slcs_ctx* ctx;
+  void* p = nullptr;
+  Scratch(slcs_ctx* c, size_t bytes) : ctx(c) {
+    if (bytes) p = ctx->alloc(bytes);
+  }
+  ~Scratch() { ctx->release(p); }
+};
+
+slcs_image* op_ccl(slcs_ctx* ctx, const slcs_image* a0) {
+  need_img(a0);
+  if (a0->kind == SLCS_LABEL)
+    fail(SLCS_ERR_KIND, "component labelling expects a boolean image, got label");
+  Ref a(bool_arg(ctx, a0, "ccl"));
+  const Geo& g = a.p->geo;
+  if ((unsigned long long)g.w * (unsigned long long)g.h >= 0xfffffffeull)
+    fail(SLCS_ERR_TOO_LARGE, "image too large for packed coordinate labels");
+  Ref out(new_image(ctx, SLCS_LABEL, g.w, g.h, g.batch));
+  Scratch s(ctx, ccl_scratch_bytes(g.w, g.h, g.batch, false, false));
+  CclScratch cs;
+  ccl_scratch_carve(s.p, g.w, g.h, g.batch, false, false, &cs);
+  ctx->launches += launch_ccl(words(a.p), words(out.p), g, cs, ctx->stream);
+  return out.release();
+}
+
+slcs_image* op_reach(slcs_ctx* ctx, const slcs_image* t0, const slcs_image* u0) {
+  need_img(t0);
+  need_img(u0);
+  if (t0->kind == SLCS_LABEL || u0->kind == SLCS_LABEL)
+    fail(SLCS_ERR_KIND, "reach expects boolean images");
+  Ref t(bool_arg(ctx, t0, "reach"));
+  Ref u(bool_arg(ctx, u0, "reach"));
+  if (t.p->geo.w != u.p->geo.w || t.p->geo.h != u.p->geo.h || t.p->geo.batch != u.p->geo.batch)
+    fail(SLCS_ERR_SHAPE, "reach: dimension mismatch (" + std::to_string(t.p->geo.w) + "x" +
+                             std::to_string(t.p->geo.h) + " vs " + std::to_string(u.p->geo.w) +
+                             "x" + std::to_string(u.p->geo.h) + ")");
+  const Geo& g = t.p->geo;
+  Ref out(new_image(ctx, SLCS_BOOL, g.w, g.h, g.batch));
+  bool small = ccl_small_path(g.w, g.h);
+  size_t sb = ccl_scratch_bytes(g.w, g.h, g.batch, true, false);
+  size_t tb = small ? 0 : g.slice * size_t(g.batch) * 4;
+  Scratch s(ctx, sb + tb);
+  CclScratch cs;
+  ccl_scratch_carve(s.p, g.w, g.h, g.batch, true, false, &cs);
+  uint32_t* tmp = small ? nullptr : reinterpret_cast<uint32_t*>(static_cast<char*>(s.p) + sb);
+  ctx->launches +=
+      launch_reach(words(t.p), words(u.p), words(out.p), tmp, g, cs, ctx->stream);
+  return out.release();
+}
+
+slcs_image* op_maxvol(slcs_ctx* ctx, const slcs_image* a0) {
+  Ref a(bool_arg(ctx, a0, "maxvol"));
+  const Geo& g = a.p->geo;
+  Ref out(new_image(ctx, SLCS_BOOL, g.w, g.h, g.batch));
+  Scratch s(ctx, ccl_scratch_bytes(g.w, g.h, g.batch, false, true));
+  CclScratch cs;
+  ccl_scratch_carve(s.p, g.w, g.h, g.batch, false, true, &cs);
+  ctx->launches += launch_maxvol(words(a.p), words(out.p), g, cs, ctx->stream);
+  return out.release();
+}
+
+slcs_image* upload(slcs_ctx* ctx, int kind, int w, int h, int batch, const void* src,
+                   bool from_device) {
+  need_ctx(ctx);
+  check_dims(w, h, batch);
+  if (!src) fail(SLCS_ERR_ARG, "null source buffer");
+  Ref img(new_image(ctx, kind, w, h, batch));
+  size_t npx = size_t(w) * size_t(h) * size_t(batch);
+  cudaMemcpyKind dir = from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (kind == SLCS_LABEL) {
+    cuda_check(cudaMemcpyAsync(img.p->data, src, npx * 4, dir, ctx->stream), "upload labels");
+  } else if (kind == SLCS_U16) {
+    cuda_check(cudaMemcpy2DAsync(img.p->data, img.p->geo.pitch * 2, src, size_t(w) * 2,
+                                 size_t(w) * 2, size_t(h) * size_t(batch), dir, ctx->stream),
+               "upload u16");
+  } else {
+    const void* dev = src;
+    void* staging = nullptr;
+    if (!from_device) {
+      staging = ctx->alloc(npx);
+      cuda_check(cudaMemcpyAsync(staging, src, npx, cudaMemcpyHostToDevice, ctx->stream),
+                 "upload bool");
+      dev = staging;
+    }
+    ctx->launches += launch_pack_u8(static_cast<const uint8_t*>(dev), words(img.p), img.p->geo,
+                                    true, ctx->stream);
+    ctx->release(staging);
+  }
+  return img.release();
+}
+
+void download(slcs_ctx* ctx, const slcs_image* img, void* dst, size_t bytes, bool to_device) {
+  need_ctx(ctx);
+  need_img(img);
+  if (!dst) fail(SLCS_ERR_ARG, "null destination buffer");
+  const Geo& g = img->geo;
+  size_t npx = size_t(g.w) * size_t(g.h) * size_t(g.batch);
+  size_t need = npx * (img->kind == SLCS_BOOL ? 1 : unit_bytes(img->kind));
+  if (bytes < need) fail(SLCS_ERR_ARG, "destination buffer too small");
+  cudaMemcpyKind dir = to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (img->kind == SLCS_LABEL) {
+    cuda_check(cudaMemcpyAsync(dst, img->data, need, dir, ctx->stream), "download labels");
+  } else if (img->kind == SLCS_U16) {
+    cuda_check(cudaMemcpy2DAsync(dst, size_t(g.w) * 2, img->data, g.pitch * 2, size_t(g.w) * 2,
+                                 size_t(g.h) * size_t(g.batch), dir, ctx->stream),
+               "download u16");
+  } else {
+    if (to_device) {
+      ctx->launches += launch_unpack(words(img), static_cast<uint8_t*>(dst), g, ctx->stream);
+    } else {
+      void* staging = ctx->alloc(npx);
+      ctx->launches += launch_unpack(words(img), static_cast<uint8_t*>(staging), g, ctx->stream);
+      cuda_check(cudaMemcpyAsync(dst, staging, npx, cudaMemcpyDeviceToHost, ctx->stream),
+                 "download bool");
+      ctx->release(staging);
+    }
+  }
+  if (!to_device) cuda_check(cudaStreamSynchronize(ctx->stream), "download sync");
+}
+
+}  // namespace slcs
+
+// ============================================================================
+extern "C" {
+
+int slcs_abi_version(void) { return SLCS_ABI_VERSION; }
+const char* slcs_last_error(void) { return g_err.c_str(); }
+
+int slcs_ctx_create(int device, void* cuda_stream, slcs_ctx** out) {
+  return guard([&] {
+    if (!out) fail(SLCS_ERR_ARG, "null output pointer");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+      fail(SLCS_ERR_NOGPU, "no CUDA device available (the SLCS library has no CPU fallback)");
+    if (device < 0 || device >= n) fail(SLCS_ERR_ARG, "device index out of range");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new slcs_ctx;
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cuda_stream) {
+      c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+      c->own_stream = true;
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+  });
+}
+
+int slcs_ctx_destroy(slcs_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->d_counts) cudaFree(ctx->d_counts);
+    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int slcs_ctx_synchronize(slcs_ctx* ctx) {
+  return guard([&] {
+    need_ctx(ctx);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+    cuda_check(cudaGetLastError(), "kernel launch");
+  });
+}
+
+void* slcs_ctx_stream(slcs_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int64_t slcs_ctx_launch_count(slcs_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+#define LOCKED(ctx) \
+  need_ctx(ctx);    \
+  std::lock_guard<std::mutex> lock_((ctx)->mu); \
+  DeviceGuard dg_((ctx)->device)
+
+int slcs_image_upload(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batch, const void* host,
+                      slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output pointer");
+    *out = upload(ctx, kind, w, h, batch, host, false);
+  });
+}
+
+int slcs_image_from_device(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batch,
+                           const void* dev, slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output pointer");
+    *out = upload(ctx, kind, w, h, batch, dev, true);
+  });
+}
+
+int slcs_image_download(slcs_ctx* ctx, const slcs_image* img, void* host, size_t bytes) {
+  return guard([&] {
+    LOCKED(ctx);
+    download(ctx, img, host, bytes, false);
+  });
+}
+
+int slcs_image_to_device(slcs_ctx* ctx, const slcs_image* img, void* dev, size_t bytes) {
+  return guard([&] {
+    LOCKED(ctx);
+    download(ctx, img, dev, bytes, true);
+  });
+}
+
+int slcs_image_retain(slcs_image* img) {
+  return guard([&] {
+    need_img(img);
+    img->refs.fetch_add(1);
+  });
+}
+
+int slcs_image_release(slcs_image* img) {
+  return guard([&] {
+    if (!img) return;
+    std::lock_guard<std::mutex> lock(img->ctx->mu);
+    drop_image(img);
+  });
+}
+
+int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch) {
+  return guard([&] {
+    need_img(img);
+    if (kind) *kind = img->kind;
+    if (w) *w = img->geo.w;
+    if (h) *h = img->geo.h;
+    if (batch) *batch = img->geo.batch;
+  });
+}
+
+int slcs_image_storage(const slcs_image* img, void** dev, size_t* row_pitch_bytes,
+                       size_t* slice_bytes) {
+  return guard([&] {
+    need_img(img);
+    size_t u = unit_bytes(img->kind);
+    if (dev) *dev = img->data;
+    if (row_pitch_bytes) *row_pitch_bytes = img->geo.pitch * u;
+    if (slice_bytes) *slice_bytes = img->geo.slice * u;
+  });
+}
+
+#define PRIM(body)                               \
+  return guard([&] {                             \
+    LOCKED(ctx);                                 \
+    if (!out) fail(SLCS_ERR_ARG, "null output"); \
+    body;                                        \
+  })
+
+int slcs_threshold(slcs_ctx* ctx, slcs_cmp op, const slcs_image* img, double n,
+                   slcs_image** out) {
+  PRIM(*out = op_threshold(ctx, op, img, n));
+}
+int slcs_not(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) { PRIM(*out = op_not(ctx, a)); }
+int slcs_and(slcs_ctx* ctx, const slcs_image* a, const slcs_image* b, slcs_image** out) {
+  PRIM(*out = op_binary(ctx, a, b, true));
+}
+int slcs_or(slcs_ctx* ctx, const slcs_image* a, const slcs_image* b, slcs_image** out) {
+  PRIM(*out = op_binary(ctx, a, b, false));
+}
+int slcs_near(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) {
+  PRIM(*out = op_near(ctx, a, 1, false));
+}
+int slcs_near_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out) {
+  PRIM(*out = op_near(ctx, a, k, false));
+}
+int slcs_interior(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) {
+  PRIM(*out = op_near(ctx, a, 1, true));
+}
+int slcs_interior_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out) {
+  PRIM(*out = op_near(ctx, a, k, true));
+}
+int slcs_volume(slcs_ctx* ctx, const slcs_image* a, int64_t* out) {
+  PRIM(op_volume(ctx, a, out));
+}
+int slcs_ccl(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) { PRIM(*out = op_ccl(ctx, a)); }
+int slcs_reach(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+               slcs_image** out) {
+  PRIM(*out = op_reach(ctx, target, through));
+}
+int slcs_maxvol(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) {
+  PRIM(*out = op_maxvol(ctx, a));
+}
+
+// ---- host-in / host-out wrappers ------------------------------------------------
+}  // extern "C"
+
+namespace {
+template <class F>
+int host_unary(slcs_ctx* ctx, int kind, const void* a, int w, int h, void* out, size_t out_bytes,
+               F&& op) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    Ref ia(upload(ctx, kind, w, h, 1, a, false));
+    Ref r(op(ia.p));
+    download(ctx, r.p, out, out_bytes, false);
+  });
+}
+template <class F>
+int host_binary(slcs_ctx* ctx, const void* a, const void* b, int w, int h, void* out, F&& op) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    Ref ia(upload(ctx, SLCS_BOOL, w, h, 1, a, false));
+    Ref ib(upload(ctx, SLCS_BOOL, w, h, 1, b, false));
+    Ref r(op(ia.p, ib.p));
+    download(ctx, r.p, out, size_t(w) * size_t(h), false);
+  });
+}
+}  // namespace
+
+extern "C" {
+
+int slcs_h_threshold(slcs_ctx* ctx, slcs_cmp op, const uint16_t* img, int w, int h, double n,
+                     uint8_t* out) {
+  return host_unary(ctx, SLCS_U16, img, w, h, out, size_t(w) * size_t(h),
+                    [&](slcs_image* a) { return op_threshold(ctx, op, a, n); });
+}
+int slcs_h_not(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint8_t* out) {
+  return host_unary(ctx, SLCS_BOOL, a, w, h, out, size_t(w) * size_t(h),
+                    [&](slcs_image* x) { return op_not(ctx, x); });
+}
+int slcs_h_and(slcs_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, uint8_t* out) {
+  return host_binary(ctx, a, b, w, h, out,
+                     [&](slcs_image* x, slcs_image* y) { return op_binary(ctx, x, y, true); });
+}
+int slcs_h_or(slcs_ctx* ctx, const uint8_t* a, const uint8_t* b, int w, int h, uint8_t* out) {
+  return host_binary(ctx, a, b, w, h, out,
+                     [&](slcs_image* x, slcs_image* y) { return op_binary(ctx, x, y, false); });
+}
+int slcs_h_dilate(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint8_t* out) {
+  return host_unary(ctx, SLCS_BOOL, a, w, h, out, size_t(w) * size_t(h),
+                    [&](slcs_image* x) { return op_near(ctx, x, 1, false); });
+}
+int slcs_h_count_true(slcs_ctx* ctx, const uint8_t* a, int w, int h, int64_t* out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    Ref ia(upload(ctx, SLCS_BOOL, w, h, 1, a, false));
+    op_volume(ctx, ia.p, out);
+  });
+}
+int slcs_h_ccl_label(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint32_t* out) {
+  return host_unary(ctx, SLCS_BOOL, a, w, h, out, size_t(w) * size_t(h) * 4,
+                    [&](slcs_image* x) { return op_ccl(ctx, x); });
+}
+int slcs_h_reach(slcs_ctx* ctx, const uint8_t* target, const uint8_t* through, int w, int h,
+                 uint8_t* out) {
+  return host_binary(ctx, target, through, w, h, out,
+                     [&](slcs_image* x, slcs_image* y) { return op_reach(ctx, x, y); });
+}
+
+}  // extern "C"

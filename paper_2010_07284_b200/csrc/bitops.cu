@@ -1,0 +1,427 @@
+// bitops.cu -- bit-packed Bool primitives for sm_100a.
+//
+// Every primitive here is HBM-bound integer work (no tensor cores): the
+// kernels move 32 pixels per uint32 word, use 16 B vector accesses where the
+// row layout allows, and keep the zero-padding invariant of slcs_internal.h.
+//
+//   threshold  kernels.cpp:75-97   u16 -> bits, integer interval compare
+//   ! & |      kernels.cpp:36-73   word NOT/AND/OR (uint4)
+//   near       kernels.cpp:99-124  funnel-shift 3x3 (k-fold: (2k+1)^2) OR
+//   interior   stdlib.imgql:5      same stencil with AND, out-of-image = 1
+//   volume     kernels.cpp:126-136 popcount + warp/block reduce + 1 atomic
+#include "slcs_internal.h"
+
+namespace slcs {
+
+Geo bool_geo(int w, int h, int batch) {
+  Geo g;
+  g.w = w;
+  g.h = h;
+  g.batch = batch;
+  g.wpr = (w + 31) / 32;
+  g.pitch = round_up(size_t(g.wpr), 4);
+  g.slice = g.pitch * size_t(h);
+  int rem = w % 32;
+  g.lastmask = rem ? ((1u << rem) - 1u) : 0xffffffffu;
+  return g;
+}
+
+Geo u16_geo(int w, int h, int batch) {
+  Geo g;
+  g.w = w;
+  g.h = h;
+  g.batch = batch;
+  g.wpr = (w + 31) / 32;
+  g.pitch = round_up(size_t(w), 32);
+  g.slice = g.pitch * size_t(h);
+  return g;
+}
+
+Geo label_geo(int w, int h, int batch) {
+  Geo g;
+  g.w = w;
+  g.h = h;
+  g.batch = batch;
+  g.wpr = (w + 31) / 32;
+  g.pitch = size_t(w);
+  g.slice = g.pitch * size_t(h);
+  return g;
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(size_t n, int threads, int cap = 148 * 16) {
+  size_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > size_t(cap)) b = cap;
+  return int(b);
+}
+
+__device__ __forceinline__ uint32_t valid_mask(int j, int wpr, uint32_t lastmask) {
+  return j < wpr - 1 ? 0xffffffffu : (j == wpr - 1 ? lastmask : 0u);
+}
+
+// dense bytes (reference Bool / U16-as-mask layout) -> bit-packed rows
+__global__ void k_pack_u8(const uint8_t* __restrict__ dense, uint32_t* __restrict__ bits, int w,
+                          int h, int wpr, size_t pitch, size_t nwords_total) {
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
+       q += size_t(gridDim.x) * blockDim.x) {
+    size_t row = q / pitch;  // global row over the batch
+    int j = int(q - row * pitch);
+    uint32_t word = 0;
+    if (j < wpr) {
+      const uint8_t* src = dense + row * size_t(w) + size_t(j) * 32;
+      int n = min(32, w - j * 32);
+      for (int b = 0; b < n; ++b) word |= (src[b] != 0 ? 1u : 0u) << b;
+    }
+    bits[q] = word;
+  }
+}
+
+__global__ void k_pack_u16(const uint16_t* __restrict__ dense, uint32_t* __restrict__ bits, int w,
+                           int wpr, size_t pitch, size_t nwords_total) {
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
+       q += size_t(gridDim.x) * blockDim.x) {
+    size_t row = q / pitch;
+    int j = int(q - row * pitch);
+    uint32_t word = 0;
+    if (j < wpr) {
+      const uint16_t* src = dense + row * size_t(w) + size_t(j) * 32;
+      int n = min(32, w - j * 32);
+      for (int b = 0; b < n; ++b) word |= (src[b] != 0 ? 1u : 0u) << b;
+    }
+    bits[q] = word;
+  }
+}
+
+// bits -> dense bytes: one thread per output byte group of 4 pixels
+__global__ void k_unpack(const uint32_t* __restrict__ bits, uint8_t* __restrict__ dense, int w,
+                         size_t pitch, size_t npix_total) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < npix_total;
+       i += size_t(gridDim.x) * blockDim.x) {
+    size_t row = i / size_t(w);
+    int c = int(i - row * size_t(w));
+    uint32_t word = __ldg(bits + row * pitch + (c >> 5));
+    dense[i] = uint8_t((word >> (c & 31)) & 1u);
+  }
+}
+
+// threshold: one thread per output word; 4 x 16 B loads of u16 pixels.
+__global__ void k_threshold(const uint16_t* __restrict__ px, uint32_t* __restrict__ bits,
+                            int wpr, uint32_t lastmask, size_t bpitch, size_t upitch,
+                            size_t nwords_total, int lo, int hi) {
+  const unsigned span = unsigned(hi - lo);  // valid only when lo <= hi
+  const bool empty = lo > hi;
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
+       q += size_t(gridDim.x) * blockDim.x) {
+    size_t row = q / bpitch;
+    int j = int(q - row * bpitch);
+    uint32_t word = 0;
+    if (j < wpr && !empty) {
+      const uint4* src = reinterpret_cast<const uint4*>(px + row * upitch + size_t(j) * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 x = __ldg(src + v);
+        uint32_t comp[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          unsigned p0 = comp[e] & 0xffffu, p1 = comp[e] >> 16;
+          word |= (unsigned(p0 - unsigned(lo)) <= span ? 1u : 0u) << (v * 8 + e * 2);
+          word |= (unsigned(p1 - unsigned(lo)) <= span ? 1u : 0u) << (v * 8 + e * 2 + 1);
+        }
+      }
+      word &= valid_mask(j, wpr, lastmask);
+    }
+    bits[q] = word;
+  }
+}
+
+__device__ __forceinline__ void interval_of(int op, double n, int& lo, int& hi) {
+  // Appendix A #5 of SURVEY.md: double(p) op n on integer p in [0, 65535]
+  double l = 0.0, u = 65535.0;
+  if (n != n) {
+    lo = 1;
+    hi = 0;
+    return;
+  }
+  switch (op) {
+    case SLCS_GT: l = floor(n) + 1.0; break;
+    case SLCS_GE: l = ceil(n); break;
+    case SLCS_LT: u = ceil(n) - 1.0; break;
+    case SLCS_LE: u = floor(n); break;
+    default:
+      if (floor(n) != n) {
+        lo = 1;
+        hi = 0;
+        return;
+      }
+      l = u = n;
+  }
+  if (l < 0.0) l = 0.0;
+  if (u > 65535.0) u = 65535.0;
+  if (l > u) {
+    lo = 1;
+    hi = 0;
+    return;
+  }
+  lo = int(l);
+  hi = int(u);
+}
+
+__global__ void k_threshold_dev(const uint16_t* __restrict__ px, uint32_t* __restrict__ bits,
+                                int wpr, uint32_t lastmask, size_t bpitch, size_t upitch,
+                                size_t nwords_total, int op, const double* n_dev) {
+  int lo, hi;
+  interval_of(op, *n_dev, lo, hi);
+  const unsigned span = unsigned(hi - lo);
+  const bool empty = lo > hi;
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
+       q += size_t(gridDim.x) * blockDim.x) {
+    size_t row = q / bpitch;
+    int j = int(q - row * bpitch);
+    uint32_t word = 0;
+    if (j < wpr && !empty) {
+      const uint16_t* src = px + row * upitch + size_t(j) * 32;
+      for (int b = 0; b < 32; ++b) word |= (unsigned(src[b] - unsigned(lo)) <= span ? 1u : 0u) << b;
+      word &= valid_mask(j, wpr, lastmask);
+    }
+    bits[q] = word;
+  }
+}
+
+// NOT over uint4 groups; the row pitch is a multiple of 4 words.
+__global__ void k_not(const uint4* __restrict__ a, uint4* __restrict__ out, int wpr,
+                      uint32_t lastmask, size_t pitch4, size_t n4) {
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+       q += size_t(gridDim.x) * blockDim.x) {
+    size_t row = q / pitch4;
+    int j0 = int(q - row * pitch4) * 4;
+    uint4 x = a[q];
+    x.x = ~x.x & valid_mask(j0 + 0, wpr, lastmask);
+    x.y = ~x.y & valid_mask(j0 + 1, wpr, lastmask);
+    x.z = ~x.z & valid_mask(j0 + 2, wpr, lastmask);
+    x.w = ~x.w & valid_mask(j0 + 3, wpr, lastmask);
+    out[q] = x;
+  }
+}
+
+template <int OP>
+__global__ void k_binop(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                        uint4* __restrict__ out, size_t n4) {
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+       q += size_t(gridDim.x) * blockDim.x) {
+    uint4 x = a[q], y = b[q];
+    if (OP == 0) {
+      x.x &= y.x; x.y &= y.y; x.z &= y.z; x.w &= y.w;
+    } else {
+      x.x |= y.x; x.y |= y.y; x.z |= y.z; x.w |= y.w;
+    }
+    out[q] = x;
+  }
+}
+
+// k-fold near / interior.  Thread = (word column j, strip of rows).  Each row
+// is first dilated (eroded) horizontally with funnel shifts across the
+// neighbouring words, then a (2K+1)-row window is OR-ed (AND-ed) vertically
+// from a register ring.  Rows/columns outside the image are absent: 0 for
+// dilation (kernels.cpp:106-121), 1 for erosion (interior(all) = all,
+// tests/test_reach.cpp:120).
+template <int K, bool ERODE>
+__global__ void k_near(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h,
+                       int wpr, uint32_t lastmask, size_t pitch, size_t slice, int strip) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s_idx = blockIdx.y * blockDim.y + threadIdx.y;
+  const int r0 = s_idx * strip;
+  if (j >= int(pitch) || r0 >= h) return;
+  const uint32_t* src = in + size_t(blockIdx.z) * slice;
+  uint32_t* dst = out + size_t(blockIdx.z) * slice;
+  const int r1 = min(h, r0 + strip);
+  if (j >= wpr) {
+    for (int r = r0; r < r1; ++r) dst[size_t(r) * pitch + j] = 0u;
+    return;
+  }
+  const uint32_t vmask = j == wpr - 1 ? lastmask : 0xffffffffu;
+  const uint32_t ident = ERODE ? 0xffffffffu : 0u;
+  // For erosion, padding bits of the current and right word act as 1.
+  const uint32_t padC = ERODE ? ~vmask : 0u;
+  const uint32_t padR = ERODE ? (j + 1 == wpr - 1 ? ~lastmask : 0u) : 0u;
+
+  auto hrow = [&](int r) -> uint32_t {
+    if (r < 0 || r >= h) return ident;
+    const uint32_t* row = src + size_t(r) * pitch;
+    uint32_t C = __ldg(row + j) | padC;
+    uint32_t L = j > 0 ? __ldg(row + j - 1) : ident;
+    uint32_t R = j + 1 < wpr ? (__ldg(row + j + 1) | padR) : ident;
+    uint32_t acc = C;
+#pragma unroll
+    for (int d = 1; d <= K; ++d) {
+      uint32_t lft = __funnelshift_l(L, C, d);
+      uint32_t rgt = __funnelshift_r(C, R, d);
+      acc = ERODE ? (acc & lft & rgt) : (acc | lft | rgt);
+    }
+    return acc;
+  };
+
+  uint32_t win[2 * K + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * K; ++i) win[i] = hrow(r0 - K + i);
+  for (int r = r0; r < r1; ++r) {
+    win[2 * K] = hrow(r + K);
+    uint32_t acc = win[0];
+#pragma unroll
+    for (int i = 1; i <= 2 * K; ++i) acc = ERODE ? (acc & win[i]) : (acc | win[i]);
+    dst[size_t(r) * pitch + j] = acc & vmask;
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i) win[i] = win[i + 1];
+  }
+}
+
+template <int K, bool ERODE>
+void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
+  int bx = 32;
+  while (bx > 1 && size_t(bx / 2) >= g.pitch) bx /= 2;
+  int by = 256 / bx;
+  const int strip = 32;
+  int strips = (g.h + strip - 1) / strip;
+  dim3 block(bx, by);
+  dim3 grid(unsigned((g.pitch + bx - 1) / bx), unsigned((strips + by - 1) / by),
+            unsigned(g.batch));
+  k_near<K, ERODE><<<grid, block, 0, st>>>(a, out, g.h, g.wpr, g.lastmask, g.pitch, g.slice,
+                                           strip);
+}
+
+template <bool ERODE>
+void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaStream_t st) {
+  switch (k) {
+    case 1: near_launch<1, ERODE>(a, out, g, st); break;
+    case 2: near_launch<2, ERODE>(a, out, g, st); break;
+    case 3: near_launch<3, ERODE>(a, out, g, st); break;
+    case 4: near_launch<4, ERODE>(a, out, g, st); break;
+    case 5: near_launch<5, ERODE>(a, out, g, st); break;
+    case 6: near_launch<6, ERODE>(a, out, g, st); break;
+    case 7: near_launch<7, ERODE>(a, out, g, st); break;
+    case 8: near_launch<8, ERODE>(a, out, g, st); break;
+    default: fail(SLCS_ERR_ARG, "near: k out of range");
+  }
+}
+
+__global__ void k_volume(const uint4* __restrict__ a, size_t slice4,
+                         unsigned long long* __restrict__ counts) {
+  const uint4* src = a + size_t(blockIdx.y) * slice4;
+  unsigned long long local = 0;
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < slice4;
+       q += size_t(gridDim.x) * blockDim.x) {
+    uint4 x = src[q];
+    local += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  __shared__ unsigned long long part[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) part[wid] = local;
+  __syncthreads();
+  if (wid == 0) {
+    local = lane < int(blockDim.x >> 5) ? part[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if (lane == 0 && local) atomicAdd(counts + blockIdx.y, local);
+  }
+}
+
+__global__ void k_counts_to_double(const unsigned long long* c, double* out, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = double(c[i]);
+}
+
+}  // namespace
+
+int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool, cudaStream_t st) {
+  size_t n = g.slice * size_t(g.batch);
+  k_pack_u8<<<grid_for(n, kThreads), kThreads, 0, st>>>(dense, bits, g.w, g.h, g.wpr, g.pitch,
+                                                        n);
+  return 1;
+}
+
+int launch_pack_u16_mask(const uint16_t* dense, uint32_t* bits, const Geo& g, cudaStream_t st) {
+  size_t n = g.slice * size_t(g.batch);
+  k_pack_u16<<<grid_for(n, kThreads), kThreads, 0, st>>>(dense, bits, g.w, g.wpr, g.pitch, n);
+  return 1;
+}
+
+int launch_unpack(const uint32_t* bits, uint8_t* dense, const Geo& g, cudaStream_t st) {
+  size_t n = size_t(g.w) * size_t(g.h) * size_t(g.batch);
+  k_unpack<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(bits, dense, g.w, g.pitch, n);
+  return 1;
+}
+
+int launch_threshold(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb, int lo,
+                     int hi, cudaStream_t st) {
+  size_t n = gb.slice * size_t(gb.batch);
+  k_threshold<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(
+      px, bits, gb.wpr, gb.lastmask, gb.pitch, gu.pitch, n, lo, hi);
+  return 1;
+}
+
+int launch_threshold_dev(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb,
+                         int op, const double* n_dev, cudaStream_t st) {
+  size_t n = gb.slice * size_t(gb.batch);
+  k_threshold_dev<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(
+      px, bits, gb.wpr, gb.lastmask, gb.pitch, gu.pitch, n, op, n_dev);
+  return 1;
+}
+
+int launch_not(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
+  size_t n4 = g.slice * size_t(g.batch) / 4;
+  k_not<<<grid_for(n4, kThreads, 148 * 32), kThreads, 0, st>>>(
+      reinterpret_cast<const uint4*>(a), reinterpret_cast<uint4*>(out), g.wpr, g.lastmask,
+      g.pitch / 4, n4);
+  return 1;
+}
+
+int launch_and(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
+               cudaStream_t st) {
+  size_t n4 = g.slice * size_t(g.batch) / 4;
+  k_binop<0><<<grid_for(n4, kThreads, 148 * 32), kThreads, 0, st>>>(
+      reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
+      reinterpret_cast<uint4*>(out), n4);
+  return 1;
+}
+
+int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
+              cudaStream_t st) {
+  size_t n4 = g.slice * size_t(g.batch) / 4;
+  k_binop<1><<<grid_for(n4, kThreads, 148 * 32), kThreads, 0, st>>>(
+      reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
+      reinterpret_cast<uint4*>(out), n4);
+  return 1;
+}
+
+int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
+                cudaStream_t st) {
+  if (k < 1 || k > 8) fail(SLCS_ERR_ARG, "near: k must be in 1..8 per launch");
+  if (erode)
+    near_dispatch<true>(a, out, g, k, st);
+  else
+    near_dispatch<false>(a, out, g, k, st);
+  return 1;
+}
+
+int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * size_t(g.batch), st);
+  size_t n4 = g.slice / 4;
+  int gx = grid_for(n4, kThreads, 148 * 8);
+  if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 8 + g.batch - 1) / g.batch));
+  dim3 grid(unsigned(gx), unsigned(g.batch));
+  k_volume<<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint4*>(a), n4, counts);
+  return 1;
+}
+
+int launch_counts_to_double(const unsigned long long* counts, double* out, int n,
+                            cudaStream_t st) {
+  k_counts_to_double<<<(n + 255) / 256, 256, 0, st>>>(counts, out, n);
+  return 1;
+}
+
+}  // namespace slcs

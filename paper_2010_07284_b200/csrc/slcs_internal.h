@@ -1,0 +1,166 @@
+// slcs_internal.h -- shared declarations of the sm_100a primitive library.
+//
+// Device data layout:
+//   Bool  : bit-packed, 32 px per uint32 word, bit b of word j of row r is
+//           pixel (r, 32j+b) (LSB = lowest column).  Row pitch P words,
+//           P = round_up(ceil(W/32), 4) so every row starts 16 B aligned and
+//           uint4 accesses never straddle rows.  Padding bits (cols >= W) and
+//           padding words are ZERO -- every kernel preserves this invariant.
+//   U16   : row pitch round_up(W, 32) pixels, so a 32-px word maps to 64
+//           aligned bytes (4 x uint4).  Padding pixels are don't-care.
+//   Label : dense uint32, pitch W (the reference layout, image.hpp:20-29).
+//   Batch : `batch` slices of identical shape, slice stride = P*H units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/slcs.h"
+
+namespace slcs {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation)
+    fail(SLCS_ERR_OOM, std::string("device allocation failed in ") + what);
+  fail(SLCS_ERR_CUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+// Row geometry of one image kind.
+struct Geo {
+  int w = 0, h = 0, batch = 1;
+  int wpr = 0;        // Bool: valid words per row = ceil(w/32)
+  size_t pitch = 0;   // row pitch in storage units (words / u16 / u32)
+  size_t slice = 0;   // units per slice = pitch * h
+  uint32_t lastmask = 0;  // Bool: valid-bit mask of word wpr-1
+};
+
+Geo bool_geo(int w, int h, int batch);
+Geo u16_geo(int w, int h, int batch);
+Geo label_geo(int w, int h, int batch);
+
+// Packed CCL keys: a pixel (r, c) is keyed (r << s) | c with s = bits(W-1),
+// which preserves the reference's row-first lexicographic order
+// (image.hpp:20-29) while making key -> 2x2 block a pair of shifts.
+struct KeyGeo {
+  int s = 1;
+  uint32_t cmask = 1;
+  int bw = 0, bh = 0;      // 2x2 block grid
+  size_t slice_blocks = 0;
+};
+KeyGeo key_geo(int w, int h);
+
+// ---- kernel launchers (stream-ordered, no sync) ----------------------------
+// All return the number of kernel launches issued.
+int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool nonzero_is_true,
+                   cudaStream_t st);
+int launch_unpack(const uint32_t* bits, uint8_t* dense, const Geo& g, cudaStream_t st);
+// interval threshold: bit = lo <= p <= hi (empty interval when lo > hi)
+int launch_threshold(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb, int lo,
+                     int hi, cudaStream_t st);
+// device-scalar threshold: comparand read from *n_dev (a double) on device
+int launch_threshold_dev(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb,
+                         int op, const double* n_dev, cudaStream_t st);
+int launch_not(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st);
+int launch_and(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
+               cudaStream_t st);
+int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
+              cudaStream_t st);
+// k-fold near (dilate) or interior (erode), 1 <= k <= 31 per launch
+int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
+                cudaStream_t st);
+int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, cudaStream_t st);
+// counts (u64 per slice) -> doubles (for device-side number values)
+int launch_counts_to_double(const unsigned long long* counts, double* out, int n,
+                            cudaStream_t st);
+
+// Fused elementwise program over bit-packed words (see fused.cu).
+struct FusedOp {
+  uint8_t op;    // FOP_*
+  uint8_t dst;   // register
+  uint8_t a, b;  // registers / input index
+  int32_t lo, hi;
+};
+enum : uint8_t {
+  FOP_LOADB = 0,   // r[dst] = bool input a
+  FOP_THRESH = 1,  // r[dst] = (lo <= u16 input a <= hi)
+  FOP_NOT = 2,
+  FOP_AND = 3,
+  FOP_OR = 4,
+  FOP_ANDNOT = 5,  // r[a] & ~r[b]
+  FOP_STORE = 6,   // output a = r[dst]
+};
+constexpr int kFusedMaxOps = 24;
+constexpr int kFusedMaxIn = 8;
+constexpr int kFusedMaxOut = 4;
+constexpr int kFusedRegs = 8;
+struct FusedProgram {
+  int n_ops = 0;
+  FusedOp ops[kFusedMaxOps];
+  const uint32_t* bin[kFusedMaxIn];
+  const uint16_t* uin[kFusedMaxIn];
+  uint32_t* out[kFusedMaxOut];
+};
+int launch_fused(const FusedProgram& p, const Geo& gb, const Geo& gu, cudaStream_t st);
+
+// ---- connected components (ccl.cu) -------------------------------------------
+struct CclScratch {
+  uint32_t* parent = nullptr;  // per 2x2 block, packed key + 1 (0 = empty)
+  uint8_t* flag = nullptr;     // per block
+  uint32_t* size = nullptr;    // per block (maxvol)
+  unsigned int* maxv = nullptr;  // per slice (maxvol)
+};
+size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes);
+void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool sizes,
+                       CclScratch* s);
+bool ccl_small_path(int w, int h);
+int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,
+               cudaStream_t st);
+int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
+                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st);
+int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
+                  cudaStream_t st);
+
+}  // namespace slcs
+
+// ---- opaque handle definitions -------------------------------------------------
+
+struct slcs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 0;
+  std::mutex mu;
+  std::atomic<int64_t> launches{0};
+  // small pinned/device scratch for reductions
+  unsigned long long* d_counts = nullptr;
+  unsigned long long* h_counts = nullptr;
+  int counts_cap = 0;
+
+  void* alloc(size_t bytes);
+  void release(void* p);
+};
+
+struct slcs_image {
+  std::atomic<int> refs{1};
+  slcs_ctx* ctx = nullptr;
+  int kind = SLCS_BOOL;
+  slcs::Geo geo;
+  void* data = nullptr;
+  size_t bytes = 0;
+};
