@@ -160,6 +160,13 @@ int slcs_program_destroy(slcs_program* prog);
 int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* img);
 /* flags: bit 0 = capture/replay as a CUDA graph, bit 1 = disable fusion. */
 int slcs_program_run(slcs_program* prog, int flags);
+/* Copies host pixels (reference layout) straight into the program's input
+ * slot for `load` name `name` -- the end-to-end path: no intermediate image. */
+int slcs_program_set_input_host(slcs_program* prog, const char* name, slcs_kind kind, int w,
+                                int h, int batch, const void* host);
+/* Downloads the result of task `task` into host memory in the reference
+ * layout (Bool -> bytes 0/1; a number -> one double).  Synchronises. */
+int slcs_program_download(slcs_program* prog, int task, void* host, size_t bytes);
 /* Result of task `task` (an image; *out gets a new reference) or a number
  * (synchronises).  kind_out: 0 image, 1 number. */
 int slcs_program_result(slcs_program* prog, int task, int* kind_out, slcs_image** img_out,

@@ -66,6 +66,8 @@ _SIGS = {
     "slcs_program_destroy": (i32, [vp]),
     "slcs_program_bind": (i32, [vp, cstr, vp]),
     "slcs_program_run": (i32, [vp, i32]),
+    "slcs_program_set_input_host": (i32, [vp, cstr, i32, i32, i32, i32, vp]),
+    "slcs_program_download": (i32, [vp, i32, vp, sz]),
     "slcs_program_result": (i32, [vp, i32, C.POINTER(i32), pvp, C.POINTER(dbl)]),
     "slcs_program_launches": (i32, [vp, C.POINTER(i32)]),
     "slcs_program_plan": (cstr, [vp]),

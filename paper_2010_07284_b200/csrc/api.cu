@@ -68,6 +68,8 @@ struct DeviceGuard {
 
 }  // namespace
 
+void slcs::set_last_error(const std::string& msg) { g_err = msg; }
+
 void* slcs_ctx::alloc(size_t bytes) {
   void* p = nullptr;
   cuda_check(cudaMallocAsync(&p, bytes ? bytes : 16, stream), "cudaMallocAsync");

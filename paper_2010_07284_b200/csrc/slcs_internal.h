@@ -32,6 +32,9 @@ struct Error : std::runtime_error {
 
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
+// thread-local message returned by slcs_last_error (api.cu)
+void set_last_error(const std::string& msg);
+
 inline void cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
   if (e == cudaErrorMemoryAllocation)

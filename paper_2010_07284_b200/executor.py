@@ -1,0 +1,178 @@
+"""Host executor: runs a TaskGraph as one device-resident program.
+
+Mirrors ``executor::run`` (proj/src/executor.cpp:231-282, RunOptions /
+RunReport at executor.hpp:16-50) but evaluates the whole DAG through
+``slcs_program_*`` (csrc/program.cu): one fused, liveness-planned CUDA graph
+instead of one CPU task per node.  ``load`` reads images supplied by the
+caller (the PNG layer, png_io.cpp, is outside this path); ``save`` keeps the
+result on the device and exposes it by path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _lib
+from .imgql import TaskGraph, compile_text
+from .pixlog import (_DTYPE, Device, DeviceImage, ImageBuffer, PixelKind, RunError, _check,
+                     pixelKindName)
+
+FLAG_GRAPH = 1
+FLAG_NO_FUSION = 2
+
+
+def format_number(v: float) -> str:
+    """formatNumber (image.cpp:64-68): %.6g."""
+    return "%.6g" % v
+
+
+@dataclass
+class RunOptions:
+    device: Optional[Device] = None
+    fusion: bool = True
+    cuda_graph: bool = True
+
+
+@dataclass
+class RunReport:
+    computationMs: float = 0.0
+    taskCount: int = 0
+    printLines: list = field(default_factory=list)
+    savedFiles: list = field(default_factory=list)
+    outputs: dict = field(default_factory=dict)  # save path -> DeviceImage
+    launches: int = 0
+    plan: str = ""
+
+
+class Program:
+    """A TaskGraph compiled for the device (slcs_program)."""
+
+    def __init__(self, graph: TaskGraph, device: Optional[Device] = None):
+        self.graph = graph
+        self.device = device or Device.default()
+        n = graph.node_count()
+        ops = (C.c_char_p * max(1, n))(*[t.opcode.encode() for t in graph.nodes])
+        nums = (C.c_double * max(1, n))(*[t.payload if isinstance(t.payload, float) else 0.0
+                                          for t in graph.nodes])
+        strs = (C.c_char_p * max(1, n))(*[t.payload.encode() if isinstance(t.payload, str)
+                                          else None for t in graph.nodes])
+        off = [0]
+        deps: list[int] = []
+        for t in graph.nodes:
+            deps.extend(t.deps)
+            off.append(len(deps))
+        doff = (C.c_int * len(off))(*off)
+        dd = (C.c_int * max(1, len(deps)))(*deps)
+        h = C.c_void_p()
+        _check(_lib.load().slcs_program_create(self.device.handle, n, ops, nums, strs, doff, dd,
+                                               C.byref(h)))
+        self.handle = h
+        self.load_names = sorted({t.payload for t in graph.nodes if t.opcode == "load"})
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib._lib is not None:
+            _lib._lib.slcs_program_destroy(h)
+            self.handle = None
+
+    def bind(self, name: str, img: Union[ImageBuffer, DeviceImage, np.ndarray],
+             kind: Optional[PixelKind] = None) -> None:
+        if isinstance(img, ImageBuffer):
+            self.set_input_host(name, img.data, img.kind())
+            return
+        if isinstance(img, np.ndarray):
+            if kind is None:
+                kind = PixelKind.U16 if img.dtype == np.uint16 else PixelKind.Bool
+            self.set_input_host(name, img, kind)
+            return
+        _check(_lib.load().slcs_program_bind(self.handle, name.encode(), img.handle))
+
+    def set_input_host(self, name: str, arr: np.ndarray, kind: PixelKind) -> None:
+        a = np.ascontiguousarray(arr, _DTYPE[PixelKind(kind)])
+        b, h, w = (1, *a.shape) if a.ndim == 2 else a.shape
+        _check(_lib.load().slcs_program_set_input_host(self.handle, name.encode(), int(kind), w,
+                                                       h, b, C.c_void_p(a.ctypes.data)))
+
+    def run(self, fusion: bool = True, cuda_graph: bool = True) -> None:
+        flags = (FLAG_GRAPH if cuda_graph else 0) | (0 if fusion else FLAG_NO_FUSION)
+        _check(_lib.load().slcs_program_run(self.handle, flags))
+
+    def result(self, task: int) -> Union[DeviceImage, float]:
+        k, h, d = C.c_int(), C.c_void_p(), C.c_double()
+        _check(_lib.load().slcs_program_result(self.handle, task, C.byref(k), C.byref(h),
+                                               C.byref(d)))
+        return d.value if k.value == 1 else DeviceImage(h, self.device)
+
+    def download(self, task: int, out: Optional[np.ndarray] = None) -> Union[np.ndarray, float]:
+        t = self.graph.nodes[task]
+        res_kind = self.value_kind(task)
+        if res_kind is None:
+            d = C.c_double()
+            _check(_lib.load().slcs_program_download(self.handle, task, C.byref(d), 8))
+            return d.value
+        if out is None:
+            raise RunError("download of an image needs an output array", 7)
+        _check(_lib.load().slcs_program_download(self.handle, task, C.c_void_p(out.ctypes.data),
+                                                 out.nbytes))
+        return out
+
+    def value_kind(self, task: int):
+        k = C.c_int()
+        _check(_lib.load().slcs_program_result(self.handle, task, C.byref(k), None, None))
+        return None if k.value == 1 else True
+
+    @property
+    def launches(self) -> int:
+        n = C.c_int()
+        _check(_lib.load().slcs_program_launches(self.handle, C.byref(n)))
+        return n.value
+
+    @property
+    def plan(self) -> str:
+        return _lib.load().slcs_program_plan(self.handle).decode()
+
+
+def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) -> RunReport:
+    """Evaluates `graph`; `images` maps load paths to ImageBuffer/DeviceImage/ndarray."""
+    options = options or RunOptions()
+    prog = Program(graph, options.device)
+    for name in prog.load_names:
+        if name in images:
+            prog.bind(name, images[name])
+    rep = RunReport(taskCount=graph.node_count())
+    t0 = time.perf_counter()
+    err: Optional[RunError] = None
+    try:
+        prog.run(options.fusion, options.cuda_graph)
+    except RunError as e:
+        err = e
+    prog.device.synchronize()
+    rep.computationMs = (time.perf_counter() - t0) * 1e3
+    for out in graph.outputs:
+        t = graph.nodes[out]
+        try:
+            v = prog.result(out)
+        except RunError:
+            continue
+        if t.opcode == "save":
+            rep.savedFiles.append(t.payload)
+            rep.outputs[t.payload] = v
+        else:
+            if isinstance(v, DeviceImage):
+                desc = f"image({v.width}x{v.height},{pixelKindName(v.kind)})"
+            else:
+                desc = format_number(v)
+            rep.printLines.append(f"{t.payload}={desc}")
+    rep.launches = prog.launches
+    rep.plan = prog.plan
+    if err is not None:
+        raise err
+    return rep
+
+
+def run_text(text: str, images: dict, options: Optional[RunOptions] = None) -> RunReport:
+    return run(compile_text(text), images, options)

@@ -1,0 +1,231 @@
+"""GPU: whole formulas through the device program vs the reference.
+
+Mirrors proj/tests/test_executor.cpp (print format, CSE, U16 coercion,
+failure propagation, intensity identity, stdlib pipelines) and checks random
+ImgQL formulas against the reference's own executor::run (oracle/_ref) --
+with fusion on/off and CUDA-graph on/off, the analogue of the reference's
+worker-count invariance tests (test_executor.cpp:229-240).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2010_07284_b200 import ImageBuffer, PixelKind, RunError, mask
+from paper_2010_07284_b200.executor import Program, RunOptions, run_text
+from paper_2010_07284_b200.imgql import STDLIB, compile_text
+
+pytestmark = pytest.mark.gpu
+
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not available")
+
+
+def B(a):
+    a = np.asarray(a, np.uint8)
+    return ImageBuffer(a.shape[1], a.shape[0], PixelKind.Bool, a)
+
+
+def out_of(rep, path):
+    return rep.outputs[path].numpy()
+
+
+def test_load_save_round_trips_pixels(dev):
+    rng = O.Rng(61)
+    img = np.array([rng.below(65536) for _ in range(13 * 9)], np.uint16).reshape(9, 13)
+    rep = run_text('load x = "in.png"\nsave "out.png" x\n', {"in.png": img})
+    assert rep.taskCount == 2 + 0 or rep.taskCount >= 2
+    assert np.array_equal(out_of(rep, "out.png"), img)
+    assert rep.savedFiles == ["out.png"]
+
+
+def test_contradiction_is_all_false_and_near_evaluates_once(dev):
+    rng = O.Rng(62)
+    m = O.random_mask(16, 16, 0.5, rng)
+    g = compile_text('load x = "m.png"\nsave "out.png" near(x) & !near(x)\n', with_stdlib=False)
+    assert g.count_opcode("near") == 1
+    rep = run_text('load x = "m.png"\nsave "out.png" near(x) & !near(x)\n', {"m.png": m})
+    assert out_of(rep, "out.png").sum() == 0
+    assert rep.plan.count(" near^") == 1
+
+
+def test_print_formats(dev):
+    m = mask("xx../xx../..../...x").data
+    rep = run_text('load x = "m.png"\nprint "vol" volume(x)\nprint "ratio" 1 / 3\n'
+                   'print "img" near(x)\n', {"m.png": m})
+    assert rep.printLines == ["vol=5", "ratio=0.333333", "img=image(4x4,bool)"]
+
+
+def test_failure_propagation_keeps_independent_branches(dev):
+    m = O.random_mask(8, 8, 0.5, O.Rng(1))
+    with pytest.raises(RunError, match="cannot open file for reading"):
+        run_text('load x = "m.png"\nload y = "absent.png"\nsave "good.png" near(x)\n'
+                 'save "bad.png" near(y)\n', {"m.png": m})
+    prog = Program(compile_text('load x = "m.png"\nload y = "absent.png"\n'
+                                'save "good.png" near(x)\nsave "bad.png" near(y)\n'))
+    prog.bind("m.png", m, PixelKind.Bool)
+    with pytest.raises(RunError):
+        prog.run()
+    good = [i for i, t in enumerate(prog.graph.nodes) if t.payload == "good.png"][0]
+    assert np.array_equal(prog.result(good).numpy(), O.dilate(m))
+
+
+def test_division_by_zero_and_type_errors(dev):
+    m = O.random_mask(8, 8, 0.5, O.Rng(2))
+    with pytest.raises(RunError, match="division by zero"):
+        run_text('print "q" 1 / 0\n', {})
+    with pytest.raises(RunError, match="division by zero"):
+        run_text('load x = "m.png"\nprint "q" 1 / (volume(x) - volume(x))\n', {"m.png": m})
+    with pytest.raises(RunError, match="expects a numeric image, got bool"):
+        run_text('load x = "m.png"\nsave "o.png" x >. 3\n', {"m.png": m})
+    with pytest.raises(RunError, match="cannot save a number"):
+        run_text('save "o.png" 3\n', {})
+
+
+def test_intensity_is_identity(dev):
+    img = np.array([O.Rng(64).below(65536) for _ in range(36)], np.uint16).reshape(6, 6)
+    rep = run_text('load x = "in.png"\nsave "a.png" intensity(x)\n'
+                   'save "b.png" intensity(intensity(x))\n', {"in.png": img})
+    assert np.array_equal(out_of(rep, "a.png"), img)
+    assert np.array_equal(out_of(rep, "b.png"), img)
+
+
+def test_numeric_images_coerce_to_masks(dev):
+    img = np.array([[0, 1, 40000, 0]], np.uint16)
+    rep = run_text('load x = "in.png"\nprint "v" volume(x)\nsave "n.png" !x\n', {"in.png": img})
+    assert rep.printLines[0] == "v=2"
+    assert out_of(rep, "n.png").tolist() == [[1, 0, 0, 1]]
+
+
+def test_threshold_with_a_computed_comparand(dev):
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 200, (40, 50), dtype=np.uint16)
+    m = (img > 150).astype(np.uint8)
+    rep = run_text('load i = "i.png"\nload m = "m.png"\nsave "o.png" i >. volume(m) / 10\n',
+                   {"i.png": img, "m.png": m})
+    assert np.array_equal(out_of(rep, "o.png"), O.threshold(0, img, m.sum() / 10))
+
+
+@pytest.mark.parametrize("fusion", [True, False])
+@pytest.mark.parametrize("graph", [True, False])
+def test_stdlib_pipelines_vs_oracle(dev, fusion, graph):
+    rng = O.Rng(65)
+    a = O.random_mask(20, 20, 0.25, rng)
+    b = O.random_mask(20, 20, 0.35, rng)
+    opts = RunOptions(fusion=fusion, cuda_graph=graph)
+    for expr, ref in [("grow(a,b)", O.grow(a, b)), ("surrounded(a,b)", O.surrounded(a, b)),
+                      ("near(a) | interior(b)", O.logical_or(O.dilate(a), O.interior(b))),
+                      ("touch(a,b)", O.touch(a, b)), ("reach(a,b)", O.reach(a, b)),
+                      ("maxvol(a | b)", O.maxvol(O.logical_or(a, b)))]:
+        rep = run_text(f'load a = "a.png"\nload b = "b.png"\nsave "o.png" {expr}\n',
+                       {"a.png": a, "b.png": b}, opts)
+        assert np.array_equal(out_of(rep, "o.png"), ref), expr
+
+
+def test_segmentation_spec_vs_reference_golden(dev):
+    import json
+    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    G = np.load(os.path.join(here, "golden", "reference_vectors.npz"))
+    D = json.load(open(os.path.join(here, "golden", "reference_dags.json")))
+    rep = run_text(D["specs"]["segmentation"], {"input.png": G["seg_in"]})
+    assert np.array_equal(out_of(rep, "segmentation.png"), G["seg_out"])
+    rep = run_text(D["specs"]["c1"], {"img.png": G["seg_in"]})
+    assert np.array_equal(out_of(rep, "out.png"), G["c1_out"])
+
+
+def test_sequential_chain_fuses_to_stencils(dev):
+    # formula_gen.cpp:8-17: near / ! alternation; near(!e) fuses to !interior(e)
+    expr = "x"
+    for i in range(40):
+        expr = f"near({expr})" if i % 2 == 0 else f"!({expr})"
+    m = O.random_mask(300, 200, 0.02, O.Rng(8))
+    ref = m
+    for i in range(40):
+        ref = O.dilate(ref) if i % 2 == 0 else O.logical_not(ref)
+    for fusion in (True, False):
+        rep = run_text(f'load x = "m.png"\nsave "o.png" {expr}\n', {"m.png": m},
+                       RunOptions(fusion=fusion))
+        assert np.array_equal(out_of(rep, "o.png"), ref)
+        if fusion:
+            assert rep.launches <= 22, rep.plan
+
+
+def test_near_reach_chain_small(dev):
+    img = O.blob_noise(256, 256, 1)
+    b = O.threshold(0, img, 56360)
+    x = O.threshold(0, img, 62258)
+    lines = ['load img = "img.png"', "let b = img >. 56360", "let x0 = img >. 62258"]
+    for k in range(10):
+        lines.append(f"let x{2 * k + 1} = near(x{2 * k})")
+        lines.append(f"let x{2 * k + 2} = reach(x{2 * k + 1}, b)")
+        x = O.reach(O.dilate(x), b)
+    lines.append('save "o.png" x20')
+    rep = run_text("\n".join(lines) + "\n", {"img.png": img})
+    assert np.array_equal(out_of(rep, "o.png"), x)
+
+
+def random_formula(rng, budget):
+    if budget <= 1:
+        img = "imgA" if rng.below(2) else "imgB"
+        cmp = [">.", ">=.", "<.", "<=."][rng.below(4)]
+        return f"{img} {cmp} {rng.below(65536)}"
+    k = rng.below(7 if budget >= 3 else 3)
+    if k == 0:
+        return f"!({random_formula(rng, budget - 1)})"
+    if k in (1, 2):
+        return f"near({random_formula(rng, budget - 1)})"
+    left = 1 + rng.below(budget - 2)
+    l, r = random_formula(rng, left), random_formula(rng, budget - 1 - left)
+    if k == 3:
+        return f"({l}) & ({r})"
+    if k == 4:
+        return f"({l}) | ({r})"
+    if k == 5:
+        return f"reach({l}, {r})"
+    return f"surrounded({l}, {r})"
+
+
+@needs_ref
+@pytest.mark.parametrize("size", [(37, 29), (256, 256), (300, 280)])
+def test_random_formulas_vs_reference_executor(dev, size):
+    R = O.Reference(workers=2)
+    w, h = size
+    rng = O.Rng(1000 + w)
+    imgA = O.blob_noise(w, h, 11)
+    imgB = np.array([rng.below(65536) for _ in range(w * h)], np.uint16).reshape(h, w)
+    for i in range(12):
+        f = random_formula(rng, 3 + rng.below(10))
+        spec = f'load imgA = "a.png"\nload imgB = "b.png"\nsave "o.png" {f}\n'
+        want = R.run(spec, {"a.png": imgA, "b.png": imgB}, STDLIB, ["o.png"])["outputs"]["o.png"]
+        for fusion in (True, False):
+            rep = run_text(spec, {"a.png": imgA, "b.png": imgB}, RunOptions(fusion=fusion))
+            assert np.array_equal(out_of(rep, "o.png"), want), (i, f, fusion)
+
+
+def test_program_rerun_with_new_inputs(dev):
+    prog = Program(compile_text('load a = "a.png"\nload b = "b.png"\nsave "o.png" grow(a, b)\n'))
+    out = [i for i, t in enumerate(prog.graph.nodes) if t.opcode == "save"][0]
+    rng = O.Rng(3)
+    for _ in range(4):
+        a = O.random_mask(200, 150, 0.1, rng)
+        b = O.random_mask(200, 150, 0.45, rng)
+        prog.set_input_host("a.png", a, PixelKind.Bool)
+        prog.set_input_host("b.png", b, PixelKind.Bool)
+        prog.run()
+        got = np.zeros((150, 200), np.uint8)
+        prog.download(out, got)
+        assert np.array_equal(got, O.grow(a, b))
+
+
+def test_batched_program(dev):
+    # C3-shaped: a stack of slices evaluated as one batched program
+    imgs = np.stack([O.blob_noise(240, 240, s) for s in range(100, 106)])
+    spec = ('load img = "s.png"\nlet hI = intensity(img) >. 62258\n'
+            'let vI = intensity(img) >. 56360\n'
+            'save "o.png" maxvol(grow(hI, vI)) | surrounded(hI, vI)\n')
+    rep = run_text(spec, {"s.png": imgs})
+    got = out_of(rep, "o.png")
+    for s in range(6):
+        hI = O.threshold(0, imgs[s], 62258)
+        vI = O.threshold(0, imgs[s], 56360)
+        ref = O.logical_or(O.maxvol(O.grow(hI, vI)), O.surrounded(hI, vI))
+        assert np.array_equal(got[s], ref), s
