@@ -283,7 +283,12 @@ void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st
   int bx = 32;
   while (bx > 1 && size_t(bx / 2) >= g.pitch) bx /= 2;
   int by = 256 / bx;
-  const int strip = 32;
+  // rows per thread: enough threads to fill every SM twice (148 x 2048),
+  // clamped to [4, 32] so the 2K halo rows stay a small overhead
+  size_t words = g.pitch * size_t(g.h) * size_t(g.batch);
+  int strip = int(words / (148ull * 2048ull));
+  strip = strip < 4 ? 4 : (strip > 32 ? 32 : strip);
+  if (strip < 2 * K) strip = 2 * K < 32 ? 2 * K : 32;
   int strips = (g.h + strip - 1) / strip;
   dim3 block(bx, by);
   dim3 grid(unsigned((g.pitch + bx - 1) / bx), unsigned((strips + by - 1) / by),

@@ -124,7 +124,20 @@ struct Tile {
     int dc = dr ? int((p >> 3) & 1u) : int((p >> 1) & 1u);
     return (uint32_t(2 * lbr + dr) << KW) | uint32_t(2 * lbc + dc);
   }
+  // find with path halving (plain stores are safe: parents only ever move to
+  // ancestors, and a racing atomicMax link is completed by the union loop)
   __device__ __forceinline__ uint32_t find(uint32_t k) const {
+    volatile uint32_t* vp = par;
+    for (;;) {
+      uint32_t p = vp[blk(k)];
+      if (p == k) return k;
+      uint32_t gp = vp[blk(p)];
+      if (gp == p) return p;
+      vp[blk(k)] = gp;
+      k = gp;
+    }
+  }
+  __device__ __forceinline__ uint32_t find_ro(uint32_t k) const {
     volatile uint32_t* vp = par;
     uint32_t q = vp[blk(k)];
     while (q != k) {
@@ -148,40 +161,89 @@ struct Tile {
       b = old;
     }
   }
-  // patterns must be in pat[]; builds par[] and flattens it (par[lb] = root key)
+  // True iff upper lanes lo..hi (any order) lie in one upper-row segment.
+  __device__ __forceinline__ static bool same_seg(int a, int b, uint32_t hcu) {
+    int lo = a < b ? a : b, hi = a < b ? b : a;
+    if (lo < 0 || hi > 31) return false;
+    if (lo == hi) return true;
+    uint32_t m = (hi == 31 ? 0xffffffffu : ((2u << hi) - 1u)) & ~((2u << lo) - 1u);
+    return (hcu & m) == m;
+  }
+  // Patterns must be in pat[].  Builds par[] and flattens it (par[lb] = root
+  // key).  Warp-per-32-block row span:
+  //  1. horizontal runs of connected blocks ("segments") are found with two
+  //     ballots and every block points straight at its segment's max key --
+  //     no atomics for horizontal adjacency;
+  //  2. only links to the row above (and across span boundaries) need
+  //     unions, and a link is skipped when the left neighbour in the same
+  //     segment already links into the same upper segment, so a solid region
+  //     costs one union per segment instead of three per block;
+  //  3. flatten.
   __device__ void solve() const {
-    const int nt = blockDim.x;
-    for (int lb = threadIdx.x; lb < nb; lb += nt) {
-      uint32_t p = pat[lb];
-      par[lb] = p ? key(lb, p) : 0xffffffffu;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int SPANS = TBW / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int items = (nb >> TBW_LOG) * SPANS;
+    for (int it = warp; it < items; it += nw) {
+      const int lbr = it / SPANS, lbc = (it % SPANS) * 32 + lane;
+      const int lb = (lbr << TBW_LOG) | lbc;
+      const uint32_t p = pat[lb];
+      const uint32_t pl = __shfl_up_sync(FULL, p, 1);
+      const uint32_t hc = __ballot_sync(FULL, lane > 0 && (p & (P00 | P10)) && (pl & (P01 | P11)));
+      const uint32_t le = lane == 31 ? FULL : ((2u << lane) - 1u);
+      const int s = 31 - __clz(~hc & le);
+      const int e = lane == 31 ? 31 : lane + __ffs(~(hc >> (lane + 1))) - 1;
+      const uint32_t segmask = (e == 31 ? FULL : ((2u << e) - 1u)) & ~((1u << s) - 1u);
+      const uint32_t bot = __ballot_sync(FULL, (p & (P10 | P11)) != 0);
+      const uint32_t cb = bot & segmask;
+      const int ml = cb ? 31 - __clz(cb) : e;
+      const uint32_t k = p ? key(lb, p) : 0u;
+      const uint32_t rk = __shfl_sync(FULL, k, ml);
+      par[lb] = p ? rk : 0xffffffffu;
     }
     __syncthreads();
-    for (int lb = threadIdx.x; lb < nb; lb += nt) {
-      uint32_t p = pat[lb];
-      if (!p) continue;
-      int lbr = lb >> TBW_LOG, lbc = lb & (TBW - 1);
-      uint32_t k = key(lb, p);
-      if (lbc > 0 && (p & (P00 | P10))) {
-        uint32_t q = pat[lb - 1];
-        if (q & (P01 | P11)) unite(k, key(lb - 1, q));
-      }
-      if (lbr > 0) {
-        uint32_t q = pat[lb - TBW];
-        if ((p & (P00 | P01)) && (q & (P10 | P11))) unite(k, key(lb - TBW, q));
-        if (lbc > 0 && (p & P00)) {
-          q = pat[lb - TBW - 1];
-          if (q & P11) unite(k, key(lb - TBW - 1, q));
+    for (int it = warp; it < items; it += nw) {
+      const int lbr = it / SPANS, lbc = (it % SPANS) * 32 + lane;
+      const int lb = (lbr << TBW_LOG) | lbc;
+      const uint32_t p = pat[lb];
+      const bool up = lbr > 0;
+      const uint32_t qu = up ? pat[lb - TBW] : 0u;
+      const uint32_t qul = (up && lbc > 0) ? pat[lb - TBW - 1] : 0u;
+      const uint32_t qur = (up && lbc < TBW - 1) ? pat[lb - TBW + 1] : 0u;
+      uint32_t tset = ((p & P00) && (qul & P11) ? 1u : 0u) |
+                      ((p & (P00 | P01)) && (qu & (P10 | P11)) ? 2u : 0u) |
+                      ((p & P01) && (qur & P10) ? 4u : 0u);
+      const uint32_t qleft = __shfl_up_sync(FULL, qu, 1);
+      const uint32_t hcu =
+          __ballot_sync(FULL, lane > 0 && (qu & (P00 | P10)) && (qleft & (P01 | P11)));
+      const uint32_t pl = __shfl_up_sync(FULL, p, 1);
+      const bool joined_left = lane > 0 && (p & (P00 | P10)) && (pl & (P01 | P11));
+      const uint32_t prev = __shfl_up_sync(FULL, tset, 1);
+      if (p) {
+        const uint32_t mine = par[lb];
+        if (lane == 0 && lbc > 0 && (p & (P00 | P10)) && (pat[lb - 1] & (P01 | P11)))
+          unite(mine, par[lb - 1]);
+        for (int t = 0; t < 3; ++t) {
+          if (!(tset & (1u << t))) continue;
+          const int j = lane - 1 + t;
+          bool covered = false;
+          if (joined_left)
+            for (int t2 = 0; t2 < 3; ++t2)
+              if ((prev & (1u << t2)) && same_seg(lane - 2 + t2, j, hcu)) covered = true;
+          if (!covered) unite(mine, par[lb - TBW - 1 + t]);
         }
-        if (lbc < TBW - 1 && (p & P01)) {
-          q = pat[lb - TBW + 1];
-          if (q & P10) unite(k, key(lb - TBW + 1, q));
-        }
       }
+      // reconverge: lanes leave their union loops at different times, and
+      // the block barrier below must not release a partially-arrived warp
+      __syncwarp();
     }
+    __syncwarp();
     __syncthreads();
-    for (int lb = threadIdx.x; lb < nb; lb += nt) {
+    // flatten with a READ-ONLY find: a halving write by another thread could
+    // otherwise overwrite a slot its owner has already set to the final root
+    for (int lb = threadIdx.x; lb < nb; lb += blockDim.x) {
       uint32_t p = pat[lb];
-      if (p) par[lb] = find(key(lb, p));
+      if (p) par[lb] = find_ro(par[lb]);
     }
     __syncthreads();
   }
@@ -194,24 +256,29 @@ __device__ __forceinline__ size_t gblk(const G& g, uint32_t v) {
   return size_t((k >> g.s) >> 1) * size_t(g.BW) + size_t((k & g.cmask) >> 1);
 }
 
-// find during concurrent unions: L2-coherent loads
-__device__ __forceinline__ uint32_t gfind_cg(const uint32_t* P, const G& g, uint32_t v) {
-  uint32_t q = __ldcg(P + gblk(g, v));
-  while (q != v) {
-    v = q;
-    q = __ldcg(P + gblk(g, v));
+// find during concurrent unions: L2-coherent loads, path halving
+__device__ __forceinline__ uint32_t gfind_cg(uint32_t* P, const G& g, uint32_t v) {
+  for (;;) {
+    uint32_t p = __ldcg(P + gblk(g, v));
+    if (p == v) return v;
+    uint32_t gp = __ldcg(P + gblk(g, p));
+    if (gp == p) return p;
+    __stcg(P + gblk(g, v), gp);
+    v = gp;
   }
-  return v;
 }
 
-// find after the union kernel completed
-__device__ __forceinline__ uint32_t gfind(const uint32_t* __restrict__ P, const G& g, uint32_t v) {
-  uint32_t q = P[gblk(g, v)];
-  while (q != v) {
-    v = q;
-    q = P[gblk(g, v)];
+// find after the union kernel completed (still halving: later finds of the
+// same component then take one or two hops)
+__device__ __forceinline__ uint32_t gfind(uint32_t* P, const G& g, uint32_t v) {
+  for (;;) {
+    uint32_t p = P[gblk(g, v)];
+    if (p == v) return v;
+    uint32_t gp = P[gblk(g, p)];
+    if (gp == p) return p;
+    P[gblk(g, v)] = gp;
+    v = gp;
   }
-  return v;
 }
 
 __device__ void gunite(uint32_t* P, const G& g, uint32_t a, uint32_t b) {
@@ -276,7 +343,7 @@ __device__ __forceinline__ void warp_store_patterns(uint32_t* __restrict__ out, 
 // ===========================================================================
 // Large-image path: 64x64-px tiles, 3-5 launches.
 constexpr int LT_LOG = 5;  // 32 blocks = 64 px wide
-constexpr int LT_H = 32;   // 32 block rows = 64 px high
+constexpr int LT_H = 64;   // 64 block rows = 128 px high
 constexpr int LT_N = (1 << LT_LOG) * LT_H;
 constexpr int LT_THREADS = 256;
 
@@ -382,11 +449,11 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
 }
 
 // labels: one thread per block, 2 rows x 2 px each
-__global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
+__global__ void k_tile_labels(const uint32_t* __restrict__ ubits, uint32_t* P,
                               uint32_t* __restrict__ L, G g) {
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
-  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
   uint32_t* Ls = L + size_t(slice) * size_t(g.W) * size_t(g.H);
   const bool even = (g.W & 1) == 0;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < g.sb;
@@ -417,9 +484,9 @@ __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t
 }
 
 // reach: flagged local roots raise the flag of their global root
-__global__ void k_reach_propagate(const uint32_t* __restrict__ P, uint8_t* F, G g) {
+__global__ void k_reach_propagate(uint32_t* P, uint8_t* F, G g) {
   const int slice = blockIdx.y;
-  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
   uint8_t* Fs = F + size_t(slice) * g.sb;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < g.sb;
        i += size_t(gridDim.x) * blockDim.x) {
@@ -433,11 +500,11 @@ __global__ void k_reach_propagate(const uint32_t* __restrict__ P, uint8_t* F, G 
 // Warp = 32 consecutive blocks of one block row; covers the full row pitch.
 __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
                                const uint32_t* __restrict__ tbits,
-                               const uint32_t* __restrict__ P, const uint8_t* __restrict__ F,
+                               uint32_t* P, const uint8_t* __restrict__ F,
                                uint32_t* __restrict__ out, G g) {
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
-  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint8_t* Fs = F + size_t(slice) * g.sb;
   const int wpb = int(g.pitch / 2);  // warps per block row (2 words per warp)
   const long long nw = (long long)g.BH * wpb;
@@ -457,11 +524,11 @@ __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
 }
 
 // maxvol: component sizes accumulated at the root block
-__global__ void k_maxvol_size(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
+__global__ void k_maxvol_size(const uint32_t* __restrict__ ubits, uint32_t* P,
                               uint32_t* SZ, G g) {
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
-  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
   uint32_t* Ss = SZ + size_t(slice) * g.sb;
   // grid-stride with whole warps alive for __match_any_sync
   const size_t n = g.sb;
@@ -485,10 +552,10 @@ __global__ void k_maxvol_size(const uint32_t* __restrict__ ubits, const uint32_t
   }
 }
 
-__global__ void k_maxvol_max(const uint32_t* __restrict__ P, const uint32_t* __restrict__ SZ,
+__global__ void k_maxvol_max(uint32_t* P, const uint32_t* __restrict__ SZ,
                              unsigned int* maxv, G g) {
   const int slice = blockIdx.y;
-  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t* Ss = SZ + size_t(slice) * g.sb;
   uint32_t best = 0;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < g.sb;
@@ -502,12 +569,12 @@ __global__ void k_maxvol_max(const uint32_t* __restrict__ P, const uint32_t* __r
 }
 
 __global__ void k_maxvol_select(const uint32_t* __restrict__ ubits,
-                                const uint32_t* __restrict__ P, const uint32_t* __restrict__ SZ,
+                                uint32_t* P, const uint32_t* __restrict__ SZ,
                                 const unsigned int* __restrict__ maxv, uint32_t* __restrict__ out,
                                 G g) {
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
-  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t* Ss = SZ + size_t(slice) * g.sb;
   const uint32_t mx = maxv[slice];
   const int wpb = int(g.pitch / 2);

@@ -143,3 +143,19 @@ def test_maxvol_ties_keep_all_maxima(dev):
     big[100:110, 200:210] = 1
     big[250, 250] = 1
     assert np.array_equal(maxvol(B(big)).data, O.maxvol(big))
+
+
+@pytest.mark.parametrize("w,h,n", [(256, 256, 60), (240, 240, 60), (600, 520, 25)])
+def test_race_stress_many_masks(dev, w, h, n):
+    """Union-find races show up as rare single-pixel errors: hammer them."""
+    rng = O.Rng(9000 + w)
+    for i in range(n):
+        d = 0.35 + 0.3 * rng.unit()
+        a = O.random_mask(w, h, d, rng)
+        t = O.random_mask(w, h, 0.01, rng)
+        da = DeviceImage.upload(a, PixelKind.Bool, dev)
+        assert np.array_equal(ccl.label(da).numpy(), O.flood_fill_label(a)), (i, d)
+        if i % 5 == 0:
+            from paper_2010_07284_b200 import reach
+            got = reach(DeviceImage.upload(t, PixelKind.Bool, dev), da).numpy()
+            assert np.array_equal(got, O.reach(t, a)), (i, d)
