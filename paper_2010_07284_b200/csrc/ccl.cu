@@ -239,11 +239,21 @@ struct Tile {
     }
     __syncwarp();
     __syncthreads();
-    // flatten with a READ-ONLY find: a halving write by another thread could
-    // otherwise overwrite a slot its owner has already set to the final root
-    for (int lb = threadIdx.x; lb < nb; lb += blockDim.x) {
-      uint32_t p = pat[lb];
-      if (p) par[lb] = find_ro(par[lb]);
+    // flatten: roots are found (with halving) into registers first and
+    // written only after a barrier -- a halving write by another thread must
+    // never overwrite a slot its owner already set to the final root
+    constexpr int MAXPER = 16;  // nb <= 16 * blockDim.x on both paths
+    uint32_t rr[MAXPER];
+#pragma unroll
+    for (int i = 0; i < MAXPER; ++i) {
+      const int lb = threadIdx.x + i * int(blockDim.x);
+      rr[i] = (lb < nb && pat[lb]) ? find(par[lb]) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MAXPER; ++i) {
+      const int lb = threadIdx.x + i * int(blockDim.x);
+      if (lb < nb && pat[lb]) par[lb] = rr[i];
     }
     __syncthreads();
   }
@@ -264,19 +274,6 @@ __device__ __forceinline__ uint32_t gfind_cg(uint32_t* P, const G& g, uint32_t v
     uint32_t gp = __ldcg(P + gblk(g, p));
     if (gp == p) return p;
     __stcg(P + gblk(g, v), gp);
-    v = gp;
-  }
-}
-
-// find after the union kernel completed (still halving: later finds of the
-// same component then take one or two hops)
-__device__ __forceinline__ uint32_t gfind(uint32_t* P, const G& g, uint32_t v) {
-  for (;;) {
-    uint32_t p = P[gblk(g, v)];
-    if (p == v) return v;
-    uint32_t gp = P[gblk(g, p)];
-    if (gp == p) return p;
-    P[gblk(g, v)] = gp;
     v = gp;
   }
 }
@@ -349,55 +346,142 @@ constexpr int LT_THREADS = 256;
 
 enum { MODE_CCL = 0, MODE_REACH = 1 };
 
+constexpr int LT_ROWS = 2 * LT_H;          // pixel rows per tile
+constexpr int LT_WORDS = LT_ROWS * 2;       // 2 words (64 px) per row
+constexpr int LT_LIST = 192;                // per-tile list: count + <= 188 ring roots
+
+// near(t) word (r, j) from global bits: 3x3 OR, out of image = 0
+__device__ __forceinline__ uint32_t near_word(const uint32_t* __restrict__ t, const G& g, int r,
+                                              int j) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int d = -1; d <= 1; ++d) {
+    int rr = r + d;
+    if (rr < 0 || rr >= g.H) continue;
+    const uint32_t* row = t + size_t(rr) * g.pitch;
+    uint32_t C = __ldg(row + j);
+    uint32_t L = j > 0 ? __ldg(row + j - 1) : 0u;
+    uint32_t R = j + 1 < g.wpr ? __ldg(row + j + 1) : 0u;
+    acc |= C | __funnelshift_l(L, C, 1) | __funnelshift_r(C, R, 1);
+  }
+  return acc;
+}
+
+// 2x2 pattern of block (lbr, lbc) from a staged 2-word-wide tile of rows
+__device__ __forceinline__ uint32_t staged_pattern(const uint32_t* w, int lbr, int lbc) {
+  const int jj = lbc >> 4, sh = (2 * lbc) & 31;
+  return ((w[(2 * lbr) * 2 + jj] >> sh) & 3u) | (((w[(2 * lbr + 1) * 2 + jj] >> sh) & 3u) << 2);
+}
+
+// Tile-local pass.  Writes, per block, P = local root key + 1 (0 = empty);
+// per local root, F = "holds a seed" (reach); and a per-tile list of the
+// local roots that touch the tile ring -- the only ones a border union can
+// link, so the only ones the root-flatten pass must visit.
 template <int MODE>
 __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __restrict__ ubits,
                                                            const uint32_t* __restrict__ tbits,
                                                            uint32_t* __restrict__ P,
-                                                           uint8_t* __restrict__ F, G g) {
+                                                           uint8_t* __restrict__ F,
+                                                           uint32_t* __restrict__ lists, G g) {
   __shared__ uint8_t pat[LT_N];
   __shared__ uint32_t par[LT_N];
+  __shared__ uint8_t touch[LT_N];
   __shared__ uint8_t fl[MODE == MODE_REACH ? LT_N : 1];
+  __shared__ uint32_t su[LT_WORDS];
+  __shared__ uint32_t snt[MODE == MODE_REACH ? LT_WORDS : 1];
+  __shared__ int s_cnt;
   using T = Tile<LT_LOG>;
   const int slice = blockIdx.z;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const int tbr0 = blockIdx.y * LT_H, tbc0 = blockIdx.x * T::TBW;
+  const int r0 = 2 * tbr0, c0 = 2 * tbc0, j0 = c0 >> 5;
+  // stage the tile's bit rows (and near(target) rows) in shared memory
+  for (int q = threadIdx.x; q < LT_WORDS; q += blockDim.x) {
+    const int r = r0 + (q >> 1), j = j0 + (q & 1);
+    const bool in = r < g.H && j < g.wpr;
+    su[q] = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
+    if (MODE == MODE_REACH)
+      snt[q] = in ? near_word(tbits + size_t(slice) * g.slice, g, r, j) : 0u;
+  }
   for (int lb = threadIdx.x; lb < LT_N; lb += blockDim.x) {
-    int br = tbr0 + (lb >> LT_LOG), bc = tbc0 + (lb & (T::TBW - 1));
-    pat[lb] = uint8_t(load_pattern(u, g, br, bc));
+    touch[lb] = 0;
     if (MODE == MODE_REACH) fl[lb] = 0;
   }
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  for (int lb = threadIdx.x; lb < LT_N; lb += blockDim.x)
+    pat[lb] = uint8_t(staged_pattern(su, lb >> LT_LOG, lb & (T::TBW - 1)));
   __syncthreads();
   T tile{pat, par, LT_N};
   tile.solve();
-  const int r0 = 2 * tbr0, c0 = 2 * tbc0;
-  if (MODE == MODE_REACH) {
-    const uint32_t* t = tbits + size_t(slice) * g.slice;
-    for (int lb = threadIdx.x; lb < LT_N; lb += blockDim.x) {
-      uint32_t p = pat[lb];
-      if (!p) continue;
-      int br = tbr0 + (lb >> LT_LOG), bc = tbc0 + (lb & (T::TBW - 1));
-      if (p & near_pattern(t, g, br, bc)) fl[T::blk(par[lb])] = 1;
-    }
-    __syncthreads();
-  }
+
   uint32_t* Ps = P + size_t(slice) * g.sb;
   for (int lb = threadIdx.x; lb < LT_N; lb += blockDim.x) {
-    int br = tbr0 + (lb >> LT_LOG), bc = tbc0 + (lb & (T::TBW - 1));
-    if (br >= g.BH || bc >= g.BW) continue;
-    uint32_t p = pat[lb];
+    const uint32_t p = pat[lb];
+    const int lbr = lb >> LT_LOG, lbc = lb & (T::TBW - 1);
+    const int br = tbr0 + lbr, bc = tbc0 + lbc;
     uint32_t v = 0;
     if (p) {
-      uint32_t lk = par[lb];
-      uint32_t gr = uint32_t(r0) + (lk >> T::KW), gc = uint32_t(c0) + (lk & ((1u << T::KW) - 1u));
+      const uint32_t lk = par[lb];
+      const uint32_t gr = uint32_t(r0) + (lk >> T::KW);
+      const uint32_t gc = uint32_t(c0) + (lk & ((1u << T::KW) - 1u));
       v = ((gr << g.s) | gc) + 1u;
+      if (lbr == 0 || lbr == LT_H - 1 || lbc == 0 || lbc == T::TBW - 1) touch[T::blk(lk)] = 1;
+      if (MODE == MODE_REACH && (p & staged_pattern(snt, lbr, lbc))) fl[T::blk(lk)] = 1;
     }
-    size_t gbi = size_t(br) * g.BW + bc;
-    Ps[gbi] = v;
-    if (MODE == MODE_REACH) {
-      bool root = p && par[lb] == T::key(lb, p);
-      F[size_t(slice) * g.sb + gbi] = (root && fl[lb]) ? 1 : 0;
+    if (br < g.BH && bc < g.BW) Ps[size_t(br) * g.BW + bc] = v;
+  }
+  __syncthreads();
+  const size_t tile_id = (size_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  uint32_t* L = lists + tile_id * LT_LIST;
+  for (int lb = threadIdx.x; lb < LT_N; lb += blockDim.x) {
+    const uint32_t p = pat[lb];
+    if (!p || par[lb] != T::key(lb, p)) continue;  // local roots only
+    const int br = tbr0 + (lb >> LT_LOG), bc = tbc0 + (lb & (T::TBW - 1));
+    const size_t gbi = size_t(br) * g.BW + bc;
+    if (MODE == MODE_REACH) F[size_t(slice) * g.sb + gbi] = fl[lb];
+    if (touch[lb]) L[1 + atomicAdd(&s_cnt, 1)] = Ps[gbi];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) L[0] = uint32_t(s_cnt);
+}
+
+// read-only find (concurrent writers only ever store final roots)
+__device__ __forceinline__ uint32_t gfind_ro(const uint32_t* P, const G& g, uint32_t v) {
+  uint32_t q = __ldcg(P + gblk(g, v));
+  while (q != v) {
+    v = q;
+    q = __ldcg(P + gblk(g, v));
+  }
+  return v;
+}
+
+// After the border merge: every ring-touching local root points straight at
+// its global root (and hands its seed flag over, for reach).  Afterwards any
+// block's global root is exactly two loads away: P[b] -> P[local root].
+__global__ void k_root_flatten(uint32_t* P, uint8_t* F, const uint32_t* __restrict__ lists, G g,
+                               int ntiles, int reach) {
+  const int slice = blockIdx.y;
+  const int tile = int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (tile >= ntiles) return;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint8_t* Fs = reach ? F + size_t(slice) * g.sb : nullptr;
+  const uint32_t* L = lists + (size_t(slice) * ntiles + tile) * LT_LIST;
+  const int n = int(L[0]);
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t r = L[1 + i];
+    const uint32_t R = gfind_ro(Ps, g, r);
+    if (R != r) {
+      Ps[gblk(g, r)] = R;
+      if (reach && Fs[gblk(g, r)]) Fs[gblk(g, R)] = 1;
     }
   }
+}
+
+// global root of a block after k_root_flatten (v = P[b] != 0)
+__device__ __forceinline__ uint32_t groot(const uint32_t* P, const G& g, uint32_t v) {
+  return P[gblk(g, v)];
 }
 
 // unions across tile borders (see DESIGN.md for the link enumeration)
@@ -462,7 +546,7 @@ __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, uint32_t* P,
     uint32_t v = Ps[i];
     uint32_t lab = 0, p = 0;
     if (v) {
-      lab = linear_label(g, gfind(Ps, g, v));
+      lab = linear_label(g, groot(Ps, g, v));
       p = load_pattern(u, g, br, bc);
     }
     int r = 2 * br, c = 2 * bc;
@@ -480,19 +564,6 @@ __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, uint32_t* P,
         if (c + 1 < g.W) Ls[o + g.W + 1] = b1;
       }
     }
-  }
-}
-
-// reach: flagged local roots raise the flag of their global root
-__global__ void k_reach_propagate(uint32_t* P, uint8_t* F, G g) {
-  const int slice = blockIdx.y;
-  uint32_t* Ps = P + size_t(slice) * g.sb;
-  uint8_t* Fs = F + size_t(slice) * g.sb;
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < g.sb;
-       i += size_t(gridDim.x) * blockDim.x) {
-    if (!Fs[i]) continue;
-    size_t rb = gblk(g, gfind(Ps, g, Ps[i]));
-    if (rb != i) Fs[rb] = 1;
   }
 }
 
@@ -516,7 +587,7 @@ __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
     uint32_t p = 0;
     if (bc < g.BW) {
       uint32_t v = Ps[size_t(br) * g.BW + bc];
-      if (v && Fs[gblk(g, gfind(Ps, g, v))]) p = load_pattern(u, g, br, bc);
+      if (v && Fs[gblk(g, groot(Ps, g, v))]) p = load_pattern(u, g, br, bc);
     }
     warp_store_patterns(out + size_t(slice) * g.slice, g, br, bc0, p,
                         tbits + size_t(slice) * g.slice);
@@ -542,7 +613,7 @@ __global__ void k_maxvol_size(const uint32_t* __restrict__ ubits, uint32_t* P,
       if (v) {
         int br = int(i / g.BW), bc = int(i - size_t(br) * g.BW);
         cnt = __popc(load_pattern(u, g, br, bc));
-        rb = gblk(g, gfind(Ps, g, v));
+        rb = gblk(g, groot(Ps, g, v));
       }
     }
     unsigned peers = __match_any_sync(0xffffffffu, (unsigned long long)rb);
@@ -587,7 +658,7 @@ __global__ void k_maxvol_select(const uint32_t* __restrict__ ubits,
     uint32_t p = 0;
     if (bc < g.BW) {
       uint32_t v = Ps[size_t(br) * g.BW + bc];
-      if (v && Ss[gblk(g, gfind(Ps, g, v))] == mx) p = load_pattern(u, g, br, bc);
+      if (v && Ss[gblk(g, groot(Ps, g, v))] == mx) p = load_pattern(u, g, br, bc);
     }
     warp_store_patterns(out + size_t(slice) * g.slice, g, br, bc0, p, nullptr);
   }
@@ -783,11 +854,15 @@ void check_label_range(const Geo& gb) {
 
 bool ccl_small_path(int w, int h) { return w <= 256 && h <= 256; }
 
+static size_t n_tiles(const KeyGeo& k) {
+  return size_t((k.bw + 31) / 32) * size_t((k.bh + LT_H - 1) / LT_H);
+}
+
 size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes) {
   if (ccl_small_path(w, h)) return 0;
   KeyGeo k = key_geo(w, h);
   size_t n = k.slice_blocks * size_t(batch);
-  size_t b = round_up(n * 4, 256);
+  size_t b = round_up(n * 4, 256) + round_up(n_tiles(k) * size_t(batch) * LT_LIST * 4, 256);
   if (flags) b += round_up(n, 256);
   if (sizes) b += round_up(n * 4, 256) + round_up(size_t(batch) * 4, 256);
   return b;
@@ -802,6 +877,8 @@ void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool siz
   unsigned char* p = static_cast<unsigned char*>(base);
   s->parent = reinterpret_cast<uint32_t*>(p);
   p += round_up(n * 4, 256);
+  s->lists = reinterpret_cast<uint32_t*>(p);
+  p += round_up(n_tiles(k) * size_t(batch) * LT_LIST * 4, 256);
   if (flags) {
     s->flag = p;
     p += round_up(n, 256);
@@ -817,16 +894,19 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
                                   CclScratch& s, bool reach, cudaStream_t st, int& launches) {
   dim3 grid(unsigned((g.BW + 31) / 32), unsigned((g.BH + LT_H - 1) / LT_H), unsigned(batch));
   if (reach)
-    k_tile_local<MODE_REACH><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, g);
+    k_tile_local<MODE_REACH><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, s.lists, g);
   else
-    k_tile_local<MODE_CCL><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, g);
+    k_tile_local<MODE_CCL><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, s.lists, g);
   ++launches;
-  int nhb = (g.BH + LT_H - 1) / LT_H - 1, nvb = (g.BW + 31) / 32 - 1;
+  int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
   size_t links = size_t(nhb) * g.BW + size_t(nvb) * g.BH;
   if (links) {
     dim3 mg(unsigned(grid_blocks(links, 256)), unsigned(batch));
     k_tile_merge<<<mg, 256, 0, st>>>(u, s.parent, g, nhb, nvb);
-    ++launches;
+    int ntiles = int(grid.x * grid.y);
+    dim3 fg(unsigned((ntiles * 32 + 255) / 256), unsigned(batch));
+    k_root_flatten<<<fg, 256, 0, st>>>(s.parent, s.flag, s.lists, g, ntiles, reach ? 1 : 0);
+    launches += 2;
   }
 }
 
@@ -855,12 +935,10 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
     fail(SLCS_ERR_TOO_LARGE, "reach: image too large for 32-bit block keys");
   int launches = 0;
   large_local_and_merge(through, target, g, gb.batch, s, true, st, launches);
-  dim3 pg(unsigned(grid_blocks(g.sb, 256)), unsigned(gb.batch));
-  k_reach_propagate<<<pg, 256, 0, st>>>(s.parent, s.flag, g);
   size_t warps = size_t(g.BH) * (gb.pitch / 2);
   dim3 sg(unsigned(grid_blocks(warps * 32, 256)), unsigned(gb.batch));
   k_reach_select<<<sg, 256, 0, st>>>(through, target, s.parent, s.flag, tmp_bits, g);
-  launches += 2;
+  launches += 1;
   launches += launch_near(tmp_bits, out, gb, 1, false, st);
   return launches;
 }

@@ -653,14 +653,6 @@ struct slcs_program {
     for (LG& n : lgs) n.consumers = 0;
     for (const LG& n : lgs)
       for (int q : n.in) lgs[q].consumers++;
-    auto expr_uses = [&](int e, auto&& self, std::vector<int>& acc) -> void {
-      const Expr& x = exprs[e];
-      if (x.k == E_LEAF || x.k == E_THRESH) acc.push_back(x.lg);
-      else {
-        self(x.a, self, acc);
-        if (x.b >= 0) self(x.b, self, acc);
-      }
-    };
     if (fuse) {
       for (size_t q = 0; q < lgs.size(); ++q) {
         LG& n = lgs[q];

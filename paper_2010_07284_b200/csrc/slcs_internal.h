@@ -124,6 +124,7 @@ int launch_fused(const FusedProgram& p, const Geo& gb, const Geo& gu, cudaStream
 // ---- connected components (ccl.cu) -------------------------------------------
 struct CclScratch {
   uint32_t* parent = nullptr;  // per 2x2 block, packed key + 1 (0 = empty)
+  uint32_t* lists = nullptr;   // per tile: count + ring-touching local roots
   uint8_t* flag = nullptr;     // per block
   uint32_t* size = nullptr;    // per block (maxvol)
   unsigned int* maxv = nullptr;  // per slice (maxvol)
