@@ -146,6 +146,25 @@ __device__ void gunite(uint32_t* P, const G& g, uint32_t a, uint32_t b) {
   }
 }
 
+
+// Border links are emitted per word; along a tile border consecutive lanes
+// usually link the same pair of local roots.  A lane skips its union when the
+// previous lane of the warp linked the identical (local root, local root)
+// pair -- checked with one shuffle, so a straight border costs one union.
+__device__ __forceinline__ void gunite_dedup(uint32_t* P, const G& g, uint32_t a, uint32_t b,
+                                             bool active) {
+  const uint32_t la = active ? __ldcg(P + gblk(g, a)) : 0u;
+  const uint32_t lb = active ? __ldcg(P + gblk(g, b)) : 0u;
+  const uint32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31;
+  const uint32_t plo = __shfl_up_sync(mask, lo, 1), phi = __shfl_up_sync(mask, hi, 1);
+  const bool prev_active = lane > 0 && ((mask >> (lane - 1)) & 1u);
+  if (!active) return;
+  if (prev_active && plo == lo && phi == hi) return;
+  if (la != lb) gunite(P, g, la, lb);
+}
+
 // read-only find (concurrent writers only ever store final roots)
 __device__ __forceinline__ uint32_t gfind_ro(const uint32_t* P, const G& g, uint32_t v) {
   uint32_t q = __ldcg(P + gblk(g, v));
@@ -452,9 +471,11 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
       load_unit(u, g, k, jl, Tl, Bl);
       load_unit(u, g, k, jr, Tr, Br);
       const uint32_t cl = Tl | Bl, cr = Tr | Br;
-      if ((cl >> 31) && (cr & 1u))
-        gunite(Ps, g, grun(g, k, jl, Tl, Bl, run_at(cl, 31)),
-               grun(g, k, jr, Tr, Br, run_at(cr, 0)));
+      // consecutive lanes walk down one border: dedupe the horizontal link
+      const bool hlink = (cl >> 31) && (cr & 1u);
+      const uint32_t va = hlink ? grun(g, k, jl, Tl, Bl, run_at(cl, 31)) : 0u;
+      const uint32_t vb = hlink ? grun(g, k, jr, Tr, Br, run_at(cr, 0)) : 0u;
+      gunite_dedup(Ps, g, va, vb, hlink);
       if (k % LTNB != 0 && ((Tr & 1u) || (Tl >> 31))) {
         uint32_t Tul, Bul, Tur, Bur;
         load_unit(u, g, k - 1, jl, Tul, Bul);
