@@ -46,6 +46,12 @@ def parse():
                    help="chain depth of one bounded CPU-reference sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--label-cse", action="store_true",
+                   help="headline with label CSE on (reaches sharing one `through` node label "
+                        "it once).  Default off: every reach node labels its own `through`, "
+                        "exactly the reference's per-node work (reach.cpp:21)")
+    p.add_argument("--alt-steps", type=int, default=3,
+                   help="steps for the secondary measurement with label CSE toggled")
     return p.parse_args()
 
 
@@ -213,8 +219,9 @@ def main():
     prog.set_input_host("img.png", pin_in.numpy(), PixelKind.U16)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
+    cse = args.label_cse
     for _ in range(max(3, args.warmup)):
-        prog.run()
+        prog.run(label_cse=cse)
     torch.cuda.synchronize()
 
     # ---- value: device-resident, per-step CUDA events, L2 flushed between steps
@@ -228,7 +235,7 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            prog.run()
+            prog.run(label_cse=cse)
             ends[i].record(stream)
         torch.cuda.synchronize()
     if ws > 1:
@@ -243,6 +250,26 @@ def main():
     value = ws * args.steps * prim_nodes * px / total_s / 1e9
     ms_per_step = total_s / args.steps * 1e3
 
+    # secondary: the same formula with label CSE toggled (reported, not the headline)
+    alt = None
+    if args.alt_steps > 0:
+        for _ in range(2):
+            prog.run(label_cse=not cse)
+        torch.cuda.synchronize()
+        a_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.alt_steps)]
+        for a0, a1 in a_ev:
+            flush.zero_()
+            a0.record(stream)
+            prog.run(label_cse=not cse)
+            a1.record(stream)
+        torch.cuda.synchronize()
+        alt_s = sum(a0.elapsed_time(a1) for a0, a1 in a_ev) / 1e3
+        alt = {"label_cse": not cse, "value": args.steps and args.alt_steps * prim_nodes * px / alt_s / 1e9,
+               "ms_per_step": alt_s / args.alt_steps * 1e3, "kernels_per_formula": prog.launches}
+        prog.run(label_cse=cse)
+        torch.cuda.synchronize()
+
     # correctness guard on the benchmarked output (bit-exact properties)
     res = np.zeros((size, size), np.uint8)
     prog.download(out_task, res)
@@ -256,7 +283,7 @@ def main():
     if not args.no_e2e:
         for _ in range(2):
             prog.set_input_host("img.png", pin_in.numpy(), PixelKind.U16)
-            prog.run()
+            prog.run(label_cse=cse)
             prog.download(out_task, pin_out.numpy())
         if ws > 1:
             torch.distributed.barrier()
@@ -264,7 +291,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.steps):
             prog.set_input_host("img.png", pin_in.numpy(), PixelKind.U16)
-            prog.run()
+            prog.run(label_cse=cse)
             prog.download(out_task, pin_out.numpy())
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
@@ -344,6 +371,7 @@ def main():
                        "parallelism": "replicas" if ws > 1 else "single",
                        "ms_per_formula": ms_per_step},
             "gpu_launches": launches, "kernels_per_formula": prog.launches,
+            "label_cse": cse, "alternate": alt,
             "clocks": clocks.summary(), "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu,
         }

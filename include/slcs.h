@@ -158,7 +158,8 @@ int slcs_program_create(slcs_ctx* ctx, int n_tasks, const char* const* opcodes,
 int slcs_program_destroy(slcs_program* prog);
 /* Binds the image loaded by `load` tasks with payload `name`. */
 int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* img);
-/* flags: bit 0 = capture/replay as a CUDA graph, bit 1 = disable fusion. */
+/* flags: bit 0 = capture/replay as a CUDA graph, bit 1 = disable fusion,
+ * bit 2 = disable label CSE (reaches sharing one `through` node label it once). */
 int slcs_program_run(slcs_program* prog, int flags);
 /* Copies host pixels (reference layout) straight into the program's input
  * slot for `load` name `name` -- the end-to-end path: no intermediate image. */

@@ -293,13 +293,13 @@ struct RunTile {
     const int band = u / TWW, w = u % TWW;
     uint32_t x = T | B;
 #pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = 0;
+#pragma unroll
     for (int i = 0; i < 16; ++i) {
-      r[i] = 0;
-      if (x) {
-        const uint32_t m = first_run(x);
-        x &= ~m;
-        r[i] = find(key(band, w, T, B, m));
-      }
+      if (!x) break;
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      r[i] = find(key(band, w, T, B, m));
     }
   }
 };
@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
     uint32_t x = Tw | Bw;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      if (x) {
+      if (!x) break;
+      {
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
@@ -395,7 +396,8 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
     uint32_t x = Tw | Bw;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      if (x) {
+      if (!x) break;
+      {
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
@@ -546,6 +548,73 @@ __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
         const uint32_t m = first_run(x);
         x &= ~m;
         if (Fs[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))]) {
+          ST |= T & m;
+          SB |= B & m;
+        }
+      }
+      ST |= __ldg(t + row);
+      if (two) SB |= __ldg(t + row + g.pitch);
+    }
+    o[row] = ST;
+    if (two) o[row + g.pitch] = SB;
+  }
+}
+
+// ---- reach against a precomputed labelling (label CSE) ------------------------
+// Flags are generation stamps so the per-block flag array never needs
+// clearing: gen = *epoch * 4096 + idx, with *epoch bumped once per program run.
+__global__ void k_epoch_bump(uint32_t* epoch) { *epoch += 1u; }
+
+__global__ void k_reach_seed(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ tbits,
+                             const uint32_t* __restrict__ P, uint32_t* __restrict__ F32,
+                             const uint32_t* __restrict__ epoch, uint32_t idx, G g) {
+  const int slice = blockIdx.y;
+  const uint32_t* u = ubits + size_t(slice) * g.slice;
+  const uint32_t* t = tbits + size_t(slice) * g.slice;
+  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* Fs = F32 + size_t(slice) * g.sb;
+  const uint32_t gen = *epoch * 4096u + idx;
+  const uint32_t n = uint32_t(g.BH) * uint32_t(g.wpr);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k = int(i / uint32_t(g.wpr)), j = int(i - uint32_t(k) * uint32_t(g.wpr));
+    const size_t row = size_t(2 * k) * g.pitch + j;
+    const bool two = 2 * k + 1 < g.H;
+    const uint32_t T = __ldg(u + row), B = two ? __ldg(u + row + g.pitch) : 0u;
+    if (!(T | B)) continue;
+    const uint32_t sd = (T & near_word(t, g, 2 * k, j)) | (two ? (B & near_word(t, g, 2 * k + 1, j)) : 0u);
+    for (uint32_t x = T | B; x;) {
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      if (sd & m) Fs[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))] = gen;
+    }
+  }
+}
+
+__global__ void k_reach_select_gen(const uint32_t* __restrict__ ubits,
+                                   const uint32_t* __restrict__ tbits,
+                                   const uint32_t* __restrict__ P,
+                                   const uint32_t* __restrict__ F32,
+                                   const uint32_t* __restrict__ epoch, uint32_t idx,
+                                   uint32_t* __restrict__ out, G g) {
+  const int slice = blockIdx.y;
+  const uint32_t* u = ubits + size_t(slice) * g.slice;
+  const uint32_t* t = tbits + size_t(slice) * g.slice;
+  const uint32_t* Ps = P + size_t(slice) * g.sb;
+  const uint32_t* Fs = F32 + size_t(slice) * g.sb;
+  uint32_t* o = out + size_t(slice) * g.slice;
+  const uint32_t gen = *epoch * 4096u + idx;
+  const uint32_t n = uint32_t(g.BH) * g.pitch;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k = int(i / g.pitch), j = int(i - uint32_t(k) * g.pitch);
+    const size_t row = size_t(2 * k) * g.pitch + j;
+    const bool two = 2 * k + 1 < g.H;
+    uint32_t ST = 0, SB = 0;
+    if (j < g.wpr) {
+      const uint32_t T = __ldg(u + row), B = two ? __ldg(u + row + g.pitch) : 0u;
+      for (uint32_t x = T | B; x;) {
+        const uint32_t m = first_run(x);
+        x &= ~m;
+        if (Fs[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))] == gen) {
           ST |= T & m;
           SB |= B & m;
         }
@@ -939,6 +1008,37 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
     k_root_flatten<<<fg, 256, 0, st>>>(s.parent, s.flag, s.size, s.lists, g, ntiles, mode);
     launches += 2;
   }
+}
+
+size_t ccl_labels_bytes(int w, int h, int batch) {
+  return ccl_scratch_bytes(w, h, batch, false, false);
+}
+
+int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStream_t st) {
+  check_key_range(gb, "reach");
+  G g = make_g(gb);
+  CclScratch s;
+  ccl_scratch_carve(labels, gb.w, gb.h, gb.batch, false, false, &s);
+  int launches = 0;
+  large_local_and_merge(through, nullptr, g, gb.batch, s, MODE_CCL, st, launches);
+  return launches;
+}
+
+int launch_epoch_bump(uint32_t* epoch, cudaStream_t st) {
+  k_epoch_bump<<<1, 1, 0, st>>>(epoch);
+  return 1;
+}
+
+int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,
+                         uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
+                         uint32_t* tmp_bits, const Geo& gb, cudaStream_t st) {
+  G g = make_g(gb);
+  const uint32_t* P = static_cast<const uint32_t*>(labels);
+  dim3 ug(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
+  k_reach_seed<<<ug, 256, 0, st>>>(through, target, P, flags32, epoch, idx, g);
+  dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
+  k_reach_select_gen<<<sg, 256, 0, st>>>(through, target, P, flags32, epoch, idx, tmp_bits, g);
+  return 2 + launch_near(tmp_bits, out, gb, 1, false, st);
 }
 
 int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,

@@ -59,7 +59,7 @@ struct PTask {
   std::vector<int> deps;
 };
 
-enum VT { VT_NONE = 0, VT_NUM, VT_BOOL, VT_U16, VT_LABEL };
+enum VT { VT_NONE = 0, VT_NUM, VT_BOOL, VT_U16, VT_LABEL, VT_AUX };
 
 const char* vt_name(VT t) {
   switch (t) {
@@ -81,7 +81,8 @@ struct Expr {
   int need = 1;        // Sethi-Ullman register need
 };
 
-enum LK { LG_INPUT, LG_EW, LG_NEAR, LG_REACH, LG_MAXVOL, LG_VOLUME, LG_ARITH, LG_THRESH_DEV };
+enum LK { LG_INPUT, LG_EW, LG_NEAR, LG_REACH, LG_MAXVOL, LG_VOLUME, LG_ARITH, LG_THRESH_DEV,
+          LG_LABELS };
 
 struct LG {
   LK kind;
@@ -95,6 +96,7 @@ struct LG {
   char aop = '+';
   int num_out = -1, num_a = -1, num_b = -1;
   double ca = 0, cb = 0;
+  int gen_idx = -1;  // LG_REACH against an LG_LABELS input (label CSE)
   std::string name;  // LG_INPUT
   bool dead = false, output = false;
   int consumers = 0, last_use = -1;
@@ -206,6 +208,8 @@ struct slcs_program {
   double* d_nums = nullptr;
   unsigned long long* d_counts = nullptr;
   int* d_err = nullptr;
+  uint32_t* d_epoch = nullptr;
+  bool label_cse_used = false;
   void* staging = nullptr;
   size_t staging_bytes = 0;
   bool has_dev_arith = false;
@@ -229,6 +233,8 @@ struct slcs_program {
     if (d_nums) cudaFree(d_nums);
     if (d_counts) cudaFree(d_counts);
     if (d_err) cudaFree(d_err);
+    if (d_epoch) cudaFree(d_epoch);
+    d_epoch = nullptr;
     arena = scratch = nullptr;
     d_nums = nullptr;
     d_counts = nullptr;
@@ -338,7 +344,7 @@ struct slcs_program {
     return add_expr(e);
   }
 
-  void plan(int fusion) {
+  void plan(int fusion, bool label_cse) {
     release_plan();
     vals.assign(tasks.size(), Val{});
     lgs.clear();
@@ -367,6 +373,15 @@ struct slcs_program {
         if (t.op != OP_INTENSITY || eff_out[i]) eff_out[d] = true;
       }
     }
+
+    // reaches per `through` task: a labelling shared by >= 2 reaches is
+    // computed once (label CSE) when enabled
+    std::vector<int> reach_uses(tasks.size(), 0);
+    for (const PTask& t : tasks)
+      if (t.op == OP_REACH) reach_uses[t.deps[1]]++;
+    std::map<int, int> labels_of;  // through LG -> LG_LABELS
+    int labeled = 0;
+    label_cse_used = false;
 
     auto fail_task = [&](int i, const std::string& msg) {
       vals[i].err = msg;
@@ -584,6 +599,23 @@ struct slcs_program {
             g.h = x.h;
             g.batch = x.batch;
             g.in = {a, b};
+            if (label_cse && reach_uses[t.deps[1]] >= 2 && !ccl_small_path(x.w, x.h) &&
+                labeled < 4096) {
+              auto it = labels_of.find(b);
+              if (it == labels_of.end()) {
+                LG l;
+                l.kind = LG_LABELS;
+                l.type = VT_AUX;
+                l.w = x.w;
+                l.h = x.h;
+                l.batch = x.batch;
+                l.in = {b};
+                it = labels_of.emplace(b, add_lg(l)).first;
+              }
+              g.in.push_back(it->second);
+              g.gen_idx = labeled++;
+              label_cse_used = true;
+            }
             v.lg = add_lg(g);
             break;
           }
@@ -717,12 +749,19 @@ struct slcs_program {
     size_t scratch_need = 0;
     for (size_t pos = 0; pos < order.size(); ++pos) {
       LG& n = lgs[order[pos]];
-      if (n.type != VT_NUM) {
+      if (n.type == VT_AUX) {
+        // labelling + the reach flag stamps (one uint32 per 2x2 block)
+        n.bytes = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256) +
+                  key_geo(n.w, n.h).slice_blocks * size_t(n.batch) * 4;
+        n.offset = alloc(n.bytes);
+      } else if (n.type != VT_NUM) {
         Geo g = geo_of(n.type, n.w, n.h, n.batch);
         n.bytes = g.slice * size_t(n.batch) * unit_of(n.type);
         n.offset = alloc(n.bytes);
       }
-      if (n.kind == LG_REACH) {
+      if (n.kind == LG_REACH && n.gen_idx >= 0) {
+        scratch_need = std::max(scratch_need, bool_geo(n.w, n.h, n.batch).slice * n.batch * 4);
+      } else if (n.kind == LG_REACH) {
         size_t s = ccl_scratch_bytes(n.w, n.h, n.batch, true, false);
         if (!ccl_small_path(n.w, n.h)) s += bool_geo(n.w, n.h, n.batch).slice * n.batch * 4;
         scratch_need = std::max(scratch_need, s);
@@ -753,6 +792,8 @@ struct slcs_program {
     cuda_check(cudaMalloc(&d_counts, sizeof(unsigned long long) * std::max(1, n_nums)),
                "program counts");
     cuda_check(cudaMalloc(&d_err, sizeof(int)), "program error flag");
+    cuda_check(cudaMalloc(&d_epoch, sizeof(uint32_t)), "program epoch");
+    cuda_check(cudaMemset(d_epoch, 0, sizeof(uint32_t)), "program epoch");
     for (LG& n : lgs) {
       if (n.kind == LG_INPUT) n.ptr = inputs[n.name].data;
       else if (!n.dead && n.type != VT_NUM) n.ptr = static_cast<char*>(arena) + n.offset;
@@ -766,10 +807,11 @@ struct slcs_program {
     for (int q : order) {
       const LG& n = lgs[q];
       static const char* kn[] = {"input", "fused", "near", "reach", "maxvol", "volume", "arith",
-                                 "threshold(dev)"};
+                                 "threshold(dev)", "labels"};
       os << "  step " << q << ": " << kn[n.kind];
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
+      if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
       os << " " << n.w << "x" << n.h;
       if (n.batch > 1) os << "x" << n.batch;
       os << " in=[";
@@ -778,7 +820,6 @@ struct slcs_program {
     }
     plan_text = os.str();
     planned = true;
-    planned_fusion = fusion;
   }
 
   // ------------------------------------------------------------------ emit
@@ -830,6 +871,7 @@ struct slcs_program {
   int enqueue(cudaStream_t st) {
     int launches = 0;
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
+    if (label_cse_used) launches += launch_epoch_bump(d_epoch, st);
     for (size_t q = 0; q < lgs.size(); ++q) {
       LG& n = lgs[q];
       if (n.dead || n.kind == LG_INPUT) continue;
@@ -867,7 +909,24 @@ struct slcs_program {
                                            u16_geo(n.w, n.h, n.batch), gb, n.cmp,
                                            d_nums + n.num_a, st);
           break;
+        case LG_LABELS: {
+          size_t lb = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256);
+          cudaMemsetAsync(static_cast<char*>(n.ptr) + lb, 0, n.bytes - lb, st);
+          launches += launch_labels(static_cast<const uint32_t*>(lgs[n.in[0]].ptr), n.ptr, gb, st);
+          break;
+        }
         case LG_REACH: {
+          if (n.gen_idx >= 0) {
+            const LG& lab = lgs[n.in[2]];
+            size_t lb = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256);
+            launches += launch_reach_labeled(
+                static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
+                static_cast<const uint32_t*>(lgs[n.in[1]].ptr), lab.ptr,
+                reinterpret_cast<uint32_t*>(static_cast<char*>(lab.ptr) + lb), d_epoch,
+                uint32_t(n.gen_idx), static_cast<uint32_t*>(n.ptr),
+                static_cast<uint32_t*>(scratch), gb, st);
+            break;
+          }
           CclScratch cs;
           ccl_scratch_carve(scratch, n.w, n.h, n.batch, true, false, &cs);
           size_t sb = ccl_scratch_bytes(n.w, n.h, n.batch, true, false);
@@ -914,7 +973,10 @@ struct slcs_program {
   void run(int flags) {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     const int fusion = (flags & 2) ? 0 : 1;
-    if (!planned || planned_fusion != fusion) plan(fusion);
+    const bool label_cse = fusion && !(flags & 4);
+    const int mode = fusion | (label_cse ? 2 : 0);
+    if (!planned || planned_fusion != mode) plan(fusion, label_cse);
+    planned_fusion = mode;
     // order after work already queued on the context stream
     cuda_check(cudaEventRecord(ev_in, ctx->stream), "event");
     cuda_check(cudaStreamWaitEvent(pstream, ev_in, 0), "wait");

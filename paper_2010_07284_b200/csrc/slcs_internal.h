@@ -139,6 +139,14 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
                  uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st);
 int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
                   cudaStream_t st);
+// label CSE: one labelling of `through` (large path only), reused by many reaches
+size_t ccl_labels_bytes(int w, int h, int batch);
+int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStream_t st);
+int launch_epoch_bump(uint32_t* epoch, cudaStream_t st);
+// flags32: one uint32 per 2x2 block (generation stamps); idx < 4096 per run
+int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,
+                         uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
+                         uint32_t* tmp_bits, const Geo& gb, cudaStream_t st);
 
 }  // namespace slcs
 

@@ -23,6 +23,7 @@ from .pixlog import (_DTYPE, Device, DeviceImage, ImageBuffer, PixelKind, RunErr
 
 FLAG_GRAPH = 1
 FLAG_NO_FUSION = 2
+FLAG_NO_LABEL_CSE = 4
 
 
 def format_number(v: float) -> str:
@@ -35,6 +36,7 @@ class RunOptions:
     device: Optional[Device] = None
     fusion: bool = True
     cuda_graph: bool = True
+    label_cse: bool = True
 
 
 @dataclass
@@ -97,8 +99,9 @@ class Program:
         _check(_lib.load().slcs_program_set_input_host(self.handle, name.encode(), int(kind), w,
                                                        h, b, C.c_void_p(a.ctypes.data)))
 
-    def run(self, fusion: bool = True, cuda_graph: bool = True) -> None:
-        flags = (FLAG_GRAPH if cuda_graph else 0) | (0 if fusion else FLAG_NO_FUSION)
+    def run(self, fusion: bool = True, cuda_graph: bool = True, label_cse: bool = True) -> None:
+        flags = ((FLAG_GRAPH if cuda_graph else 0) | (0 if fusion else FLAG_NO_FUSION)
+                 | (0 if label_cse else FLAG_NO_LABEL_CSE))
         _check(_lib.load().slcs_program_run(self.handle, flags))
 
     def result(self, task: int) -> Union[DeviceImage, float]:
@@ -147,7 +150,7 @@ def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) ->
     t0 = time.perf_counter()
     err: Optional[RunError] = None
     try:
-        prog.run(options.fusion, options.cuda_graph)
+        prog.run(options.fusion, options.cuda_graph, options.label_cse)
     except RunError as e:
         err = e
     prog.device.synchronize()

@@ -163,6 +163,31 @@ def test_near_reach_chain_small(dev):
     assert np.array_equal(out_of(rep, "o.png"), x)
 
 
+@pytest.mark.parametrize("cse", [True, False])
+@pytest.mark.parametrize("graph", [True, False])
+def test_near_reach_chain_large_path_label_cse(dev, cse, graph):
+    # > 256 px: the tiled path; the 6 reaches share `b`, so with label CSE on
+    # the labelling of b is computed once per run (generation-stamped flags)
+    img = O.blob_noise(700, 530, 5)
+    b = O.threshold(0, img, 56360)
+    x = O.threshold(0, img, 62258)
+    lines = ['load img = "img.png"', "let b = img >. 56360", "let x0 = img >. 62258"]
+    for k in range(6):
+        lines.append(f"let x{2 * k + 1} = near(x{2 * k})")
+        lines.append(f"let x{2 * k + 2} = reach(x{2 * k + 1}, b)")
+        x = O.reach(O.dilate(x), b)
+    lines.append('save "o.png" x12')
+    prog = Program(compile_text("\n".join(lines) + "\n"))
+    prog.set_input_host("img.png", img, PixelKind.U16)
+    out = [i for i, t in enumerate(prog.graph.nodes) if t.opcode == "save"][0]
+    for _ in range(3):  # replays must not see stale flag stamps
+        prog.run(cuda_graph=graph, label_cse=cse)
+        got = np.zeros(img.shape, np.uint8)
+        prog.download(out, got)
+        assert np.array_equal(got, x)
+    assert ("shared labelling" in prog.plan) == cse
+
+
 def random_formula(rng, budget):
     if budget <= 1:
         img = "imgA" if rng.below(2) else "imgB"
