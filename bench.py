@@ -50,6 +50,10 @@ def parse():
                    help="headline with label CSE on (reaches sharing one `through` node label "
                         "it once).  Default off: every reach node labels its own `through`, "
                         "exactly the reference's per-node work (reach.cpp:21)")
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
+                   help="BASELINE.json config: c2 (default, the headline) or the parity/"
+                        "secondary workloads c1, c3 (sharded by slice under torchrun), c4")
+    p.add_argument("--density", type=float, default=0.5, help="c4 mask density")
     p.add_argument("--alt-steps", type=int, default=3,
                    help="steps for the secondary measurement with label CSE toggled")
     return p.parse_args()
@@ -184,11 +188,206 @@ def run_reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+C1_SPEC = ('load img = "img.png"\nlet a = img >. 62258\nlet b = img >. 56360\n'
+           'save "out.png" reach(near(near(near(near(a & !b)))), b)\n')
+
+
+def formula_config(args, ws, rank, local):
+    """c1 (256^2) and c3 (155 x 240^2 slices, segmentation spec)."""
+    import numpy as np
+    import torch
+
+    from paper_2010_07284_b200 import Device, PixelKind
+    from paper_2010_07284_b200 import synth as S
+    from paper_2010_07284_b200.executor import Program
+    from paper_2010_07284_b200.imgql import STDLIB, compile_text
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    dev = Device(local, stream=stream.cuda_stream)
+    if args.config == "c1":
+        spec, name, seeds, n = C1_SPEC, "img.png", [args.seed], 256
+        workload = "BASELINE config 1: reach(near^4(a & !b), b) on a 256x256 blob-noise image"
+    else:
+        spec, name, n = S.SEGMENTATION_SPEC, "slices.png", 240
+        all_seeds = list(range(100, 255))  # 155 slices
+        per = (len(all_seeds) + ws - 1) // ws
+        seeds = all_seeds[rank * per:(rank + 1) * per] or [100]
+        workload = ("BASELINE config 3: segmentation spec maxvol(grow(hI,vI)) | surrounded(hI,vI) "
+                    "over 155 blob-noise 240x240 slices (seeds 100..254), one batched program")
+    imgs = np.stack([S.blob_noise(n, n, sd) for sd in seeds])
+    graph = compile_text(spec)
+    prim = sum(1 for t in graph.nodes if t.opcode not in ("load", "save", "const"))
+    out_task = [i for i, t in enumerate(graph.nodes) if t.opcode == "save"][0]
+    prog = Program(graph, dev)
+    pin_in = torch.from_numpy(imgs if len(seeds) > 1 else imgs[0]).pin_memory()
+    pin_out = torch.empty(tuple(pin_in.shape), dtype=torch.uint8).pin_memory()
+    prog.set_input_host(name, pin_in.numpy(), PixelKind.U16)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    for _ in range(max(3, args.warmup)):
+        prog.run()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    l0 = dev.launches
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for a, b in ev:
+            flush.zero_()
+            a.record(stream)
+            prog.run()
+            b.record(stream)
+        torch.cuda.synchronize()
+    launches = dev.launches - l0
+    t = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+    units_local = prim * n * n * len(seeds)
+    if ws > 1:
+        tt = torch.tensor([t], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+        uu = torch.tensor([units_local], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(uu)
+        units = float(uu.item())
+    else:
+        units = units_local
+    value = units * args.steps / t / 1e9
+    # e2e through the public API with host buffers
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prog.set_input_host(name, pin_in.numpy(), PixelKind.U16)
+        prog.run()
+        prog.download(out_task, pin_out.numpy())
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        if os.path.exists(O._REF):
+            R = O.Reference(workers=os.cpu_count() or 1)
+            k = min(len(seeds), 31)
+            res = R.run(spec, {name: imgs[:k] if k > 1 else imgs[0]}, STDLIB) if k == 1 else None
+            if k > 1:  # the reference executor takes one image per load: run slices in turn
+                tcpu = 0.0
+                for q in range(k):
+                    tcpu += R.run(spec, {name: imgs[q]}, STDLIB)["computation_ms"] / 1e3
+            else:
+                tcpu = res["computation_ms"] / 1e3
+            cpu = {"value": prim * n * n * k / tcpu / 1e9, "unit": "Gpixel-ops/s",
+                   "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"{k} slice(s) through executor::run", "ms": tcpu * 1e3}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Gpixel-ops/s", "value": value, "unit": "Gpixel-ops/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u1/u16 (bit-packed integer)", "data": "synthetic",
+            "config": {"workload": workload, "slices_per_rank": len(seeds), "image": f"{n}x{n}",
+                       "primitive_nodes": prim, "l2": "flushed before every timed step",
+                       "parallelism": f"slices sharded over {ws} rank(s)" if ws > 1 else "single"},
+            "gpu_launches": launches, "kernels_per_formula": prog.launches,
+            "clocks": clocks.summary(),
+            "e2e": {"value": units * args.steps / e2e_s / 1e9, "unit": "Gpixel-ops/s",
+                    "h2d_bytes_per_step": int(pin_in.numel()) * 2,
+                    "d2h_bytes_per_step": int(pin_out.numel()),
+                    "ms_per_step": e2e_s / args.steps * 1e3},
+            "cpu_baseline": cpu}), flush=True)
+
+
+def c4_config(args, ws, rank, local):
+    """c4: CCL + reach on a 16384^2 random mask (device-generated randomMask stream)."""
+    import torch
+
+    from paper_2010_07284_b200 import Device, ccl, reach
+    from paper_2010_07284_b200.pixlog import random_mask_device
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    dev = Device(local, stream=stream.cuda_stream)
+    n = args.size if args.size != 4096 else 16384
+    mask = random_mask_device(n, n, args.density, 1, 0, dev)
+    target = random_mask_device(n, n, 0.05, 2, 0, dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    for _ in range(max(2, args.warmup)):
+        ccl.label(mask, dev)
+        reach(target, mask, dev)
+    torch.cuda.synchronize()
+    ec = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    er = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    l0 = dev.launches
+    with ClockSampler(local) as clocks:
+        for (a, b), (c, d) in zip(ec, er):
+            flush.zero_()
+            a.record(stream)
+            lab = ccl.label(mask, dev)
+            b.record(stream)
+            del lab
+            flush.zero_()
+            c.record(stream)
+            r = reach(target, mask, dev)
+            d.record(stream)
+            del r
+        torch.cuda.synchronize()
+    tc = sum(a.elapsed_time(b) for a, b in ec) / 1e3 / args.steps
+    tr = sum(a.elapsed_time(b) for a, b in er) / 1e3 / args.steps
+    px = n * n
+    peak, pk = measured_peak_gbs()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle as O
+        if os.path.exists(O._REF):
+            R = O.Reference(workers=os.cpu_count() or 1)
+            m = 4096
+            a = O.random_mask(m, m, args.density, O.Rng(1))
+            t0 = time.perf_counter()
+            R.ccl_label(a)
+            t_cpu = time.perf_counter() - t0
+            cpu = {"value": m * m / t_cpu / 1e9, "unit": "Gpixel-ops/s", "cores": os.cpu_count(),
+                   "kind": "reference", "sample": f"ccl::label on a {m}x{m} random mask "
+                                                  f"(density {args.density})",
+                   "ms": t_cpu * 1e3}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Gpixel-ops/s", "value": 2 * px / (tc + tr) / 1e9, "unit": "Gpixel-ops/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": (tc + tr) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u1 -> u32 labels", "data": "synthetic",
+            "config": {"workload": f"BASELINE config 4: ccl::label + reach on a {n}x{n} random "
+                                   f"mask, density {args.density} (target density 0.05)",
+                       "ccl_ms": tc * 1e3, "reach_ms": tr * 1e3},
+            "gpu_launches": dev.launches - l0, "clocks": clocks.summary(),
+            "roofline": {"bound": "hbm", "kernel": "ccl::label (tile-local UF, merge, flatten, "
+                                                   "labels)",
+                         "achieved": 4.125 * px / tc / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": 4.125 * px / tc / 1e9 / peak, "traffic": None,
+                         "peak_source": pk},
+            "cpu_baseline": cpu}), flush=True)
+
+
 def main():
     args = parse()
     ws, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
+        return
+    if args.config != "c2":
+        import torch
+        torch.cuda.set_device(local)
+        if ws > 1:
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.config == "c4":
+            c4_config(args, ws, rank, local)
+        else:
+            formula_config(args, ws, rank, local)
+        if ws > 1:
+            torch.distributed.destroy_process_group()
         return
 
     import numpy as np

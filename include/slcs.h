@@ -90,6 +90,12 @@ int slcs_image_from_device(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batc
 int slcs_image_download(slcs_ctx* ctx, const slcs_image* img, void* host, size_t bytes);
 /* Device-to-device copy into the reference dense layout (no sync). */
 int slcs_image_to_device(slcs_ctx* ctx, const slcs_image* img, void* dev, size_t bytes);
+/* Rows [row0, row0 + h) of the reference's randomMask(w, H, density, Rng(seed))
+ * fixture (proj/tests/oracles.cpp:44-49, splitmix64 proj/include/pixlog/rng.hpp:14-19)
+ * generated on the device, bit-identical to the CPU stream: pixel i consumes
+ * draw i.  Lets each rank of a banded run generate its own band. */
+int slcs_random_mask(slcs_ctx* ctx, int w, int h, long long row0, uint64_t seed, double density,
+                     slcs_image** out);
 int slcs_image_retain(slcs_image* img);
 int slcs_image_release(slcs_image* img);
 int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch);

@@ -36,6 +36,7 @@ _SIGS = {
     "slcs_image_from_device": (i32, [vp, i32, i32, i32, i32, vp, pvp]),
     "slcs_image_download": (i32, [vp, vp, vp, sz]),
     "slcs_image_to_device": (i32, [vp, vp, vp, sz]),
+    "slcs_random_mask": (i32, [vp, i32, i32, C.c_longlong, C.c_uint64, dbl, pvp]),
     "slcs_image_retain": (i32, [vp]),
     "slcs_image_release": (i32, [vp]),
     "slcs_image_info": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),

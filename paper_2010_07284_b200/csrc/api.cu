@@ -280,9 +280,9 @@ slcs_image* op_ccl(slcs_ctx* ctx, const slcs_image* a0) {
   if ((unsigned long long)g.w * (unsigned long long)g.h >= 0xfffffffeull)
     fail(SLCS_ERR_TOO_LARGE, "image too large for packed coordinate labels");
   Ref out(new_image(ctx, SLCS_LABEL, g.w, g.h, g.batch));
-  Scratch s(ctx, ccl_scratch_bytes(g.w, g.h, g.batch, false, false));
+  Scratch s(ctx, ccl_scratch_bytes(g.w, g.h, g.batch, false, true));  // sizes hold max keys
   CclScratch cs;
-  ccl_scratch_carve(s.p, g.w, g.h, g.batch, false, false, &cs);
+  ccl_scratch_carve(s.p, g.w, g.h, g.batch, false, true, &cs);
   ctx->launches += launch_ccl(words(a.p), words(out.p), g, cs, ctx->stream);
   return out.release();
 }
@@ -476,6 +476,18 @@ int slcs_image_to_device(slcs_ctx* ctx, const slcs_image* img, void* dev, size_t
   return guard([&] {
     LOCKED(ctx);
     download(ctx, img, dev, bytes, true);
+  });
+}
+
+int slcs_random_mask(slcs_ctx* ctx, int w, int h, long long row0, uint64_t seed, double density,
+                     slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    if (row0 < 0) fail(SLCS_ERR_ARG, "row0 must be >= 0");
+    Ref img(new_image(ctx, SLCS_BOOL, w, h, 1));
+    ctx->launches += launch_random_mask(words(img.p), img.p->geo, row0, seed, density, ctx->stream);
+    *out = img.release();
   });
 }
 

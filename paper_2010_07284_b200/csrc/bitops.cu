@@ -335,6 +335,34 @@ __global__ void k_volume(const uint4* __restrict__ a, size_t slice4,
   }
 }
 
+// randomMask (tests/oracles.cpp:44-49) on device: pixel i of the full image
+// consumes draw i of splitmix64(seed) (rng.hpp:14-19), so any row band is
+// generated independently and bit-identically to the CPU fixture.
+__global__ void k_random_mask(uint32_t* __restrict__ bits, int w, int h, long long row0,
+                              int wpr, size_t pitch, unsigned long long seed, double density) {
+  const size_t n = pitch * size_t(h);
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = q / pitch;
+    const int j = int(q - r * pitch);
+    uint32_t word = 0;
+    if (j < wpr) {
+      const unsigned long long base =
+          (unsigned long long)(row0 + (long long)r) * (unsigned long long)w + 32ull * j;
+      const int nb = min(32, w - 32 * j);
+      for (int b = 0; b < nb; ++b) {
+        unsigned long long z = seed + (base + b + 1ull) * 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        const double u = double(z >> 11) * 0x1.0p-53;
+        word |= (u < density ? 1u : 0u) << b;
+      }
+    }
+    bits[q] = word;
+  }
+}
+
 __global__ void k_counts_to_double(const unsigned long long* c, double* out, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = double(c[i]);
@@ -420,6 +448,14 @@ int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, c
   if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 8 + g.batch - 1) / g.batch));
   dim3 grid(unsigned(gx), unsigned(g.batch));
   k_volume<<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint4*>(a), n4, counts);
+  return 1;
+}
+
+int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned long long seed,
+                       double density, cudaStream_t st) {
+  size_t n = g.slice;
+  k_random_mask<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(bits, g.w, g.h, row0, g.wpr,
+                                                                      g.pitch, seed, density);
   return 1;
 }
 

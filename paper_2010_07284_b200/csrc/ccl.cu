@@ -100,22 +100,40 @@ __device__ __forceinline__ void run_max(uint32_t T, uint32_t B, uint32_t m, int&
 
 __device__ __forceinline__ uint32_t dil1(uint32_t x) { return x | (x << 1) | (x >> 1); }
 
-// ---- global union-find over P (values = packed key + 1, 0 = none) -----------
-__device__ __forceinline__ uint32_t gblk(const G& g, uint32_t v) {
-  const uint32_t k = v - 1u;
+// ---- global union-find over P ------------------------------------------------
+// Global nodes are identified by an invertible hash of their key, and unions
+// hang the smaller id under the larger: random priorities keep the trees
+// O(log n) deep.  (Max-key linking over a regular grid of tiles builds
+// linear chains -- tile after tile along a row, row after row -- and every
+// find then walks ~20 dependent L2 hops.)  The canonical max key of a
+// component is carried separately where labels need it (MK).
+constexpr uint32_t HMUL = 0x9E3779B1u, HINV = 0x0E8B2F51u;
+__device__ __forceinline__ uint32_t hnode(uint32_t key) {
+  return (key ^ (key >> 16)) * HMUL;
+}
+__device__ __forceinline__ uint32_t hkey(uint32_t node) {
+  const uint32_t x = node * HINV;
+  return x ^ (x >> 16);
+}
+__device__ __forceinline__ uint32_t kblk(const G& g, uint32_t k) {
   return ((k >> g.s) >> 1) * uint32_t(g.BW) + ((k & g.cmask) >> 1);
 }
+// parent slot of a node: the 2x2 block of its key
+__device__ __forceinline__ uint32_t gblk(const G& g, uint32_t n) { return kblk(g, hkey(n)); }
 
-__device__ __forceinline__ uint32_t gkey1(const G& g, int row, int col) {
-  return ((uint32_t(row) << g.s) | uint32_t(col)) + 1u;
+__device__ __forceinline__ uint32_t gkey(const G& g, int row, int col) {
+  return (uint32_t(row) << g.s) | uint32_t(col);
+}
+__device__ __forceinline__ uint32_t gnode(const G& g, int row, int col) {
+  return hnode(gkey(g, row, col));
 }
 
-// global key+1 of the run m of word j in band k
+// global node of the run m of word j in band k
 __device__ __forceinline__ uint32_t grun(const G& g, int k, int j, uint32_t T, uint32_t B,
                                          uint32_t m) {
   int dr, col;
   run_max(T, B, m, dr, col);
-  return gkey1(g, 2 * k + dr, 32 * j + col);
+  return gnode(g, 2 * k + dr, 32 * j + col);
 }
 
 // find during concurrent unions: L2-coherent loads, path halving
@@ -175,8 +193,7 @@ __device__ __forceinline__ uint32_t gfind_ro(const uint32_t* P, const G& g, uint
   return v;
 }
 
-__device__ __forceinline__ uint32_t linear_label(const G& g, uint32_t v) {
-  const uint32_t k = v - 1u;
+__device__ __forceinline__ uint32_t linear_label(const G& g, uint32_t k) {
   return (k >> g.s) * uint32_t(g.W) + (k & g.cmask) + 1u;
 }
 
@@ -305,14 +322,14 @@ struct RunTile {
 };
 
 // ===========================================================================
-// Large-image path: 128x128-px tiles (64 bands x 4 words = 256 threads).
-constexpr int LKW = 7;
-constexpr int LTWW = 4;
-constexpr int LTNB = 64;
-constexpr int LUNITS = LTNB * LTWW;              // 256
-constexpr int LSLOTS = LTNB * (1 << (LKW - 1));  // 4096 blocks per tile
-constexpr int LT_LIST = 256;                     // per-tile list: count + ring roots
-constexpr int LT_THREADS = 256;
+// Large-image path: 256x256-px tiles (128 bands x 8 words = 1024 threads).
+constexpr int LKW = 8;
+constexpr int LTWW = 8;
+constexpr int LTNB = 128;
+constexpr int LUNITS = LTNB * LTWW;              // 1024
+constexpr int LSLOTS = LTNB * (1 << (LKW - 1));  // 16384 blocks per tile
+constexpr int LT_LIST = 520;                     // count + <= 512 ring roots
+constexpr int LT_THREADS = LUNITS;
 
 enum { MODE_CCL = 0, MODE_REACH = 1, MODE_SIZE = 2 };
 
@@ -327,11 +344,13 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
                                                            uint8_t* __restrict__ F,
                                                            uint32_t* __restrict__ SZ,
                                                            uint32_t* __restrict__ lists, G g) {
-  __shared__ uint32_t par[LSLOTS];
-  __shared__ uint32_t sT[LUNITS], sB[LUNITS];
-  __shared__ uint8_t touch[LSLOTS];
-  __shared__ uint8_t fl[MODE == MODE_REACH ? LSLOTS : 4];
-  __shared__ uint32_t lsz[MODE == MODE_SIZE ? LSLOTS : 1];
+  extern __shared__ __align__(16) unsigned char lsm[];
+  uint32_t* par = reinterpret_cast<uint32_t*>(lsm);           // LSLOTS
+  uint32_t* sT = par + LSLOTS;                                 // LUNITS
+  uint32_t* sB = sT + LUNITS;                                  // LUNITS
+  uint32_t* lsz = sB + LUNITS;                                 // LSLOTS (MODE_SIZE)
+  uint8_t* touch = reinterpret_cast<uint8_t*>(lsz + (MODE == MODE_SIZE ? LSLOTS : 0));
+  uint8_t* fl = touch + LSLOTS;                                // LSLOTS (MODE_REACH)
   __shared__ int s_cnt;
   using T = RunTile<LKW>;
   const int slice = blockIdx.z;
@@ -379,8 +398,8 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
         const uint32_t root = rt[i];
-        Ps[gblk(g, gkey1(g, R0 + int(k >> LKW), C0 + int(k & lmask)))] =
-            gkey1(g, R0 + int(root >> LKW), C0 + int(root & lmask));
+        Ps[kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask)))] =
+            gnode(g, R0 + int(root >> LKW), C0 + int(root & lmask));
         const int rs = T::slot(root);
         if (band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31)))
           touch[rs] = 1;
@@ -403,10 +422,12 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
         const uint32_t k = T::key(band, w, Tw, Bw, m);
         if (rt[i] == k) {  // local root
           const int ks = T::slot(k);
-          const uint32_t gk = gkey1(g, R0 + int(k >> LKW), C0 + int(k & lmask));
-          if (MODE == MODE_REACH) F[size_t(slice) * g.sb + gblk(g, gk)] = fl[ks];
-          if (MODE == MODE_SIZE) SZ[size_t(slice) * g.sb + gblk(g, gk)] = lsz[ks];
-          if (touch[ks]) L[1 + atomicAdd(&s_cnt, 1)] = gk;
+          const uint32_t gk = gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask));
+          const uint32_t b = kblk(g, gk);
+          if (MODE == MODE_REACH) F[size_t(slice) * g.sb + b] = fl[ks];
+          if (MODE == MODE_SIZE) SZ[size_t(slice) * g.sb + b] = lsz[ks];
+          if (MODE == MODE_CCL && SZ) SZ[size_t(slice) * g.sb + b] = gk;  // max key (MK)
+          if (touch[ks]) L[1 + atomicAdd(&s_cnt, 1)] = hnode(gk);
         }
       }
     }
@@ -430,25 +451,31 @@ __device__ __forceinline__ void load_unit(const uint32_t* u, const G& g, int k, 
 // against the band above (all three column offsets).  Part B: the word pair
 // straddling every vertical tile border (the horizontal link, and the two
 // diagonals into the band above when that band is in the same tile row).
+template <int PART>
 __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G g, int nhb,
                              int nvb) {
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t nA = uint32_t(nhb) * uint32_t(g.wpr), nB = uint32_t(nvb) * uint32_t(g.BH);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nA + nB;
+  const uint32_t lo = PART == 0 ? 0u : nA, hi = PART == 0 ? nA : nA + nB;
+  for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi;
        i += gridDim.x * blockDim.x) {
     if (i < nA) {
       const int t = int(i / uint32_t(g.wpr)), j = int(i - uint32_t(t) * uint32_t(g.wpr));
       const int k = (t + 1) * LTNB;
       uint32_t T, B, Tu, Bu;
       load_unit(u, g, k, j, T, B);
-      if (!T) continue;
       load_unit(u, g, k - 1, j, Tu, Bu);
       uint32_t Tl = 0, Bl = 0, Tr = 0, Br = 0;
       if (T & 1u) load_unit(u, g, k - 1, j - 1, Tl, Bl);
       if (T >> 31) load_unit(u, g, k - 1, j + 1, Tr, Br);
       const uint32_t cu = Tu | Bu;
+      // the first link of every word goes through the warp dedupe (along a
+      // solid stretch of border all words link the same two local roots);
+      // any further links are united directly
+      bool first = true;
+      uint32_t fa = 0, fb = 0;
       for (uint32_t x = T | B; x;) {
         const uint32_t m = first_run(x);
         x &= ~m;
@@ -458,13 +485,21 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
         for (uint32_t a = dil1(td) & Bu; a;) {
           const uint32_t mu = run_at(cu, __ffs(a) - 1);
           a &= ~mu;
-          gunite(Ps, g, v, grun(g, k - 1, j, Tu, Bu, mu));
+          const uint32_t w = grun(g, k - 1, j, Tu, Bu, mu);
+          if (first) {
+            fa = v;
+            fb = w;
+            first = false;
+          } else {
+            gunite(Ps, g, v, w);
+          }
         }
         if ((td & 1u) && (Bl >> 31))
           gunite(Ps, g, v, grun(g, k - 1, j - 1, Tl, Bl, run_at(Tl | Bl, 31)));
         if ((td >> 31) && (Br & 1u))
           gunite(Ps, g, v, grun(g, k - 1, j + 1, Tr, Br, run_at(Tr | Br, 0)));
       }
+      gunite_dedup(Ps, g, fa, fb, !first);
     } else {
       const uint32_t i2 = i - nA;
       const int t = int(i2 / uint32_t(g.BH)), k = int(i2 - uint32_t(t) * uint32_t(g.BH));
@@ -516,6 +551,9 @@ __global__ void k_root_flatten(uint32_t* P, uint8_t* F, uint32_t* SZ,
       } else if (mode == MODE_SIZE) {
         uint32_t* Ss = SZ + size_t(slice) * g.sb;
         atomicAdd(Ss + gblk(g, R), Ss[gblk(g, rv)]);
+      } else if (SZ) {  // MODE_CCL: SZ holds the max key of each root (MK)
+        uint32_t* Ss = SZ + size_t(slice) * g.sb;
+        atomicMax(Ss + gblk(g, R), Ss[gblk(g, rv)]);
       }
     }
   }
@@ -636,10 +674,11 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
 
 // labels: per word, each run's pixels get linear(global root) + 1
 __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
-                              uint32_t* __restrict__ L, G g) {
+                              const uint32_t* __restrict__ MKall, uint32_t* __restrict__ L, G g) {
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
+  const uint32_t* MK = MKall + size_t(slice) * g.sb;
   uint32_t* Ls = L + size_t(slice) * size_t(g.W) * size_t(g.H);
   const uint32_t n = uint32_t(g.BH) * uint32_t(g.wpr);
   const bool vec = (g.W & 3) == 0;
@@ -659,7 +698,7 @@ __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t
           const uint32_t m = first_run(x);
           x &= ~m;
           starts |= m & (0u - m);
-          labs[q] = linear_label(g, groot(Ps, g, grun(g, k, j, T, B, m)));
+          labs[q] = linear_label(g, MK[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))]);
         }
       }
     }
@@ -984,29 +1023,54 @@ void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool siz
   }
 }
 
+template <int MODE>
+size_t tile_smem() {
+  return size_t(LSLOTS) * 4 + 2 * size_t(LUNITS) * 4 + (MODE == MODE_SIZE ? size_t(LSLOTS) * 4 : 0) +
+         2 * size_t(LSLOTS) + 16;
+}
+
+template <int MODE>
+void tile_launch(dim3 grid, const uint32_t* u, const uint32_t* t, CclScratch& s, const G& g,
+                 cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tile_local<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(tile_smem<MODE>()));
+    attr = true;
+  }
+  k_tile_local<MODE><<<grid, LT_THREADS, tile_smem<MODE>(), st>>>(u, t, s.parent, s.flag, s.size,
+                                                                 s.lists, g);
+}
+
 static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G& g, int batch,
                                   CclScratch& s, int mode, cudaStream_t st, int& launches) {
   dim3 grid(unsigned((g.wpr + LTWW - 1) / LTWW), unsigned((g.BH + LTNB - 1) / LTNB),
             unsigned(batch));
   if (mode == MODE_REACH)
-    k_tile_local<MODE_REACH><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, s.size,
-                                                          s.lists, g);
+    tile_launch<MODE_REACH>(grid, u, t, s, g, st);
   else if (mode == MODE_SIZE)
-    k_tile_local<MODE_SIZE><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, s.size,
-                                                         s.lists, g);
+    tile_launch<MODE_SIZE>(grid, u, t, s, g, st);
   else
-    k_tile_local<MODE_CCL><<<grid, LT_THREADS, 0, st>>>(u, t, s.parent, s.flag, s.size,
-                                                        s.lists, g);
+    tile_launch<MODE_CCL>(grid, u, t, s, g, st);
   ++launches;
   const int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
   const size_t links = size_t(nhb) * g.wpr + size_t(nvb) * g.BH;
   if (links) {
-    dim3 mg(unsigned(grid_blocks(links, 256)), unsigned(batch));
-    k_tile_merge<<<mg, 256, 0, st>>>(u, s.parent, g, nhb, nvb);
+    const size_t la = size_t(nhb) * g.wpr, lb = size_t(nvb) * g.BH;
+    if (la) {
+      dim3 mg(unsigned(grid_blocks(la, 256)), unsigned(batch));
+      k_tile_merge<0><<<mg, 256, 0, st>>>(u, s.parent, g, nhb, nvb);
+      ++launches;
+    }
+    if (lb) {
+      dim3 mg(unsigned(grid_blocks(lb, 256)), unsigned(batch));
+      k_tile_merge<1><<<mg, 256, 0, st>>>(u, s.parent, g, nhb, nvb);
+      ++launches;
+    }
     const int ntiles = int(grid.x * grid.y);
     dim3 fg(unsigned((ntiles * 32 + 255) / 256), unsigned(batch));
     k_root_flatten<<<fg, 256, 0, st>>>(s.parent, s.flag, s.size, s.lists, g, ntiles, mode);
-    launches += 2;
+    launches += 1;
   }
 }
 
@@ -1031,14 +1095,14 @@ int launch_epoch_bump(uint32_t* epoch, cudaStream_t st) {
 
 int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,
                          uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
-                         uint32_t* tmp_bits, const Geo& gb, cudaStream_t st) {
+                         uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out) {
   G g = make_g(gb);
   const uint32_t* P = static_cast<const uint32_t*>(labels);
   dim3 ug(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
   k_reach_seed<<<ug, 256, 0, st>>>(through, target, P, flags32, epoch, idx, g);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
   k_reach_select_gen<<<sg, 256, 0, st>>>(through, target, P, flags32, epoch, idx, tmp_bits, g);
-  return 2 + launch_near(tmp_bits, out, gb, 1, false, st);
+  return 2 + launch_near(tmp_bits, out, gb, k_out, false, st);
 }
 
 int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,
@@ -1051,21 +1115,24 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   int launches = 0;
   large_local_and_merge(bits, nullptr, g, gb.batch, s, MODE_CCL, st, launches);
   dim3 lg(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
-  k_tile_labels<<<lg, 256, 0, st>>>(bits, s.parent, labels, g);
+  k_tile_labels<<<lg, 256, 0, st>>>(bits, s.parent, s.size, labels, g);
   return launches + 1;
 }
 
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
-                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st) {
+                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st, int k_out) {
   G g = make_g(gb);
-  if (ccl_small_path(gb.w, gb.h)) return small_launch<1>(through, target, out, g, gb.batch, st);
+  if (ccl_small_path(gb.w, gb.h)) {
+    if (k_out != 1) fail(SLCS_ERR_ARG, "reach: closing radius > 1 needs the tiled path");
+    return small_launch<1>(through, target, out, g, gb.batch, st);
+  }
   check_key_range(gb, "reach");
   int launches = 0;
   large_local_and_merge(through, target, g, gb.batch, s, MODE_REACH, st, launches);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
   k_reach_select<<<sg, 256, 0, st>>>(through, target, s.parent, s.flag, tmp_bits, g);
   launches += 1;
-  launches += launch_near(tmp_bits, out, gb, 1, false, st);
+  launches += launch_near(tmp_bits, out, gb, k_out, false, st);
   return launches;
 }
 

@@ -698,6 +698,19 @@ struct slcs_program {
           n.in[0] = m.in[0];
           m.dead = true;
         }
+        // near(reach(t, u)): reach closes with near(t | S), so a following
+        // near widens that closing stencil instead of running separately
+        LG& m = lgs[n.in[0]];
+        if (!n.erode && m.kind == LG_REACH && m.consumers == 1 && !m.output &&
+            !ccl_small_path(m.w, m.h) && n.k + m.k <= 8) {
+          const int k = n.k + m.k;
+          const bool out = n.output;
+          LG merged = m;
+          merged.k = k;
+          merged.output = out;
+          m.dead = true;
+          n = merged;
+        }
       }
     }
 
@@ -812,6 +825,7 @@ struct slcs_program {
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
       if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
+      if (n.kind == LG_REACH && n.k > 1) os << " closing near^" << n.k;
       os << " " << n.w << "x" << n.h;
       if (n.batch > 1) os << "x" << n.batch;
       os << " in=[";
@@ -924,7 +938,7 @@ struct slcs_program {
                 static_cast<const uint32_t*>(lgs[n.in[1]].ptr), lab.ptr,
                 reinterpret_cast<uint32_t*>(static_cast<char*>(lab.ptr) + lb), d_epoch,
                 uint32_t(n.gen_idx), static_cast<uint32_t*>(n.ptr),
-                static_cast<uint32_t*>(scratch), gb, st);
+                static_cast<uint32_t*>(scratch), gb, st, n.k);
             break;
           }
           CclScratch cs;
@@ -935,7 +949,7 @@ struct slcs_program {
                               : reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + sb);
           launches += launch_reach(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
                                    static_cast<const uint32_t*>(lgs[n.in[1]].ptr),
-                                   static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st);
+                                   static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st, n.k);
           break;
         }
         case LG_MAXVOL: {

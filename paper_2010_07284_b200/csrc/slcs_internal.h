@@ -88,6 +88,9 @@ int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
 int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
                 cudaStream_t st);
 int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, cudaStream_t st);
+// rows [row0, row0 + g.h) of randomMask(g.w x H, density, Rng(seed)) as bits
+int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned long long seed,
+                       double density, cudaStream_t st);
 // counts (u64 per slice) -> doubles (for device-side number values)
 int launch_counts_to_double(const unsigned long long* counts, double* out, int n,
                             cudaStream_t st);
@@ -135,8 +138,10 @@ void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool siz
 bool ccl_small_path(int w, int h);
 int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,
                cudaStream_t st);
+// k_out: radius of the closing near (1 = reach; > 1 absorbs following nears)
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
-                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st);
+                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st,
+                 int k_out = 1);
 int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
                   cudaStream_t st);
 // label CSE: one labelling of `through` (large path only), reused by many reaches
@@ -146,7 +151,7 @@ int launch_epoch_bump(uint32_t* epoch, cudaStream_t st);
 // flags32: one uint32 per 2x2 block (generation stamps); idx < 4096 per run
 int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,
                          uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
-                         uint32_t* tmp_bits, const Geo& gb, cudaStream_t st);
+                         uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out = 1);
 
 }  // namespace slcs
 

@@ -429,6 +429,17 @@ def surrounded(a: Image, b: Image, device: Optional[Device] = None):
     return kernels.logicalAnd(a, kernels.logicalNot(reach(notAB, notB, device), device), device)
 
 
+def random_mask_device(w: int, h: int, density: float, seed: int, row0: int = 0,
+                       device: Optional[Device] = None) -> DeviceImage:
+    """Rows [row0, row0+h) of randomMask(w, H, density, Rng(seed)), generated on the GPU
+    (bit-identical to the reference fixture, tests/oracles.cpp:44-49)."""
+    device = device or Device.default()
+    out = C.c_void_p()
+    _check(_lib.load().slcs_random_mask(device.handle, w, h, row0, seed, float(density),
+                                        C.byref(out)))
+    return DeviceImage(out, device)
+
+
 def mask(pattern: str) -> ImageBuffer:
     """ASCII mask helper of tests/oracles.cpp:20-42 ('x', '#', '1' set; '/' rows)."""
     rows = [r for r in pattern.replace("\n", "/").split("/") if r != ""]

@@ -225,3 +225,13 @@ def test_u16_coerces_to_mask_where_booleans_are_expected(dev):
     assert out[0] == 2
     with pytest.raises(RunError, match="expects a boolean image, got u16"):
         kernels.logicalNot(du)
+
+
+def test_device_random_mask_matches_reference_stream(dev):
+    from paper_2010_07284_b200.pixlog import random_mask_device
+    for (w, h, d, seed) in [(37, 19, 0.5, 7), (300, 200, 0.41, 1), (64, 64, 0.05, 2)]:
+        full = O.random_mask(w, h, d, O.Rng(seed))
+        assert np.array_equal(random_mask_device(w, h, d, seed, 0, dev).numpy(), full)
+        # a band starting mid-image continues the same stream
+        band = random_mask_device(w, 7, d, seed, 5, dev).numpy()
+        assert np.array_equal(band, full[5:12])
