@@ -134,6 +134,26 @@ int slcs_reach(slcs_ctx* ctx, const slcs_image* target, const slcs_image* throug
  * count (ties keep all maxima; per slice for batches).  No reference pin. */
 int slcs_maxvol(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
 
+/* ---- row bands (multi-GPU) ------------------------------------
+ * A 65536^2 image is split into row bands, one per GPU.  reach is run in
+ * phases so bands can be stitched: prepare labels `through` and flags the
+ * components holding a seed (through & near(target)); reach_row exports, per
+ * pixel of one row, the component's root node and a class byte (0 background,
+ * 1 unseeded, 2 seeded); the host resolves cross-band components and hands the
+ * roots that became seeded back with reach_set_flags; finish writes
+ * near^k_out(target | selected components) (k_out = 0: no closing near). */
+typedef struct slcs_reach_state slcs_reach_state;
+int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+                       slcs_reach_state** out);
+int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls);
+int slcs_reach_set_flags(slcs_reach_state* st, int n, const uint32_t* roots);
+int slcs_reach_finish(slcs_reach_state* st, int k_out, slcs_image** out);
+int slcs_reach_state_destroy(slcs_reach_state* st);
+/* Rows [row0, row0 + nrows) of an image / vertical concatenation (same kind
+ * and width) -- halo assembly for banded stencils. */
+int slcs_image_rows(slcs_ctx* ctx, const slcs_image* img, int row0, int nrows, slcs_image** out);
+int slcs_image_vstack(slcs_ctx* ctx, int n, const slcs_image* const* imgs, slcs_image** out);
+
 /* ---- host-in / host-out wrappers with the reference signatures -----------
  * kernels::threshold / logicalNot / logicalAnd / logicalOr / dilate /
  * countTrue, ccl::label, reach -- for callers holding host ImageBuffers. */

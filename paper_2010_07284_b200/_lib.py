@@ -54,6 +54,13 @@ _SIGS = {
     "slcs_ccl": (i32, [vp, vp, pvp]),
     "slcs_reach": (i32, [vp, vp, vp, pvp]),
     "slcs_maxvol": (i32, [vp, vp, pvp]),
+    "slcs_reach_prepare": (i32, [vp, vp, vp, pvp]),
+    "slcs_reach_row": (i32, [vp, i32, vp, vp]),
+    "slcs_reach_set_flags": (i32, [vp, i32, vp]),
+    "slcs_reach_finish": (i32, [vp, i32, pvp]),
+    "slcs_reach_state_destroy": (i32, [vp]),
+    "slcs_image_rows": (i32, [vp, vp, i32, i32, pvp]),
+    "slcs_image_vstack": (i32, [vp, i32, C.POINTER(vp), pvp]),
     "slcs_h_threshold": (i32, [vp, i32, vp, i32, i32, dbl, vp]),
     "slcs_h_not": (i32, [vp, vp, i32, i32, vp]),
     "slcs_h_and": (i32, [vp, vp, vp, i32, i32, vp]),

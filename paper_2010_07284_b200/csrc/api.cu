@@ -569,6 +569,156 @@ int slcs_maxvol(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) {
   PRIM(*out = op_maxvol(ctx, a));
 }
 
+// ---- row bands ------------------------------------------------------------------
+int slcs_image_rows(slcs_ctx* ctx, const slcs_image* img, int row0, int nrows, slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    need_img(img);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    const Geo& g = img->geo;
+    if (g.batch != 1) fail(SLCS_ERR_ARG, "row crop needs a single image");
+    if (row0 < 0 || nrows < 1 || row0 + nrows > g.h) fail(SLCS_ERR_SHAPE, "row range out of image");
+    Ref o(new_image(ctx, img->kind, g.w, nrows, 1));
+    size_t rowb = g.pitch * unit_bytes(img->kind);
+    cuda_check(cudaMemcpyAsync(o.p->data, static_cast<char*>(img->data) + size_t(row0) * rowb,
+                               rowb * size_t(nrows), cudaMemcpyDeviceToDevice, ctx->stream),
+               "row crop");
+    *out = o.release();
+  });
+}
+
+int slcs_image_vstack(slcs_ctx* ctx, int n, const slcs_image* const* imgs, slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out || n < 1 || !imgs) fail(SLCS_ERR_ARG, "bad vstack arguments");
+    int h = 0;
+    for (int i = 0; i < n; ++i) {
+      need_img(imgs[i]);
+      if (imgs[i]->kind != imgs[0]->kind || imgs[i]->geo.w != imgs[0]->geo.w ||
+          imgs[i]->geo.batch != 1)
+        fail(SLCS_ERR_SHAPE, "vstack: images must share kind and width");
+      h += imgs[i]->geo.h;
+    }
+    Ref o(new_image(ctx, imgs[0]->kind, imgs[0]->geo.w, h, 1));
+    size_t rowb = imgs[0]->geo.pitch * unit_bytes(imgs[0]->kind), off = 0;
+    for (int i = 0; i < n; ++i) {
+      size_t b = rowb * size_t(imgs[i]->geo.h);
+      cuda_check(cudaMemcpyAsync(static_cast<char*>(o.p->data) + off, imgs[i]->data, b,
+                                 cudaMemcpyDeviceToDevice, ctx->stream),
+                 "vstack");
+      off += b;
+    }
+    *out = o.release();
+  });
+}
+
+}  // extern "C"
+
+struct slcs_reach_state {
+  slcs_ctx* ctx = nullptr;
+  slcs_image* t = nullptr;
+  slcs_image* u = nullptr;
+  void* scratch = nullptr;
+  CclScratch cs;
+  uint32_t* tmp = nullptr;
+  uint32_t* d_roots = nullptr;
+  uint8_t* d_cls = nullptr;
+  int d_cap = 0;
+};
+
+extern "C" {
+
+int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+                       slcs_reach_state** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    Ref t(bool_arg(ctx, target, "reach"));
+    Ref u(bool_arg(ctx, through, "reach"));
+    same_shape(t.p, u.p, "reach");
+    if (t.p->geo.batch != 1) fail(SLCS_ERR_ARG, "banded reach takes single images");
+    const Geo& g = t.p->geo;
+    auto* st = new slcs_reach_state;
+    st->ctx = ctx;
+    size_t sb = ccl_scratch_bytes_large(g.w, g.h, 1, true, false);
+    st->scratch = ctx->alloc(sb + g.slice * 4);
+    ccl_scratch_carve_large(st->scratch, g.w, g.h, 1, true, false, &st->cs);
+    st->tmp = reinterpret_cast<uint32_t*>(static_cast<char*>(st->scratch) + sb);
+    ctx->launches += launch_reach_prepare(words(t.p), words(u.p), g, st->cs, ctx->stream);
+    st->t = t.release();
+    st->u = u.release();
+    *out = st;
+  });
+}
+
+int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls) {
+  return guard([&] {
+    if (!st || !roots || !cls) fail(SLCS_ERR_ARG, "null argument");
+    slcs_ctx* ctx = st->ctx;
+    LOCKED(ctx);
+    const Geo& g = st->u->geo;
+    if (row < 0 || row >= g.h) fail(SLCS_ERR_SHAPE, "row out of image");
+    if (st->d_cap < g.w) {
+      ctx->release(st->d_roots);
+      ctx->release(st->d_cls);
+      st->d_roots = static_cast<uint32_t*>(ctx->alloc(size_t(g.w) * 4));
+      st->d_cls = static_cast<uint8_t*>(ctx->alloc(size_t(g.w)));
+      st->d_cap = g.w;
+    }
+    ctx->launches += launch_reach_row(words(st->u), st->cs, g, row, st->d_roots, st->d_cls,
+                                      ctx->stream);
+    cuda_check(cudaMemcpyAsync(roots, st->d_roots, size_t(g.w) * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream), "row roots");
+    cuda_check(cudaMemcpyAsync(cls, st->d_cls, size_t(g.w), cudaMemcpyDeviceToHost, ctx->stream),
+               "row classes");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "row sync");
+  });
+}
+
+int slcs_reach_set_flags(slcs_reach_state* st, int n, const uint32_t* roots) {
+  return guard([&] {
+    if (!st || (n > 0 && !roots)) fail(SLCS_ERR_ARG, "null argument");
+    if (n <= 0) return;
+    slcs_ctx* ctx = st->ctx;
+    LOCKED(ctx);
+    uint32_t* d = static_cast<uint32_t*>(ctx->alloc(size_t(n) * 4));
+    cuda_check(cudaMemcpyAsync(d, roots, size_t(n) * 4, cudaMemcpyHostToDevice, ctx->stream),
+               "flags upload");
+    ctx->launches += launch_reach_set_flags(st->cs, st->u->geo, d, n, ctx->stream);
+    ctx->release(d);
+  });
+}
+
+int slcs_reach_finish(slcs_reach_state* st, int k_out, slcs_image** out) {
+  return guard([&] {
+    if (!st || !out) fail(SLCS_ERR_ARG, "null argument");
+    if (k_out < 0 || k_out > 8) fail(SLCS_ERR_ARG, "closing radius must be in 0..8");
+    slcs_ctx* ctx = st->ctx;
+    LOCKED(ctx);
+    const Geo& g = st->u->geo;
+    Ref o(new_image(ctx, SLCS_BOOL, g.w, g.h, 1));
+    ctx->launches += launch_reach_finish(words(st->t), words(st->u), st->cs, words(o.p), st->tmp,
+                                         g, k_out, ctx->stream);
+    *out = o.release();
+  });
+}
+
+int slcs_reach_state_destroy(slcs_reach_state* st) {
+  return guard([&] {
+    if (!st) return;
+    slcs_ctx* ctx = st->ctx;
+    {
+      LOCKED(ctx);
+      ctx->release(st->scratch);
+      ctx->release(st->d_roots);
+      ctx->release(st->d_cls);
+    }
+    slcs_image_release(st->t);
+    slcs_image_release(st->u);
+    delete st;
+  });
+}
+
 // ---- host-in / host-out wrappers ------------------------------------------------
 }  // extern "C"
 

@@ -665,6 +665,48 @@ __global__ void k_reach_select_gen(const uint32_t* __restrict__ ubits,
   }
 }
 
+// ---- row-band support (multi-GPU) ------------------------------------
+// Per pixel of row r: the global root node of its through-component and a
+// class byte (0 background, 1 unseeded, 2 seeded).  Used to stitch bands.
+__global__ void k_band_row(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
+                           const uint8_t* __restrict__ F, int r, uint32_t* __restrict__ roots,
+                           uint8_t* __restrict__ cls, G g) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= g.wpr) return;
+  const int k = r >> 1;
+  uint32_t T, B;
+  {
+    const uint32_t* row = ubits + size_t(2 * k) * g.pitch + j;
+    T = __ldg(row);
+    B = 2 * k + 1 < g.H ? __ldg(row + g.pitch) : 0u;
+  }
+  const uint32_t mine = (r & 1) ? B : T;
+  const int c0 = 32 * j, ncol = min(32, g.W - c0);
+  for (int b = 0; b < ncol; ++b) {
+    roots[c0 + b] = 0;
+    cls[c0 + b] = 0;
+  }
+  for (uint32_t x = T | B; x;) {
+    const uint32_t m = first_run(x);
+    x &= ~m;
+    const uint32_t px = mine & m;
+    if (!px) continue;
+    const uint32_t R = groot(P, g, grun(g, k, j, T, B, m));
+    const uint8_t c = F[gblk(g, R)] ? 2 : 1;
+    for (uint32_t y = px; y;) {
+      const int b = __ffs(y) - 1;
+      y &= y - 1;
+      roots[c0 + b] = R;
+      cls[c0 + b] = c;
+    }
+  }
+}
+
+__global__ void k_band_set_flags(const uint32_t* __restrict__ roots, int n, uint8_t* F, G g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) F[gblk(g, roots[i])] = 1;
+}
+
 __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
   uint32_t lab = 0;
 #pragma unroll
@@ -979,7 +1021,7 @@ void check_key_range(const Geo& gb, const char* what) {
   KeyGeo k = key_geo(gb.w, gb.h);
   unsigned long long maxkey =
       ((unsigned long long)(gb.h - 1) << k.s) | (unsigned long long)(gb.w - 1);
-  if (maxkey + 1 >= 0xffffffffull)
+  if (maxkey > 0xffffffffull)
     fail(SLCS_ERR_TOO_LARGE, std::string(what) + ": image too large for 32-bit run keys");
 }
 
@@ -993,6 +1035,10 @@ static size_t n_tiles(int w, int h) {
 
 size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes) {
   if (ccl_small_path(w, h)) return 0;
+  return ccl_scratch_bytes_large(w, h, batch, flags, sizes);
+}
+
+size_t ccl_scratch_bytes_large(int w, int h, int batch, bool flags, bool sizes) {
   KeyGeo k = key_geo(w, h);
   size_t n = k.slice_blocks * size_t(batch);
   size_t b = round_up(n * 4, 256) + round_up(n_tiles(w, h) * size_t(batch) * LT_LIST * 4, 256);
@@ -1005,6 +1051,12 @@ void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool siz
                        CclScratch* s) {
   *s = CclScratch{};
   if (ccl_small_path(w, h)) return;
+  ccl_scratch_carve_large(base, w, h, batch, flags, sizes, s);
+}
+
+void ccl_scratch_carve_large(void* base, int w, int h, int batch, bool flags, bool sizes,
+                             CclScratch* s) {
+  *s = CclScratch{};
   KeyGeo k = key_geo(w, h);
   size_t n = k.slice_blocks * size_t(batch);
   unsigned char* p = static_cast<unsigned char*>(base);
@@ -1103,6 +1155,42 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
   k_reach_select_gen<<<sg, 256, 0, st>>>(through, target, P, flags32, epoch, idx, tmp_bits, g);
   return 2 + launch_near(tmp_bits, out, gb, k_out, false, st);
+}
+
+// reach split in phases for row bands: prepare (labels + seed flags), export a
+// row's roots/classes, import resolved flags, finish (select [+ closing near])
+int launch_reach_prepare(const uint32_t* target, const uint32_t* through, const Geo& gb,
+                         CclScratch& s, cudaStream_t st) {
+  check_key_range(gb, "reach");
+  G g = make_g(gb);
+  int launches = 0;
+  large_local_and_merge(through, target, g, gb.batch, s, MODE_REACH, st, launches);
+  return launches;
+}
+
+int launch_reach_row(const uint32_t* through, const CclScratch& s, const Geo& gb, int row,
+                     uint32_t* roots, uint8_t* cls, cudaStream_t st) {
+  G g = make_g(gb);
+  k_band_row<<<(g.wpr + 127) / 128, 128, 0, st>>>(through, s.parent, s.flag, row, roots, cls, g);
+  return 1;
+}
+
+int launch_reach_set_flags(const CclScratch& s, const Geo& gb, const uint32_t* roots, int n,
+                           cudaStream_t st) {
+  if (n <= 0) return 0;
+  G g = make_g(gb);
+  k_band_set_flags<<<(n + 255) / 256, 256, 0, st>>>(roots, n, s.flag, g);
+  return 1;
+}
+
+int launch_reach_finish(const uint32_t* target, const uint32_t* through, const CclScratch& s,
+                        uint32_t* out, uint32_t* tmp_bits, const Geo& gb, int k_out,
+                        cudaStream_t st) {
+  G g = make_g(gb);
+  dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
+  uint32_t* dst = k_out > 0 ? tmp_bits : out;
+  k_reach_select<<<sg, 256, 0, st>>>(through, target, s.parent, s.flag, dst, g);
+  return 1 + (k_out > 0 ? launch_near(tmp_bits, out, gb, k_out, false, st) : 0);
 }
 
 int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,

@@ -136,6 +136,10 @@ size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes);
 void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool sizes,
                        CclScratch* s);
 bool ccl_small_path(int w, int h);
+// the tiled path's scratch regardless of size (row bands always use it)
+size_t ccl_scratch_bytes_large(int w, int h, int batch, bool flags, bool sizes);
+void ccl_scratch_carve_large(void* base, int w, int h, int batch, bool flags, bool sizes,
+                             CclScratch* s);
 int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,
                cudaStream_t st);
 // k_out: radius of the closing near (1 = reach; > 1 absorbs following nears)
@@ -144,6 +148,16 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
                  int k_out = 1);
 int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
                   cudaStream_t st);
+// row bands: reach in phases (large path always)
+int launch_reach_prepare(const uint32_t* target, const uint32_t* through, const Geo& gb,
+                         CclScratch& s, cudaStream_t st);
+int launch_reach_row(const uint32_t* through, const CclScratch& s, const Geo& gb, int row,
+                     uint32_t* roots, uint8_t* cls, cudaStream_t st);
+int launch_reach_set_flags(const CclScratch& s, const Geo& gb, const uint32_t* roots, int n,
+                           cudaStream_t st);
+int launch_reach_finish(const uint32_t* target, const uint32_t* through, const CclScratch& s,
+                        uint32_t* out, uint32_t* tmp_bits, const Geo& gb, int k_out,
+                        cudaStream_t st);
 // label CSE: one labelling of `through` (large path only), reused by many reaches
 size_t ccl_labels_bytes(int w, int h, int batch);
 int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStream_t st);

@@ -1,0 +1,129 @@
+"""CPU: the row-band protocol of paper_2010_07284_b200/bands.py.
+
+The device work of each band (band-local components, seed classes) is
+emulated with the oracle, so the host protocol -- border edges, the cross-band
+union-find, flag hand-back -- is checked against the full-image reach on CPU,
+in-process and across 2 processes with torch.distributed gloo.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2010_07284_b200.bands import band_rows, border_edges, resolve_border_flags
+
+
+def test_band_rows_partition():
+    for h in (1, 2, 7, 100, 65536):
+        for world in (1, 2, 3, 8):
+            if world > h:
+                continue
+            spans = [band_rows(h, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == h
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def emulate_band(t_full, u_full, r0, r1):
+    """What the device exports for one band: per-pixel (root, class) rows + labels."""
+    u = u_full[r0:r1]
+    lab = O.flood_fill_label(u)                 # band-local components
+    nt = O.dilate(t_full)[r0:r1]                # near(t) with the neighbours' halo rows
+    seeded = np.zeros(lab.max() + 1, bool)
+    seeded[lab[(u > 0) & (nt > 0)]] = True
+    seeded[0] = False
+    cls = np.where(lab > 0, np.where(seeded[lab], 2, 1), 0).astype(np.uint8)
+    roots = (lab * 2654435761).astype(np.uint32)  # any per-band unique ids
+    return lab, roots, cls, seeded
+
+
+def finish_band(lab, roots, seeded, newly):
+    extra = np.isin(roots, newly) & (lab > 0)
+    return (seeded[lab] & (lab > 0)) | extra
+
+
+def banded_reach_cpu(t, u, world):
+    h = t.shape[0]
+    parts = []
+    for r in range(world):
+        r0, r1 = band_rows(h, world, r)
+        lab, roots, cls, seeded = emulate_band(t, u, r0, r1)
+        parts.append((r0, r1, lab, roots, cls, seeded))
+    rows = [(p[3][0], p[4][0], p[3][-1], p[4][-1]) for p in parts]
+    newly = resolve_border_flags(rows)
+    S = np.zeros_like(u)
+    for (r0, r1, lab, roots, cls, seeded), nw in zip(parts, newly):
+        S[r0:r1] = finish_band(lab, roots, seeded, nw)
+    return O.dilate(O.logical_or(t, S.astype(np.uint8)))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+@pytest.mark.parametrize("w,h,ud", [(40, 37, 0.5), (64, 64, 0.41), (33, 90, 0.6)])
+def test_banded_reach_protocol_matches_full_image(world, w, h, ud):
+    rng = O.Rng(w * h + world)
+    t = O.random_mask(w, h, 0.02, rng)
+    u = O.random_mask(w, h, ud, rng)
+    assert np.array_equal(banded_reach_cpu(t, u, world), O.reach(t, u))
+
+
+def test_border_edges_use_8_connectivity():
+    last_cls = np.array([0, 1, 0, 0], np.uint8)
+    first_cls = np.array([0, 0, 1, 0], np.uint8)   # diagonal neighbour
+    e = border_edges(np.array([0, 7, 0, 0], np.uint32), last_cls,
+                     np.array([0, 0, 9, 0], np.uint32), first_cls)
+    assert e.tolist() == [[7, 9]]
+    first_cls = np.array([0, 0, 0, 1], np.uint8)   # two columns away: no edge
+    assert len(border_edges(np.array([0, 7, 0, 0], np.uint32), last_cls,
+                            np.array([0, 0, 0, 9], np.uint32), first_cls)) == 0
+
+
+def test_long_component_crossing_many_bands():
+    # a vertical line through every band, seeded only in the last band
+    h, w = 40, 9
+    u = np.zeros((h, w), np.uint8)
+    u[:, 4] = 1
+    t = np.zeros((h, w), np.uint8)
+    t[h - 1, 0] = 0
+    t[h - 1, 3] = 1
+    assert np.array_equal(banded_reach_cpu(t, u, 8), O.reach(t, u))
+
+
+def _gloo_worker(rank, world, port, t, u, out):
+    import torch.distributed as dist
+    from paper_2010_07284_b200.bands import TorchComm
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    comm = TorchComm()
+    r0, r1 = band_rows(t.shape[0], world, rank)
+    lab, roots, cls, seeded = emulate_band(t, u, r0, r1)
+    rows = comm.allgather((roots[0], cls[0], roots[-1], cls[-1]))
+    newly = resolve_border_flags(rows)[rank]
+    S = finish_band(lab, roots, seeded, newly).astype(np.uint8)
+    above, below = comm.neighbours(S[0] | t[r0], S[-1] | t[r1 - 1])
+    parts = comm.allgather(S)
+    assert comm.allreduce_sum(int(S.sum())) == sum(int(p.sum()) for p in parts)
+    if rank == 0:
+        out.put(np.concatenate(parts))
+    dist.destroy_process_group()
+
+
+def test_two_process_gloo_banded_reach():
+    import torch.multiprocessing as mp
+    rng = O.Rng(2024)
+    t = O.random_mask(48, 50, 0.03, rng)
+    u = O.random_mask(48, 50, 0.5, rng)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, t, u, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    S = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(O.dilate(O.logical_or(t, S)), O.reach(t, u))

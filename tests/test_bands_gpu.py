@@ -1,0 +1,49 @@
+"""GPU: the row-band path (bands.py) equals the single-image path bit-exactly.
+
+N bands run on one GPU through LocalGroup (the same protocol a torch.distributed
+job runs across GPUs: halo rows, border-row export, cross-band union-find,
+flag hand-back, halo-exchanged closing near)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2010_07284_b200 import DeviceImage, PixelKind, kernels, reach
+from paper_2010_07284_b200.bands import (LocalGroup, band_rows, near_banded, reach_banded,
+                                         volume_banded)
+
+pytestmark = pytest.mark.gpu
+
+
+def split(dev, a, world):
+    h = a.shape[0]
+    return [DeviceImage.upload(a[slice(*band_rows(h, world, r))], PixelKind.Bool, dev)
+            for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("w,h,ud", [(600, 517, 0.5), (1000, 1000, 0.41), (300, 257, 0.7)])
+def test_banded_reach_near_volume(dev, world, w, h, ud):
+    rng = O.Rng(w + h + world)
+    t = O.random_mask(w, h, 0.01, rng)
+    u = O.random_mask(w, h, ud, rng)
+    tb, ub = split(dev, t, world), split(dev, u, world)
+    grp = LocalGroup(world)
+    out = grp.run(lambda c, b: reach_banded(c, b[0], b[1]).numpy(), list(zip(tb, ub)))
+    assert np.array_equal(np.concatenate(out), O.reach(t, u))
+    near = grp.run(lambda c, b: near_banded(c, b, 2).numpy(), ub)
+    assert np.array_equal(np.concatenate(near), O.dilate(O.dilate(u)))
+    inter = grp.run(lambda c, b: near_banded(c, b, 1, erode=True).numpy(), ub)
+    assert np.array_equal(np.concatenate(inter), O.erode(u))
+    vol = grp.run(lambda c, b: volume_banded(c, b), ub)
+    assert all(v == int(u.sum()) for v in vol)
+
+
+def test_banded_reach_blob_giant_component(dev):
+    img = O.blob_noise(1024, 1024, 1)
+    t = O.threshold(0, img, 62258)
+    u = O.threshold(0, img, 56360)
+    for world in (2, 5):
+        tb, ub = split(dev, t, world), split(dev, u, world)
+        out = LocalGroup(world).run(lambda c, b: reach_banded(c, b[0], b[1]).numpy(),
+                                    list(zip(tb, ub)))
+        assert np.array_equal(np.concatenate(out), O.reach(t, u))
