@@ -50,7 +50,7 @@ def parse():
                    help="headline with label CSE on (reaches sharing one `through` node label "
                         "it once).  Default off: every reach node labels its own `through`, "
                         "exactly the reference's per-node work (reach.cpp:21)")
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                    help="BASELINE.json config: c2 (default, the headline) or the parity/"
                         "secondary workloads c1, c3 (sharded by slice under torchrun), c4")
     p.add_argument("--density", type=float, default=0.5, help="c4 mask density")
@@ -377,6 +377,77 @@ def c4_config(args, ws, rank, local):
             "cpu_baseline": cpu}), flush=True)
 
 
+def c5_config(args, ws, rank, local):
+    """c5: a 65536^2 random mask in row bands, one per rank (weak in pixels per GPU
+    only at N=1 vs N>1 on the same image: the image is fixed -> strong scaling).
+    Per step: near^4 (halo exchange), volume (all-reduce), reach (cross-band merge)."""
+    import torch
+
+    from paper_2010_07284_b200 import Device
+    from paper_2010_07284_b200.bands import (TorchComm, band_rows, near_banded, reach_banded,
+                                             volume_banded)
+    from paper_2010_07284_b200.pixlog import random_mask_device
+
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    dev = Device(local, stream=stream.cuda_stream)
+    n = args.size if args.size != 4096 else 65536
+    r0, r1 = band_rows(n, ws, rank)
+    mask = random_mask_device(n, r1 - r0, args.density, 1, r0, dev)
+    target = random_mask_device(n, r1 - r0, 0.05, 2, r0, dev)
+
+    class _Solo:
+        rank, world = 0, 1
+
+        def neighbours(self, first, last):
+            return None, None
+
+        def allgather(self, obj):
+            return [obj]
+
+        def allreduce_sum(self, x):
+            return x
+
+    comm = TorchComm() if ws > 1 else _Solo()
+
+    def step():
+        x = near_banded(comm, mask, 4)
+        v = volume_banded(comm, x)
+        r = reach_banded(comm, target, mask)
+        return v, r
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    l0 = dev.launches
+    with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dev.synchronize()
+        t = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([t], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    ops = 4 + 1 + 1
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Gpixel-ops/s", "value": ops * n * n * args.steps / t / 1e9,
+            "unit": "Gpixel-ops/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u1 (bit-packed)", "data": "synthetic",
+            "config": {"workload": f"BASELINE config 5: {n}x{n} random mask (density "
+                                   f"{args.density}) in {ws} row band(s): near^4 + volume + "
+                                   f"reach (target density 0.05)",
+                       "rows_per_rank": r1 - r0, "timing": "host wall clock around synced "
+                                                           "steps (includes exchanges), max over ranks"},
+            "gpu_launches": dev.launches - l0, "clocks": clocks.summary(),
+            "cpu_baseline": None}), flush=True)
+
+
 def main():
     args = parse()
     ws, rank, local = dist_setup()
@@ -390,6 +461,8 @@ def main():
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         if args.config == "c4":
             c4_config(args, ws, rank, local)
+        elif args.config == "c5":
+            c5_config(args, ws, rank, local)
         else:
             formula_config(args, ws, rank, local)
         if ws > 1:

@@ -235,16 +235,29 @@ def _halo(row: Optional[np.ndarray], w: int, fill: int, dev: Device) -> DeviceIm
     return DeviceImage.upload(a, PixelKind.Bool, dev)
 
 
+def _extend(cur: DeviceImage, above, below, fill: int):
+    """[above; cur; below] with halo rows only where a neighbour exists (at the
+    image edges the kernels clip exactly like the reference)."""
+    dev, w = cur.device, cur.width
+    parts, off = [], 0
+    if above is not None:
+        parts.append(_halo(above, w, fill, dev))
+        off = 1
+    parts.append(cur)
+    if below is not None:
+        parts.append(_halo(below, w, fill, dev))
+    return (_vstack(parts) if len(parts) > 1 else cur), off
+
+
 def near_banded(comm: Comm, band: DeviceImage, k: int = 1, erode: bool = False) -> DeviceImage:
     """near^k (or interior^k) of the full image, restricted to this band."""
-    dev, w, h = band.device, band.width, band.height
+    dev, h = band.device, band.height
     cur = band
     for _ in range(k):  # one halo row per step keeps the exchange tiny (W bits)
         above, below = comm.neighbours(_row_bytes(cur, 0), _row_bytes(cur, h - 1))
-        fill = 1 if erode else 0
-        ext = _vstack([_halo(above, w, fill, dev), cur, _halo(below, w, fill, dev)])
+        ext, off = _extend(cur, above, below, 1 if erode else 0)
         ext = kernels.erode(ext, dev) if erode else kernels.dilate(ext, dev)
-        cur = _rows(ext, 1, h)
+        cur = _rows(ext, off, h) if ext.height != h else ext
     return cur
 
 
@@ -257,9 +270,10 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
     L = _lib.load()
     dev, w, h = target.device, target.width, target.height
     above, below = comm.neighbours(_row_bytes(target, 0), _row_bytes(target, h - 1))
-    zero = DeviceImage.upload(np.zeros((1, w), np.uint8), PixelKind.Bool, dev)
-    t_ext = _vstack([_halo(above, w, 0, dev), target, _halo(below, w, 0, dev)])
-    u_ext = _vstack([zero, through, zero])
+    t_ext, off = _extend(target, above, below, 0)
+    zero = np.zeros((1, w), np.uint8)
+    u_ext, _ = _extend(through, None if above is None else zero,
+                       None if below is None else zero, 0)
     st = C.c_void_p()
     _check(L.slcs_reach_prepare(dev.handle, t_ext.handle, u_ext.handle, C.byref(st)))
     try:
@@ -269,8 +283,8 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
             _check(L.slcs_reach_row(st, r, roots.ctypes.data, cls.ctypes.data))
             return roots, cls
 
-        fr, fc = row(1)
-        lr, lc = row(h)
+        fr, fc = row(off)
+        lr, lc = row(off + h - 1)
         rows = comm.allgather((fr, fc, lr, lc))
         newly = np.ascontiguousarray(resolve_border_flags(rows)[comm.rank], np.uint32)
         if newly.size:
@@ -280,4 +294,5 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
         sel_ext = DeviceImage(sel, dev)
     finally:
         L.slcs_reach_state_destroy(st)
-    return near_banded(comm, _rows(sel_ext, 1, h), 1)
+    sel_band = _rows(sel_ext, off, h) if sel_ext.height != h else sel_ext
+    return near_banded(comm, sel_band, 1)

@@ -334,9 +334,21 @@ slcs_image* upload(slcs_ctx* ctx, int kind, int w, int h, int batch, const void*
   if (kind == SLCS_LABEL) {
     cuda_check(cudaMemcpyAsync(img.p->data, src, npx * 4, dir, ctx->stream), "upload labels");
   } else if (kind == SLCS_U16) {
-    cuda_check(cudaMemcpy2DAsync(img.p->data, img.p->geo.pitch * 2, src, size_t(w) * 2,
-                                 size_t(w) * 2, size_t(h) * size_t(batch), dir, ctx->stream),
-               "upload u16");
+    if (!from_device && img.p->geo.pitch != size_t(w)) {
+      // dense H2D, then a device-side repitch (short pitched host rows are slow)
+      void* staging = ctx->alloc(npx * 2);
+      cuda_check(cudaMemcpyAsync(staging, src, npx * 2, cudaMemcpyHostToDevice, ctx->stream),
+                 "upload u16");
+      cuda_check(cudaMemcpy2DAsync(img.p->data, img.p->geo.pitch * 2, staging, size_t(w) * 2,
+                                   size_t(w) * 2, size_t(h) * size_t(batch),
+                                   cudaMemcpyDeviceToDevice, ctx->stream),
+                 "repitch u16");
+      ctx->release(staging);
+    } else {
+      cuda_check(cudaMemcpy2DAsync(img.p->data, img.p->geo.pitch * 2, src, size_t(w) * 2,
+                                   size_t(w) * 2, size_t(h) * size_t(batch), dir, ctx->stream),
+                 "upload u16");
+    }
   } else {
     const void* dev = src;
     void* staging = nullptr;

@@ -1171,9 +1171,21 @@ int slcs_program_set_input_host(slcs_program* prog, const char* name, slcs_kind 
     }
     cudaStream_t st = prog->pstream;
     if (kind == SLCS_U16) {
-      cuda_check(cudaMemcpy2DAsync(s.data, s.geo.pitch * 2, host, size_t(w) * 2, size_t(w) * 2,
-                                   size_t(h) * size_t(batch), cudaMemcpyHostToDevice, st),
-                 "input upload");
+      // one dense H2D copy (many short pitched rows are slow over PCIe), then
+      // a device-side repitch
+      const size_t dense = size_t(w) * size_t(h) * size_t(batch) * 2;
+      if (s.geo.pitch == size_t(w)) {
+        cuda_check(cudaMemcpyAsync(s.data, host, dense, cudaMemcpyHostToDevice, st),
+                   "input upload");
+      } else {
+        prog->ensure_staging(dense);
+        cuda_check(cudaMemcpyAsync(prog->staging, host, dense, cudaMemcpyHostToDevice, st),
+                   "input upload");
+        cuda_check(cudaMemcpy2DAsync(s.data, s.geo.pitch * 2, prog->staging, size_t(w) * 2,
+                                     size_t(w) * 2, size_t(h) * size_t(batch),
+                                     cudaMemcpyDeviceToDevice, st),
+                   "input repitch");
+      }
     } else if (kind == SLCS_LABEL) {
       cuda_check(cudaMemcpyAsync(s.data, host, size_t(w) * h * batch * 4, cudaMemcpyHostToDevice,
                                  st),
