@@ -70,6 +70,14 @@ struct DeviceGuard {
 
 void slcs::set_last_error(const std::string& msg) { g_err = msg; }
 
+bool slcs::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SLCS_NO_PDL");
+    return !(e && e[0] && e[0] != '0');
+  }();
+  return on;
+}
+
 void* slcs_ctx::alloc(size_t bytes) {
   void* p = nullptr;
   cuda_check(cudaMallocAsync(&p, bytes ? bytes : 16, stream), "cudaMallocAsync");

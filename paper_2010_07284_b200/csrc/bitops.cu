@@ -66,6 +66,7 @@ __device__ __forceinline__ uint32_t valid_mask(int j, int wpr, uint32_t lastmask
 // dense bytes (reference Bool / U16-as-mask layout) -> bit-packed rows
 __global__ void k_pack_u8(const uint8_t* __restrict__ dense, uint32_t* __restrict__ bits, int w,
                           int h, int wpr, size_t pitch, size_t nwords_total) {
+  slcs_pdl_wait();
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
        q += size_t(gridDim.x) * blockDim.x) {
     size_t row = q / pitch;  // global row over the batch
@@ -82,6 +83,7 @@ __global__ void k_pack_u8(const uint8_t* __restrict__ dense, uint32_t* __restric
 
 __global__ void k_pack_u16(const uint16_t* __restrict__ dense, uint32_t* __restrict__ bits, int w,
                            int wpr, size_t pitch, size_t nwords_total) {
+  slcs_pdl_wait();
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
        q += size_t(gridDim.x) * blockDim.x) {
     size_t row = q / pitch;
@@ -99,6 +101,7 @@ __global__ void k_pack_u16(const uint16_t* __restrict__ dense, uint32_t* __restr
 // bits -> dense bytes: one thread per output byte group of 4 pixels
 __global__ void k_unpack(const uint32_t* __restrict__ bits, uint8_t* __restrict__ dense, int w,
                          size_t pitch, size_t npix_total) {
+  slcs_pdl_wait();
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < npix_total;
        i += size_t(gridDim.x) * blockDim.x) {
     size_t row = i / size_t(w);
@@ -112,6 +115,7 @@ __global__ void k_unpack(const uint32_t* __restrict__ bits, uint8_t* __restrict_
 __global__ void k_threshold(const uint16_t* __restrict__ px, uint32_t* __restrict__ bits,
                             int wpr, uint32_t lastmask, size_t bpitch, size_t upitch,
                             size_t nwords_total, int lo, int hi) {
+  slcs_pdl_wait();
   const unsigned span = unsigned(hi - lo);  // valid only when lo <= hi
   const bool empty = lo > hi;
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
@@ -173,6 +177,7 @@ __device__ __forceinline__ void interval_of(int op, double n, int& lo, int& hi) 
 __global__ void k_threshold_dev(const uint16_t* __restrict__ px, uint32_t* __restrict__ bits,
                                 int wpr, uint32_t lastmask, size_t bpitch, size_t upitch,
                                 size_t nwords_total, int op, const double* n_dev) {
+  slcs_pdl_wait();
   int lo, hi;
   interval_of(op, *n_dev, lo, hi);
   const unsigned span = unsigned(hi - lo);
@@ -194,6 +199,7 @@ __global__ void k_threshold_dev(const uint16_t* __restrict__ px, uint32_t* __res
 // NOT over uint4 groups; the row pitch is a multiple of 4 words.
 __global__ void k_not(const uint4* __restrict__ a, uint4* __restrict__ out, int wpr,
                       uint32_t lastmask, size_t pitch4, size_t n4) {
+  slcs_pdl_wait();
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
        q += size_t(gridDim.x) * blockDim.x) {
     size_t row = q / pitch4;
@@ -210,6 +216,7 @@ __global__ void k_not(const uint4* __restrict__ a, uint4* __restrict__ out, int 
 template <int OP>
 __global__ void k_binop(const uint4* __restrict__ a, const uint4* __restrict__ b,
                         uint4* __restrict__ out, size_t n4) {
+  slcs_pdl_wait();
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
        q += size_t(gridDim.x) * blockDim.x) {
     uint4 x = a[q], y = b[q];
@@ -231,6 +238,7 @@ __global__ void k_binop(const uint4* __restrict__ a, const uint4* __restrict__ b
 template <int K, bool ERODE>
 __global__ void k_near(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h,
                        int wpr, uint32_t lastmask, size_t pitch, size_t slice, int strip) {
+  slcs_pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int s_idx = blockIdx.y * blockDim.y + threadIdx.y;
   const int r0 = s_idx * strip;
@@ -293,7 +301,7 @@ void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st
   dim3 block(bx, by);
   dim3 grid(unsigned((g.pitch + bx - 1) / bx), unsigned((strips + by - 1) / by),
             unsigned(g.batch));
-  k_near<K, ERODE><<<grid, block, 0, st>>>(a, out, g.h, g.wpr, g.lastmask, g.pitch, g.slice,
+  pdl(k_near<K, ERODE>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, g.pitch, g.slice,
                                            strip);
 }
 
@@ -314,6 +322,7 @@ void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaSt
 
 __global__ void k_volume(const uint4* __restrict__ a, size_t slice4,
                          unsigned long long* __restrict__ counts) {
+  slcs_pdl_wait();
   const uint4* src = a + size_t(blockIdx.y) * slice4;
   unsigned long long local = 0;
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < slice4;
@@ -340,6 +349,7 @@ __global__ void k_volume(const uint4* __restrict__ a, size_t slice4,
 // generated independently and bit-identically to the CPU fixture.
 __global__ void k_random_mask(uint32_t* __restrict__ bits, int w, int h, long long row0,
                               int wpr, size_t pitch, unsigned long long seed, double density) {
+  slcs_pdl_wait();
   const size_t n = pitch * size_t(h);
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
        q += size_t(gridDim.x) * blockDim.x) {
@@ -364,6 +374,7 @@ __global__ void k_random_mask(uint32_t* __restrict__ bits, int w, int h, long lo
 }
 
 __global__ void k_counts_to_double(const unsigned long long* c, double* out, int n) {
+  slcs_pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = double(c[i]);
 }
@@ -372,27 +383,27 @@ __global__ void k_counts_to_double(const unsigned long long* c, double* out, int
 
 int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool, cudaStream_t st) {
   size_t n = g.slice * size_t(g.batch);
-  k_pack_u8<<<grid_for(n, kThreads), kThreads, 0, st>>>(dense, bits, g.w, g.h, g.wpr, g.pitch,
+  pdl(k_pack_u8, grid_for(n, kThreads), kThreads, 0, st, dense, bits, g.w, g.h, g.wpr, g.pitch,
                                                         n);
   return 1;
 }
 
 int launch_pack_u16_mask(const uint16_t* dense, uint32_t* bits, const Geo& g, cudaStream_t st) {
   size_t n = g.slice * size_t(g.batch);
-  k_pack_u16<<<grid_for(n, kThreads), kThreads, 0, st>>>(dense, bits, g.w, g.wpr, g.pitch, n);
+  pdl(k_pack_u16, grid_for(n, kThreads), kThreads, 0, st, dense, bits, g.w, g.wpr, g.pitch, n);
   return 1;
 }
 
 int launch_unpack(const uint32_t* bits, uint8_t* dense, const Geo& g, cudaStream_t st) {
   size_t n = size_t(g.w) * size_t(g.h) * size_t(g.batch);
-  k_unpack<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(bits, dense, g.w, g.pitch, n);
+  pdl(k_unpack, grid_for(n, kThreads, 148 * 32), kThreads, 0, st, bits, dense, g.w, g.pitch, n);
   return 1;
 }
 
 int launch_threshold(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb, int lo,
                      int hi, cudaStream_t st) {
   size_t n = gb.slice * size_t(gb.batch);
-  k_threshold<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(
+  pdl(k_threshold, grid_for(n, kThreads, 148 * 32), kThreads, 0, st, 
       px, bits, gb.wpr, gb.lastmask, gb.pitch, gu.pitch, n, lo, hi);
   return 1;
 }
@@ -400,14 +411,14 @@ int launch_threshold(const uint16_t* px, uint32_t* bits, const Geo& gu, const Ge
 int launch_threshold_dev(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb,
                          int op, const double* n_dev, cudaStream_t st) {
   size_t n = gb.slice * size_t(gb.batch);
-  k_threshold_dev<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(
+  pdl(k_threshold_dev, grid_for(n, kThreads, 148 * 32), kThreads, 0, st, 
       px, bits, gb.wpr, gb.lastmask, gb.pitch, gu.pitch, n, op, n_dev);
   return 1;
 }
 
 int launch_not(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
   size_t n4 = g.slice * size_t(g.batch) / 4;
-  k_not<<<grid_for(n4, kThreads, 148 * 32), kThreads, 0, st>>>(
+  pdl(k_not, grid_for(n4, kThreads, 148 * 32), kThreads, 0, st, 
       reinterpret_cast<const uint4*>(a), reinterpret_cast<uint4*>(out), g.wpr, g.lastmask,
       g.pitch / 4, n4);
   return 1;
@@ -416,7 +427,7 @@ int launch_not(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) 
 int launch_and(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
                cudaStream_t st) {
   size_t n4 = g.slice * size_t(g.batch) / 4;
-  k_binop<0><<<grid_for(n4, kThreads, 148 * 32), kThreads, 0, st>>>(
+  pdl(k_binop<0>, grid_for(n4, kThreads, 148 * 32), kThreads, 0, st, 
       reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
       reinterpret_cast<uint4*>(out), n4);
   return 1;
@@ -425,7 +436,7 @@ int launch_and(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g
 int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
               cudaStream_t st) {
   size_t n4 = g.slice * size_t(g.batch) / 4;
-  k_binop<1><<<grid_for(n4, kThreads, 148 * 32), kThreads, 0, st>>>(
+  pdl(k_binop<1>, grid_for(n4, kThreads, 148 * 32), kThreads, 0, st, 
       reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
       reinterpret_cast<uint4*>(out), n4);
   return 1;
@@ -447,21 +458,21 @@ int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, c
   int gx = grid_for(n4, kThreads, 148 * 8);
   if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 8 + g.batch - 1) / g.batch));
   dim3 grid(unsigned(gx), unsigned(g.batch));
-  k_volume<<<grid, kThreads, 0, st>>>(reinterpret_cast<const uint4*>(a), n4, counts);
+  pdl(k_volume, grid, kThreads, 0, st, reinterpret_cast<const uint4*>(a), n4, counts);
   return 1;
 }
 
 int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned long long seed,
                        double density, cudaStream_t st) {
   size_t n = g.slice;
-  k_random_mask<<<grid_for(n, kThreads, 148 * 32), kThreads, 0, st>>>(bits, g.w, g.h, row0, g.wpr,
+  pdl(k_random_mask, grid_for(n, kThreads, 148 * 32), kThreads, 0, st, bits, g.w, g.h, row0, g.wpr,
                                                                       g.pitch, seed, density);
   return 1;
 }
 
 int launch_counts_to_double(const unsigned long long* counts, double* out, int n,
                             cudaStream_t st) {
-  k_counts_to_double<<<(n + 255) / 256, 256, 0, st>>>(counts, out, n);
+  pdl(k_counts_to_double, (n + 255) / 256, 256, 0, st, counts, out, n);
   return 1;
 }
 

@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
                                                            uint8_t* __restrict__ F,
                                                            uint32_t* __restrict__ SZ,
                                                            uint32_t* __restrict__ lists, G g) {
+  slcs_pdl_wait();
   extern __shared__ __align__(16) unsigned char lsm[];
   uint32_t* par = reinterpret_cast<uint32_t*>(lsm);           // LSLOTS
   uint32_t* sT = par + LSLOTS;                                 // LUNITS
@@ -454,11 +455,13 @@ __device__ __forceinline__ void load_unit(const uint32_t* u, const G& g, int k, 
 template <int PART>
 __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G g, int nhb,
                              int nvb) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t nA = uint32_t(nhb) * uint32_t(g.wpr), nB = uint32_t(nvb) * uint32_t(g.BH);
-  const uint32_t lo = PART == 0 ? 0u : nA, hi = PART == 0 ? nA : nA + nB;
+  // PART 0: horizontal borders only, 1: vertical only, 2: both in one grid
+  const uint32_t lo = PART == 1 ? nA : 0u, hi = PART == 0 ? nA : nA + nB;
   for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi;
        i += gridDim.x * blockDim.x) {
     if (i < nA) {
@@ -533,6 +536,7 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
 // run's global root is exactly P[P[key block]].
 __global__ void k_root_flatten(uint32_t* P, uint8_t* F, uint32_t* SZ,
                                const uint32_t* __restrict__ lists, G g, int ntiles, int mode) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const int tile = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -568,6 +572,7 @@ __device__ __forceinline__ uint32_t groot(const uint32_t* P, const G& g, uint32_
 __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
                                const uint32_t* __restrict__ tbits, const uint32_t* __restrict__ P,
                                const uint8_t* __restrict__ F, uint32_t* __restrict__ out, G g) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* t = tbits + size_t(slice) * g.slice;
@@ -601,11 +606,13 @@ __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
 // ---- reach against a precomputed labelling (label CSE) ------------------------
 // Flags are generation stamps so the per-block flag array never needs
 // clearing: gen = *epoch * 4096 + idx, with *epoch bumped once per program run.
-__global__ void k_epoch_bump(uint32_t* epoch) { *epoch += 1u; }
+__global__ void k_epoch_bump(uint32_t* epoch) {
+  slcs_pdl_wait(); *epoch += 1u; }
 
 __global__ void k_reach_seed(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ tbits,
                              const uint32_t* __restrict__ P, uint32_t* __restrict__ F32,
                              const uint32_t* __restrict__ epoch, uint32_t idx, G g) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* t = tbits + size_t(slice) * g.slice;
@@ -634,6 +641,7 @@ __global__ void k_reach_select_gen(const uint32_t* __restrict__ ubits,
                                    const uint32_t* __restrict__ F32,
                                    const uint32_t* __restrict__ epoch, uint32_t idx,
                                    uint32_t* __restrict__ out, G g) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* t = tbits + size_t(slice) * g.slice;
@@ -671,6 +679,7 @@ __global__ void k_reach_select_gen(const uint32_t* __restrict__ ubits,
 __global__ void k_band_row(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
                            const uint8_t* __restrict__ F, int r, uint32_t* __restrict__ roots,
                            uint8_t* __restrict__ cls, G g) {
+  slcs_pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= g.wpr) return;
   const int k = r >> 1;
@@ -703,6 +712,7 @@ __global__ void k_band_row(const uint32_t* __restrict__ ubits, const uint32_t* _
 }
 
 __global__ void k_band_set_flags(const uint32_t* __restrict__ roots, int n, uint8_t* F, G g) {
+  slcs_pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) F[gblk(g, roots[i])] = 1;
 }
@@ -717,6 +727,7 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
 // labels: per word, each run's pixels get linear(global root) + 1
 __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
                               const uint32_t* __restrict__ MKall, uint32_t* __restrict__ L, G g) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
@@ -772,6 +783,7 @@ __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t
 // slot points at itself)
 __global__ void k_maxvol_max(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
                              const uint32_t* __restrict__ SZ, unsigned int* maxv, G g) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
@@ -798,6 +810,7 @@ __global__ void k_maxvol_select(const uint32_t* __restrict__ ubits, const uint32
                                 const uint32_t* __restrict__ SZ,
                                 const unsigned int* __restrict__ maxv, uint32_t* __restrict__ out,
                                 G g) {
+  slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
@@ -841,6 +854,7 @@ template <int MODE>
 __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict__ ubits,
                                                       const uint32_t* __restrict__ tbits,
                                                       uint32_t* __restrict__ out, G g) {
+  slcs_pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* par = reinterpret_cast<uint32_t*>(smem);  // SSLOTS
   uint32_t* sT = par + SSLOTS;                         // 1024
@@ -1006,7 +1020,7 @@ int small_launch(const uint32_t* u, const uint32_t* t, uint32_t* out, const G& g
                          int(small_smem_bytes()));
     attr_set = true;
   }
-  k_small<MODE><<<batch, ST_THREADS, small_smem_bytes(), st>>>(u, t, out, g);
+  pdl(k_small<MODE>, batch, ST_THREADS, small_smem_bytes(), st, u, t, out, g);
   return 1;
 }
 
@@ -1090,7 +1104,7 @@ void tile_launch(dim3 grid, const uint32_t* u, const uint32_t* t, CclScratch& s,
                          int(tile_smem<MODE>()));
     attr = true;
   }
-  k_tile_local<MODE><<<grid, LT_THREADS, tile_smem<MODE>(), st>>>(u, t, s.parent, s.flag, s.size,
+  pdl(k_tile_local<MODE>, grid, LT_THREADS, tile_smem<MODE>(), st, u, t, s.parent, s.flag, s.size,
                                                                  s.lists, g);
 }
 
@@ -1108,20 +1122,12 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
   const int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
   const size_t links = size_t(nhb) * g.wpr + size_t(nvb) * g.BH;
   if (links) {
-    const size_t la = size_t(nhb) * g.wpr, lb = size_t(nvb) * g.BH;
-    if (la) {
-      dim3 mg(unsigned(grid_blocks(la, 256)), unsigned(batch));
-      k_tile_merge<0><<<mg, 256, 0, st>>>(u, s.parent, g, nhb, nvb);
-      ++launches;
-    }
-    if (lb) {
-      dim3 mg(unsigned(grid_blocks(lb, 256)), unsigned(batch));
-      k_tile_merge<1><<<mg, 256, 0, st>>>(u, s.parent, g, nhb, nvb);
-      ++launches;
-    }
+    dim3 mg(unsigned(grid_blocks(links, 256)), unsigned(batch));
+    pdl(k_tile_merge<2>, mg, 256, 0, st, u, s.parent, g, nhb, nvb);
+    ++launches;
     const int ntiles = int(grid.x * grid.y);
     dim3 fg(unsigned((ntiles * 32 + 255) / 256), unsigned(batch));
-    k_root_flatten<<<fg, 256, 0, st>>>(s.parent, s.flag, s.size, s.lists, g, ntiles, mode);
+    pdl(k_root_flatten, fg, 256, 0, st, s.parent, s.flag, s.size, s.lists, g, ntiles, mode);
     launches += 1;
   }
 }
@@ -1141,7 +1147,7 @@ int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStre
 }
 
 int launch_epoch_bump(uint32_t* epoch, cudaStream_t st) {
-  k_epoch_bump<<<1, 1, 0, st>>>(epoch);
+  pdl(k_epoch_bump, 1, 1, 0, st, epoch);
   return 1;
 }
 
@@ -1151,9 +1157,9 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
   G g = make_g(gb);
   const uint32_t* P = static_cast<const uint32_t*>(labels);
   dim3 ug(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
-  k_reach_seed<<<ug, 256, 0, st>>>(through, target, P, flags32, epoch, idx, g);
+  pdl(k_reach_seed, ug, 256, 0, st, through, target, P, flags32, epoch, idx, g);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
-  k_reach_select_gen<<<sg, 256, 0, st>>>(through, target, P, flags32, epoch, idx, tmp_bits, g);
+  pdl(k_reach_select_gen, sg, 256, 0, st, through, target, P, flags32, epoch, idx, tmp_bits, g);
   return 2 + launch_near(tmp_bits, out, gb, k_out, false, st);
 }
 
@@ -1171,7 +1177,7 @@ int launch_reach_prepare(const uint32_t* target, const uint32_t* through, const 
 int launch_reach_row(const uint32_t* through, const CclScratch& s, const Geo& gb, int row,
                      uint32_t* roots, uint8_t* cls, cudaStream_t st) {
   G g = make_g(gb);
-  k_band_row<<<(g.wpr + 127) / 128, 128, 0, st>>>(through, s.parent, s.flag, row, roots, cls, g);
+  pdl(k_band_row, (g.wpr + 127) / 128, 128, 0, st, through, s.parent, s.flag, row, roots, cls, g);
   return 1;
 }
 
@@ -1179,7 +1185,7 @@ int launch_reach_set_flags(const CclScratch& s, const Geo& gb, const uint32_t* r
                            cudaStream_t st) {
   if (n <= 0) return 0;
   G g = make_g(gb);
-  k_band_set_flags<<<(n + 255) / 256, 256, 0, st>>>(roots, n, s.flag, g);
+  pdl(k_band_set_flags, (n + 255) / 256, 256, 0, st, roots, n, s.flag, g);
   return 1;
 }
 
@@ -1189,7 +1195,7 @@ int launch_reach_finish(const uint32_t* target, const uint32_t* through, const C
   G g = make_g(gb);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
   uint32_t* dst = k_out > 0 ? tmp_bits : out;
-  k_reach_select<<<sg, 256, 0, st>>>(through, target, s.parent, s.flag, dst, g);
+  pdl(k_reach_select, sg, 256, 0, st, through, target, s.parent, s.flag, dst, g);
   return 1 + (k_out > 0 ? launch_near(tmp_bits, out, gb, k_out, false, st) : 0);
 }
 
@@ -1203,7 +1209,7 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   int launches = 0;
   large_local_and_merge(bits, nullptr, g, gb.batch, s, MODE_CCL, st, launches);
   dim3 lg(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
-  k_tile_labels<<<lg, 256, 0, st>>>(bits, s.parent, s.size, labels, g);
+  pdl(k_tile_labels, lg, 256, 0, st, bits, s.parent, s.size, labels, g);
   return launches + 1;
 }
 
@@ -1218,7 +1224,7 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
   int launches = 0;
   large_local_and_merge(through, target, g, gb.batch, s, MODE_REACH, st, launches);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
-  k_reach_select<<<sg, 256, 0, st>>>(through, target, s.parent, s.flag, tmp_bits, g);
+  pdl(k_reach_select, sg, 256, 0, st, through, target, s.parent, s.flag, tmp_bits, g);
   launches += 1;
   launches += launch_near(tmp_bits, out, gb, k_out, false, st);
   return launches;
@@ -1233,9 +1239,9 @@ int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch
   cudaMemsetAsync(s.maxv, 0, size_t(gb.batch) * 4, st);
   large_local_and_merge(bits, nullptr, g, gb.batch, s, MODE_SIZE, st, launches);
   dim3 pg(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
-  k_maxvol_max<<<pg, 256, 0, st>>>(bits, s.parent, s.size, s.maxv, g);
+  pdl(k_maxvol_max, pg, 256, 0, st, bits, s.parent, s.size, s.maxv, g);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
-  k_maxvol_select<<<sg, 256, 0, st>>>(bits, s.parent, s.size, s.maxv, out, g);
+  pdl(k_maxvol_select, sg, 256, 0, st, bits, s.parent, s.size, s.maxv, out, g);
   return launches + 2;
 }
 

@@ -48,6 +48,7 @@ __device__ __forceinline__ uint32_t thresh_word(const uint16_t* __restrict__ src
 
 __global__ void k_fused(const FusedProgram prog, int wpr, uint32_t lastmask, size_t bpitch,
                         size_t upitch, size_t nwords_total) {
+  slcs_pdl_wait();
   for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nwords_total;
        q += size_t(gridDim.x) * blockDim.x) {
     size_t row = q / bpitch;
@@ -84,7 +85,7 @@ int launch_fused(const FusedProgram& p, const Geo& gb, const Geo& gu, cudaStream
   size_t blocks = (n + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  k_fused<<<unsigned(blocks), 256, 0, st>>>(p, gb.wpr, gb.lastmask, gb.pitch, gu.pitch, n);
+  pdl(k_fused, unsigned(blocks), 256, 0, st, p, gb.wpr, gb.lastmask, gb.pitch, gu.pitch, n);
   return 1;
 }
 

@@ -167,6 +167,7 @@ Geo geo_of(VT t, int w, int h, int b) {
 // device scalar arithmetic: out = a op b; division by zero raises a flag
 __global__ void k_arith(const double* nums, int a, int b, double ca, double cb, int out, char op,
                         int* err, int err_code) {
+  slcs_pdl_wait();
   double x = a >= 0 ? nums[a] : ca;
   double y = b >= 0 ? nums[b] : cb;
   double r = 0;
@@ -966,7 +967,7 @@ struct slcs_program {
                                               st);
           break;
         case LG_ARITH:
-          k_arith<<<1, 1, 0, st>>>(d_nums, n.num_a, n.num_b, n.ca, n.cb, n.num_out, n.aop, d_err,
+          pdl(k_arith, 1, 1, 0, st, d_nums, n.num_a, n.num_b, n.ca, n.cb, n.num_out, n.aop, d_err,
                                    n.k + 1);
           ++launches;
           break;

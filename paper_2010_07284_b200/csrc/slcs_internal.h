@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 #include <cstdint>
 #include <mutex>
 #include <stdexcept>
@@ -43,6 +45,37 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 
 inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+// ---- programmatic dependent launch (sm_90+) ----------------------------------
+// Every kernel starts with slcs_pdl_wait() and is launched with the
+// programmatic-stream-serialization attribute, so the next kernel of a chain
+// is scheduled while the previous one drains and only its ACQBULK waits for
+// the predecessor's completion -- launch latency overlaps instead of adding up
+// (kernels never trigger early, so memory visibility is unchanged).  Set
+// SLCS_NO_PDL=1 to launch plainly.
+__device__ __forceinline__ void slcs_pdl_wait() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  cudaGridDependencySynchronize();
+#endif
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Row geometry of one image kind.
 struct Geo {
