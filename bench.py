@@ -46,6 +46,8 @@ def parse():
                    help="chain depth of one bounded CPU-reference sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-primitives", action="store_true",
+                   help="skip the per-primitive table at 16384^2 (config 4 size)")
     p.add_argument("--label-cse", action="store_true",
                    help="headline with label CSE on (reaches sharing one `through` node label "
                         "it once).  Default off: every reach node labels its own `through`, "
@@ -186,6 +188,98 @@ def run_reference_arm(args, ws, rank):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+PRIM_BYTES = {"threshold": 2.125, "not": 0.25, "and": 0.375, "or": 0.375, "near": 0.25,
+              "interior": 0.25, "near^4": 0.25, "volume": 0.125, "ccl": 4.125, "reach": 8.375,
+              "maxvol": 8.25}  # SURVEY.md §8d algorithmic bytes per pixel
+
+
+def primitive_table(dev, stream, local, n=16384, reps=10, copies=8):
+    """Every primitive at BASELINE config 4's size (n x n) through the device
+    program path (C ABI, CUDA graph): one program applies the primitive to
+    `copies` distinct inputs (copies x the image > L2, and L2 is flushed by a
+    512 MiB write before every rep), timed with CUDA events on the stream the
+    program is ordered on; per-launch time = rep time / copies.  ccl, reach and
+    maxvol (ms-scale) are timed per direct C-ABI call.  GB/s = SURVEY §8d
+    algorithmic bytes / time."""
+    import torch
+
+    from paper_2010_07284_b200 import DeviceImage, PixelKind, ccl, maxvol, reach
+    from paper_2010_07284_b200.executor import Program
+    from paper_2010_07284_b200.imgql import compile_text
+    from paper_2010_07284_b200.pixlog import random_mask_device
+
+    peak, _ = measured_peak_gbs()
+    g = torch.Generator(device=f"cuda:{local}")
+    g.manual_seed(1)
+    R = copies
+    raws = [torch.randint(-32768, 32767, (n, n), dtype=torch.int16, device=f"cuda:{local}",
+                          generator=g) for _ in range(R)]
+    torch.cuda.synchronize()
+    u16 = [DeviceImage.from_device(r.data_ptr(), PixelKind.U16, n, n, 1, dev) for r in raws]
+    del raws
+    A = [random_mask_device(n, n, 0.5, 10 + i, 0, dev) for i in range(R)]
+    B = [random_mask_device(n, n, 0.41, 30 + i, 0, dev) for i in range(R)]
+    t = random_mask_device(n, n, 0.05, 2, 0, dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    forms = {"threshold": ("u{i} >. 30000", True), "not": ("!a{i}", False),
+             "and": ("a{i} & b{i}", False), "or": ("a{i} | b{i}", False),
+             "near": ("near(a{i})", False), "interior": ("interior(a{i})", False),
+             "near^4": ("near(near(near(near(a{i}))))", False), "volume": ("volume(a{i})", False)}
+
+    def time_fn(fn, k):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        l0 = dev.launches
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev) / k
+        return ms, (dev.launches - l0) / reps / k
+
+    out = {}
+    for name, (expr, is_u16) in forms.items():
+        lines = []
+        for i in range(R):
+            lines.append(f'load u{i} = "u{i}"' if is_u16 else f'load a{i} = "a{i}"')
+            if "b{i}" in expr:
+                lines.append(f'load b{i} = "b{i}"')
+            e = expr.format(i=i)
+            lines.append(f'print "v{i}" {e}' if name == "volume" else f'save "o{i}" {e}')
+        prog = Program(compile_text("\n".join(lines) + "\n"), dev)
+        for i in range(R):
+            if is_u16:
+                prog.bind(f"u{i}", u16[i])
+            else:
+                prog.bind(f"a{i}", A[i])
+                if "b{i}" in expr:
+                    prog.bind(f"b{i}", B[i])
+        prog.run()
+        ms, per = time_fn(prog.run, R)
+        out[name] = {"ms": ms, "launches": per, "plan": prog.plan.strip().splitlines()[:2]}
+        del prog
+    for name, fn in {"ccl": lambda: ccl.label(A[0], dev), "reach": lambda: reach(t, A[0], dev),
+                     "maxvol": lambda: maxvol(A[0], dev)}.items():
+        ms, per = time_fn(fn, 1)
+        out[name] = {"ms": ms, "launches": per}
+    for name, d in out.items():
+        gbs = PRIM_BYTES[name] * n * n / (d["ms"] / 1e3) / 1e9
+        d.update({"ms": round(d["ms"], 4), "gbs": round(gbs, 1), "frac": round(gbs / peak, 3),
+                  "bytes_per_px": PRIM_BYTES[name]})
+    del flush
+    return {"image": f"{n}x{n}", "inputs": f"{R} distinct inputs per primitive: u16 uniform "
+                                           "random (torch); randomMask density 0.5 / 0.41; "
+                                           "reach target density 0.05",
+            "timing": "CUDA events on the program stream around one graph replay of "
+                      f"{R} independent applications, L2 flushed before each; ms = per "
+                      "application", "peak_gbs": peak, "ops": out}
 
 
 C1_SPEC = ('load img = "img.png"\nlet a = img >. 62258\nlet b = img >. 56360\n'
@@ -623,6 +717,10 @@ def main():
         "compulsory_frac": 0.375 * px / t_reach / 1e9 / peak,
     }
 
+    prims = None
+    if rank == 0 and not args.no_primitives:
+        prims = primitive_table(dev, stream, local)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -651,7 +749,7 @@ def main():
             "gpu_launches": launches, "kernels_per_formula": prog.launches,
             "label_cse": cse, "alternate": alt,
             "clocks": clocks.summary(), "e2e": e2e, "roofline": roofline,
-            "cpu_baseline": cpu,
+            "cpu_baseline": cpu, "primitives_c4": prims,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -124,6 +124,10 @@ int slcs_interior_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out)
 /* kernels::countTrue = volume (kernels.cpp:126-136).  `out` holds `batch`
  * counts (one per slice).  Synchronises. */
 int slcs_volume(slcs_ctx* ctx, const slcs_image* a, int64_t* out);
+/* volume without a host round trip: `batch` int64 counts are written to DEVICE
+ * memory `dev_counts` in stream order (no synchronisation) -- the device-side
+ * volume -> print path of SURVEY §8(f) rank 3. */
+int slcs_volume_async(slcs_ctx* ctx, const slcs_image* a, int64_t* dev_counts);
 /* ccl::label (ccl.cpp:127-165): 8-connected labels, each component labelled
  * with its max row-major index + 1 (ccl.hpp:52-60), background 0. */
 int slcs_ccl(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);

@@ -51,6 +51,7 @@ _SIGS = {
     "slcs_interior": (i32, [vp, vp, pvp]),
     "slcs_interior_k": (i32, [vp, vp, i32, pvp]),
     "slcs_volume": (i32, [vp, vp, C.POINTER(i64)]),
+    "slcs_volume_async": (i32, [vp, vp, vp]),
     "slcs_ccl": (i32, [vp, vp, pvp]),
     "slcs_reach": (i32, [vp, vp, vp, pvp]),
     "slcs_maxvol": (i32, [vp, vp, pvp]),

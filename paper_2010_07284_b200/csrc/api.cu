@@ -60,6 +60,7 @@ void check_dims(int w, int h, int batch) {
     fail(SLCS_ERR_SHAPE, "image dimensions must be at least 1x1, got " + std::to_string(w) +
                              "x" + std::to_string(h));
   if (batch < 1) fail(SLCS_ERR_SHAPE, "batch must be at least 1");
+  if (batch > 65535) fail(SLCS_ERR_SHAPE, "batch must be at most 65535 slices");
 }
 
 struct DeviceGuard {
@@ -250,24 +251,42 @@ slcs_image* op_near(slcs_ctx* ctx, const slcs_image* a0, int k, bool erode) {
   return cur.release();
 }
 
+void ensure_counts(slcs_ctx* ctx, int b) {
+  if (ctx->counts_cap >= b) return;
+  if (ctx->d_counts) cudaFree(ctx->d_counts);
+  if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+  if (ctx->d_vscratch) cudaFree(ctx->d_vscratch);
+  ctx->d_counts = nullptr;
+  ctx->h_counts = nullptr;
+  ctx->d_vscratch = nullptr;
+  ctx->counts_cap = 0;
+  cuda_check(cudaMalloc(&ctx->d_counts, sizeof(unsigned long long) * b), "cudaMalloc");
+  cuda_check(cudaMallocHost(&ctx->h_counts, sizeof(unsigned long long) * b), "cudaMallocHost");
+  cuda_check(cudaMalloc(&ctx->d_vscratch, sizeof(unsigned long long) * 2 * b), "cudaMalloc");
+  cuda_check(cudaMemsetAsync(ctx->d_vscratch, 0, sizeof(unsigned long long) * 2 * b, ctx->stream),
+             "cudaMemsetAsync");
+  ctx->counts_cap = b;
+}
+
 void op_volume(slcs_ctx* ctx, const slcs_image* a0, int64_t* out) {
   Ref a(bool_arg(ctx, a0, "volume"));
   int b = a.p->geo.batch;
-  if (ctx->counts_cap < b) {
-    if (ctx->d_counts) cudaFree(ctx->d_counts);
-    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
-    ctx->d_counts = nullptr;
-    ctx->h_counts = nullptr;
-    cuda_check(cudaMalloc(&ctx->d_counts, sizeof(unsigned long long) * b), "cudaMalloc");
-    cuda_check(cudaMallocHost(&ctx->h_counts, sizeof(unsigned long long) * b), "cudaMallocHost");
-    ctx->counts_cap = b;
-  }
-  ctx->launches += launch_volume(words(a.p), ctx->d_counts, a.p->geo, ctx->stream);
+  ensure_counts(ctx, b);
+  ctx->launches += launch_volume(words(a.p), ctx->d_counts, nullptr, ctx->d_vscratch, a.p->geo,
+                                 ctx->stream);
   cuda_check(cudaMemcpyAsync(ctx->h_counts, ctx->d_counts, sizeof(unsigned long long) * b,
                              cudaMemcpyDeviceToHost, ctx->stream),
              "volume readback");
   cuda_check(cudaStreamSynchronize(ctx->stream), "volume sync");
   for (int i = 0; i < b; ++i) out[i] = int64_t(ctx->h_counts[i]);
+}
+
+// device-side volume: counts land in device memory, no synchronisation
+void op_volume_async(slcs_ctx* ctx, const slcs_image* a0, int64_t* dev_counts) {
+  Ref a(bool_arg(ctx, a0, "volume"));
+  ensure_counts(ctx, a.p->geo.batch);
+  ctx->launches += launch_volume(words(a.p), reinterpret_cast<unsigned long long*>(dev_counts),
+                                 nullptr, ctx->d_vscratch, a.p->geo, ctx->stream);
 }
 
 struct Scratch {
@@ -444,6 +463,7 @@ int slcs_ctx_destroy(slcs_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->d_counts) cudaFree(ctx->d_counts);
     if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
+    if (ctx->d_vscratch) cudaFree(ctx->d_vscratch);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -579,6 +599,13 @@ int slcs_interior_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out)
 }
 int slcs_volume(slcs_ctx* ctx, const slcs_image* a, int64_t* out) {
   PRIM(op_volume(ctx, a, out));
+}
+int slcs_volume_async(slcs_ctx* ctx, const slcs_image* a, int64_t* dev_counts) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!dev_counts) fail(SLCS_ERR_ARG, "null output");
+    op_volume_async(ctx, a, dev_counts);
+  });
 }
 int slcs_ccl(slcs_ctx* ctx, const slcs_image* a, slcs_image** out) { PRIM(*out = op_ccl(ctx, a)); }
 int slcs_reach(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,

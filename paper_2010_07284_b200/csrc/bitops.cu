@@ -59,9 +59,6 @@ inline int grid_for(size_t n, int threads, int cap = 148 * 16) {
   return int(b);
 }
 
-__device__ __forceinline__ uint32_t valid_mask(int j, int wpr, uint32_t lastmask) {
-  return j < wpr - 1 ? 0xffffffffu : (j == wpr - 1 ? lastmask : 0u);
-}
 
 // dense bytes (reference Bool / U16-as-mask layout) -> bit-packed rows
 __global__ void k_pack_u8(const uint8_t* __restrict__ dense, uint32_t* __restrict__ bits, int w,
@@ -196,113 +193,156 @@ __global__ void k_threshold_dev(const uint16_t* __restrict__ px, uint32_t* __res
   }
 }
 
-// NOT over uint4 groups; the row pitch is a multiple of 4 words.
+// NOT / AND / OR over uint4 groups (the row pitch is a multiple of 4 words).
+// Grid-stride with UNR independent 16 B loads per operand in flight per
+// thread; NOT re-masks the padding bits/words of every row.
+constexpr int kUnr = 4;
+
+__device__ __forceinline__ uint4 not_group(uint4 x, size_t q, size_t pitch4, int wpr,
+                                           uint32_t lastmask) {
+  const int j0 = int(q % pitch4) * 4;
+  x.x = ~x.x & valid_mask(j0 + 0, wpr, lastmask);
+  x.y = ~x.y & valid_mask(j0 + 1, wpr, lastmask);
+  x.z = ~x.z & valid_mask(j0 + 2, wpr, lastmask);
+  x.w = ~x.w & valid_mask(j0 + 3, wpr, lastmask);
+  return x;
+}
+
 __global__ void k_not(const uint4* __restrict__ a, uint4* __restrict__ out, int wpr,
                       uint32_t lastmask, size_t pitch4, size_t n4) {
   slcs_pdl_wait();
-  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
-       q += size_t(gridDim.x) * blockDim.x) {
-    size_t row = q / pitch4;
-    int j0 = int(q - row * pitch4) * 4;
-    uint4 x = a[q];
-    x.x = ~x.x & valid_mask(j0 + 0, wpr, lastmask);
-    x.y = ~x.y & valid_mask(j0 + 1, wpr, lastmask);
-    x.z = ~x.z & valid_mask(j0 + 2, wpr, lastmask);
-    x.w = ~x.w & valid_mask(j0 + 3, wpr, lastmask);
-    out[q] = x;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; q + (kUnr - 1) * stride < n4; q += kUnr * stride) {
+    uint4 x[kUnr];
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) x[u] = __ldg(a + q + u * stride);
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) out[q + u * stride] = not_group(x[u], q + u * stride, pitch4, wpr, lastmask);
   }
+  for (; q < n4; q += stride) out[q] = not_group(__ldg(a + q), q, pitch4, wpr, lastmask);
+}
+
+template <int OP>
+__device__ __forceinline__ uint4 bin_group(uint4 x, const uint4 y) {
+  if (OP == 0) {
+    x.x &= y.x; x.y &= y.y; x.z &= y.z; x.w &= y.w;
+  } else {
+    x.x |= y.x; x.y |= y.y; x.z |= y.z; x.w |= y.w;
+  }
+  return x;
 }
 
 template <int OP>
 __global__ void k_binop(const uint4* __restrict__ a, const uint4* __restrict__ b,
                         uint4* __restrict__ out, size_t n4) {
   slcs_pdl_wait();
-  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
-       q += size_t(gridDim.x) * blockDim.x) {
-    uint4 x = a[q], y = b[q];
-    if (OP == 0) {
-      x.x &= y.x; x.y &= y.y; x.z &= y.z; x.w &= y.w;
-    } else {
-      x.x |= y.x; x.y |= y.y; x.z |= y.z; x.w |= y.w;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; q + (kUnr - 1) * stride < n4; q += kUnr * stride) {
+    uint4 x[kUnr], y[kUnr];
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) {
+      x[u] = __ldg(a + q + u * stride);
+      y[u] = __ldg(b + q + u * stride);
     }
-    out[q] = x;
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) out[q + u * stride] = bin_group<OP>(x[u], y[u]);
   }
+  for (; q < n4; q += stride) out[q] = bin_group<OP>(__ldg(a + q), __ldg(b + q));
 }
 
-// k-fold near / interior.  Thread = (word column j, strip of rows).  Each row
-// is first dilated (eroded) horizontally with funnel shifts across the
-// neighbouring words, then a (2K+1)-row window is OR-ed (AND-ed) vertically
-// from a register ring.  Rows/columns outside the image are absent: 0 for
-// dilation (kernels.cpp:106-121), 1 for erosion (interior(all) = all,
-// tests/test_reach.cpp:120).
-template <int K, bool ERODE>
-__global__ void k_near(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int h,
-                       int wpr, uint32_t lastmask, size_t pitch, size_t slice, int strip) {
+// k-fold near / interior.  Thread = (16 B column group q of 4 words, strip of
+// S rows).  All S + 2K input rows are loaded up front (one uint4 plus the two
+// neighbouring words per row, independent loads -> deep memory-level
+// parallelism), each row is dilated (eroded) horizontally with funnel shifts,
+// then the (2K+1)-row window is OR-ed (AND-ed) vertically and S uint4 rows are
+// stored.  Rows/columns outside the image are absent: 0 for dilation
+// (kernels.cpp:106-121), 1 for erosion (interior(all) = all,
+// tests/test_reach.cpp:120); padding bits/words of the output stay zero.
+template <int K, bool ERODE, int S>
+__global__ void __launch_bounds__(128) k_near(const uint32_t* __restrict__ in,
+                                              uint32_t* __restrict__ out, int h, int wpr,
+                                              uint32_t lastmask, int pitch4, size_t slice,
+                                              int nstrips) {
   slcs_pdl_wait();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int s_idx = blockIdx.y * blockDim.y + threadIdx.y;
-  const int r0 = s_idx * strip;
-  if (j >= int(pitch) || r0 >= h) return;
-  const uint32_t* src = in + size_t(blockIdx.z) * slice;
-  uint32_t* dst = out + size_t(blockIdx.z) * slice;
-  const int r1 = min(h, r0 + strip);
-  if (j >= wpr) {
-    for (int r = r0; r < r1; ++r) dst[size_t(r) * pitch + j] = 0u;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = t / pitch4, q = t - s * pitch4;
+  if (s >= nstrips) return;
+  const uint32_t* src = in + size_t(blockIdx.y) * slice;
+  uint4* dst = reinterpret_cast<uint4*>(out + size_t(blockIdx.y) * slice);
+  const int r0 = s * S, j0 = 4 * q;
+  const int rows = min(S, h - r0);
+  const size_t pitch = size_t(pitch4) * 4;
+  if (j0 >= wpr) {  // a group of padding words: stays zero
+    for (int i = 0; i < rows; ++i) dst[size_t(r0 + i) * pitch4 + q] = make_uint4(0, 0, 0, 0);
     return;
   }
-  const uint32_t vmask = j == wpr - 1 ? lastmask : 0xffffffffu;
-  const uint32_t ident = ERODE ? 0xffffffffu : 0u;
-  // For erosion, padding bits of the current and right word act as 1.
-  const uint32_t padC = ERODE ? ~vmask : 0u;
-  const uint32_t padR = ERODE ? (j + 1 == wpr - 1 ? ~lastmask : 0u) : 0u;
-
-  auto hrow = [&](int r) -> uint32_t {
-    if (r < 0 || r >= h) return ident;
-    const uint32_t* row = src + size_t(r) * pitch;
-    uint32_t C = __ldg(row + j) | padC;
-    uint32_t L = j > 0 ? __ldg(row + j - 1) : ident;
-    uint32_t R = j + 1 < wpr ? (__ldg(row + j + 1) | padR) : ident;
-    uint32_t acc = C;
+  constexpr uint32_t ID = ERODE ? 0xffffffffu : 0u;
+  uint32_t pad[5];  // erosion: out-of-image bits of words j0..j0+4 act as 1
 #pragma unroll
-    for (int d = 1; d <= K; ++d) {
-      uint32_t lft = __funnelshift_l(L, C, d);
-      uint32_t rgt = __funnelshift_r(C, R, d);
-      acc = ERODE ? (acc & lft & rgt) : (acc | lft | rgt);
+  for (int e = 0; e < 5; ++e) pad[e] = ERODE ? ~valid_mask(j0 + e, wpr, lastmask) : 0u;
+  const bool has_l = j0 > 0, has_r = j0 + 4 < wpr;
+
+  uint32_t hr[S + 2 * K][4];
+#pragma unroll
+  for (int i = 0; i < S + 2 * K; ++i) {
+    const int r = r0 - K + i;
+    uint32_t w[6];
+    if (r < 0 || r >= h) {
+#pragma unroll
+      for (int e = 0; e < 6; ++e) w[e] = ID;
+    } else {
+      const uint32_t* row = src + size_t(r) * pitch;
+      const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + j0));
+      w[0] = has_l ? __ldg(row + j0 - 1) : ID;
+      w[1] = c.x | pad[0];
+      w[2] = c.y | pad[1];
+      w[3] = c.z | pad[2];
+      w[4] = c.w | pad[3];
+      w[5] = has_r ? (__ldg(row + j0 + 4) | pad[4]) : ID;
     }
-    return acc;
-  };
-
-  uint32_t win[2 * K + 1];
 #pragma unroll
-  for (int i = 0; i < 2 * K; ++i) win[i] = hrow(r0 - K + i);
-  for (int r = r0; r < r1; ++r) {
-    win[2 * K] = hrow(r + K);
-    uint32_t acc = win[0];
+    for (int e = 0; e < 4; ++e) {
+      uint32_t acc = w[e + 1];
 #pragma unroll
-    for (int i = 1; i <= 2 * K; ++i) acc = ERODE ? (acc & win[i]) : (acc | win[i]);
-    dst[size_t(r) * pitch + j] = acc & vmask;
+      for (int d = 1; d <= K; ++d) {
+        const uint32_t lft = __funnelshift_l(w[e], w[e + 1], d);
+        const uint32_t rgt = __funnelshift_r(w[e + 1], w[e + 2], d);
+        acc = ERODE ? (acc & lft & rgt) : (acc | lft | rgt);
+      }
+      hr[i][e] = acc;
+    }
+  }
+  uint32_t vm[4];
 #pragma unroll
-    for (int i = 0; i < 2 * K; ++i) win[i] = win[i + 1];
+  for (int e = 0; e < 4; ++e) vm[e] = valid_mask(j0 + e, wpr, lastmask);
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    if (i < rows) {
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t acc = hr[i][e];
+#pragma unroll
+        for (int d = 1; d <= 2 * K; ++d) acc = ERODE ? (acc & hr[i + d][e]) : (acc | hr[i + d][e]);
+        o[e] = acc & vm[e];
+      }
+      dst[size_t(r0 + i) * pitch4 + q] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
 template <int K, bool ERODE>
 void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
-  int bx = 32;
-  while (bx > 1 && size_t(bx / 2) >= g.pitch) bx /= 2;
-  int by = 256 / bx;
-  // rows per thread: enough threads to fill every SM twice (148 x 2048),
-  // clamped to [4, 32] so the 2K halo rows stay a small overhead
-  size_t words = g.pitch * size_t(g.h) * size_t(g.batch);
-  int strip = int(words / (148ull * 2048ull));
-  strip = strip < 4 ? 4 : (strip > 32 ? 32 : strip);
-  if (strip < 2 * K) strip = 2 * K < 32 ? 2 * K : 32;
-  int strips = (g.h + strip - 1) / strip;
-  dim3 block(bx, by);
-  dim3 grid(unsigned((g.pitch + bx - 1) / bx), unsigned((strips + by - 1) / by),
-            unsigned(g.batch));
-  pdl(k_near<K, ERODE>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, g.pitch, g.slice,
-                                           strip);
+  constexpr int S = K <= 4 ? 8 : 4;
+  const int pitch4 = int(g.pitch / 4);
+  const int nstrips = (g.h + S - 1) / S;
+  const size_t threads = size_t(pitch4) * size_t(nstrips);
+  const int block = 128;
+  dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
+  pdl(k_near<K, ERODE, S>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, pitch4, g.slice,
+      nstrips);
 }
 
 template <bool ERODE>
@@ -320,14 +360,30 @@ void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaSt
   }
 }
 
-__global__ void k_volume(const uint4* __restrict__ a, size_t slice4,
-                         unsigned long long* __restrict__ counts) {
+// volume: one launch.  4 independent uint4 loads in flight per thread,
+// popcount, warp + block reduction, one u64 atomic per CTA into a per-slice
+// accumulator; the slice's last CTA (done counter) publishes the count (u64
+// and/or double) and resets accumulator and counter to zero, so no memset
+// launch is needed (acc/done must be zero before the first use).
+__global__ void k_volume(const uint4* __restrict__ a, size_t slice4, unsigned long long* acc,
+                         unsigned int* done, unsigned long long* __restrict__ counts,
+                         double* __restrict__ dbl) {
   slcs_pdl_wait();
   const uint4* src = a + size_t(blockIdx.y) * slice4;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long local = 0;
-  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < slice4;
-       q += size_t(gridDim.x) * blockDim.x) {
-    uint4 x = src[q];
+  for (; q + 3 * stride < slice4; q += 4 * stride) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldg(src + q + u * stride);
+    unsigned c = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c += __popc(x[u].x) + __popc(x[u].y) + __popc(x[u].z) + __popc(x[u].w);
+    local += c;
+  }
+  for (; q < slice4; q += stride) {
+    const uint4 x = __ldg(src + q);
     local += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
   }
 #pragma unroll
@@ -340,7 +396,18 @@ __global__ void k_volume(const uint4* __restrict__ a, size_t slice4,
     local = lane < int(blockDim.x >> 5) ? part[lane] : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if (lane == 0 && local) atomicAdd(counts + blockIdx.y, local);
+    if (lane == 0) {
+      const int s = blockIdx.y;
+      if (local) atomicAdd(acc + s, local);
+      __threadfence();
+      if (atomicAdd(done + s, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const unsigned long long total = atomicExch(acc + s, 0ull);
+        done[s] = 0u;
+        if (counts) counts[s] = total;
+        if (dbl) dbl[s] = double(total);
+      }
+    }
   }
 }
 
@@ -373,11 +440,6 @@ __global__ void k_random_mask(uint32_t* __restrict__ bits, int w, int h, long lo
   }
 }
 
-__global__ void k_counts_to_double(const unsigned long long* c, double* out, int n) {
-  slcs_pdl_wait();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = double(c[i]);
-}
 
 }  // namespace
 
@@ -418,7 +480,7 @@ int launch_threshold_dev(const uint16_t* px, uint32_t* bits, const Geo& gu, cons
 
 int launch_not(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
   size_t n4 = g.slice * size_t(g.batch) / 4;
-  pdl(k_not, grid_for(n4, kThreads, 148 * 32), kThreads, 0, st, 
+  pdl(k_not, grid_for(n4, kThreads * kUnr, 148 * 8), kThreads, 0, st, 
       reinterpret_cast<const uint4*>(a), reinterpret_cast<uint4*>(out), g.wpr, g.lastmask,
       g.pitch / 4, n4);
   return 1;
@@ -427,7 +489,7 @@ int launch_not(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) 
 int launch_and(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
                cudaStream_t st) {
   size_t n4 = g.slice * size_t(g.batch) / 4;
-  pdl(k_binop<0>, grid_for(n4, kThreads, 148 * 32), kThreads, 0, st, 
+  pdl(k_binop<0>, grid_for(n4, kThreads * kUnr, 148 * 8), kThreads, 0, st, 
       reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
       reinterpret_cast<uint4*>(out), n4);
   return 1;
@@ -436,7 +498,7 @@ int launch_and(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g
 int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
               cudaStream_t st) {
   size_t n4 = g.slice * size_t(g.batch) / 4;
-  pdl(k_binop<1>, grid_for(n4, kThreads, 148 * 32), kThreads, 0, st, 
+  pdl(k_binop<1>, grid_for(n4, kThreads * kUnr, 148 * 8), kThreads, 0, st, 
       reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
       reinterpret_cast<uint4*>(out), n4);
   return 1;
@@ -452,13 +514,15 @@ int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erod
   return 1;
 }
 
-int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, cudaStream_t st) {
-  cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * size_t(g.batch), st);
+int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
+                  unsigned long long* vscratch, const Geo& g, cudaStream_t st) {
   size_t n4 = g.slice / 4;
-  int gx = grid_for(n4, kThreads, 148 * 8);
-  if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 8 + g.batch - 1) / g.batch));
+  int gx = grid_for(n4, kThreads * 4, 148 * 4);
+  if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 4 + g.batch - 1) / g.batch));
   dim3 grid(unsigned(gx), unsigned(g.batch));
-  pdl(k_volume, grid, kThreads, 0, st, reinterpret_cast<const uint4*>(a), n4, counts);
+  unsigned int* done = reinterpret_cast<unsigned int*>(vscratch + g.batch);
+  pdl(k_volume, grid, kThreads, 0, st, reinterpret_cast<const uint4*>(a), n4, vscratch, done,
+      counts, dbl);
   return 1;
 }
 
@@ -470,10 +534,5 @@ int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned lo
   return 1;
 }
 
-int launch_counts_to_double(const unsigned long long* counts, double* out, int n,
-                            cudaStream_t st) {
-  pdl(k_counts_to_double, (n + 255) / 256, 256, 0, st, counts, out, n);
-  return 1;
-}
 
 }  // namespace slcs

@@ -122,6 +122,7 @@ struct InputSlot {
   void* data = nullptr;
   size_t bytes = 0;
   const slcs_image* bound = nullptr;
+  const slcs_image* copied = nullptr;  // bound image whose bytes are already in `data`
   bool host_set = false;
 };
 
@@ -803,7 +804,9 @@ struct slcs_program {
     if (arena_bytes) cuda_check(cudaMalloc(&arena, arena_bytes), "program arena");
     if (scratch_bytes) cuda_check(cudaMalloc(&scratch, scratch_bytes), "program scratch");
     cuda_check(cudaMalloc(&d_nums, sizeof(double) * std::max(1, n_nums)), "program numbers");
-    cuda_check(cudaMalloc(&d_counts, sizeof(unsigned long long) * std::max(1, n_nums)),
+    cuda_check(cudaMalloc(&d_counts, 2 * sizeof(unsigned long long) * std::max(1, n_nums)),
+               "program counts");
+    cuda_check(cudaMemset(d_counts, 0, 2 * sizeof(unsigned long long) * std::max(1, n_nums)),
                "program counts");
     cuda_check(cudaMalloc(&d_err, sizeof(int)), "program error flag");
     cuda_check(cudaMalloc(&d_epoch, sizeof(uint32_t)), "program epoch");
@@ -909,6 +912,7 @@ struct slcs_program {
           st_op.lo = st_op.hi = 0;
           fp.ops[fp.n_ops++] = st_op;
           for (size_t z = 0; z < bin.size(); ++z) fp.bin[z] = bin[z];
+          fp.n_bin = int(bin.size());
           for (size_t z = 0; z < uin.size(); ++z) fp.uin[z] = uin[z];
           fp.out[0] = static_cast<uint32_t*>(n.ptr);
           launches += launch_fused(fp, gb, u16_geo(n.w, n.h, n.batch), st);
@@ -961,10 +965,9 @@ struct slcs_program {
           break;
         }
         case LG_VOLUME:
-          launches += launch_volume(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
-                                    d_counts + n.num_out, gb, st);
-          launches += launch_counts_to_double(d_counts + n.num_out, d_nums + n.num_out, n.batch,
-                                              st);
+          // d_counts: 2 zeroed u64 per number slot = volume accumulators/counters
+          launches += launch_volume(static_cast<const uint32_t*>(lgs[n.in[0]].ptr), nullptr,
+                                    d_nums + n.num_out, d_counts + 2 * n.num_out, gb, st);
           break;
         case LG_ARITH:
           pdl(k_arith, 1, 1, 0, st, d_nums, n.num_a, n.num_b, n.ca, n.cb, n.num_out, n.aop, d_err,
@@ -997,10 +1000,14 @@ struct slcs_program {
     cuda_check(cudaStreamWaitEvent(pstream, ev_in, 0), "wait");
     for (auto& kv : inputs) {
       InputSlot& s = kv.second;
-      if (s.bound) {
+      // images are immutable (shared_ptr<const ImageBuffer>, image.hpp:74) and the
+      // slot holds a reference, so a still-bound image that was already copied in
+      // has not changed: skip the copy
+      if (s.bound && s.copied != s.bound) {
         cuda_check(cudaMemcpyAsync(s.data, s.bound->data, s.bytes, cudaMemcpyDeviceToDevice,
                                    pstream),
                    "bind copy");
+        s.copied = s.bound;
       }
     }
     int launches = 0;
@@ -1156,6 +1163,7 @@ int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* im
     const_cast<slcs_image*>(img)->refs.fetch_add(1);
     if (s.bound) drop_image(const_cast<slcs_image*>(s.bound));
     s.bound = img;
+    s.copied = nullptr;
   });
 }
 
@@ -1170,6 +1178,7 @@ int slcs_program_set_input_host(slcs_program* prog, const char* name, slcs_kind 
       drop_image(const_cast<slcs_image*>(s.bound));
       s.bound = nullptr;
     }
+    s.copied = nullptr;
     cudaStream_t st = prog->pstream;
     if (kind == SLCS_U16) {
       // one dense H2D copy (many short pitched rows are slow over PCIe), then

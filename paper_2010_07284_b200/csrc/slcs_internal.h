@@ -48,11 +48,12 @@ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 
 // ---- programmatic dependent launch (sm_90+) ----------------------------------
 // Every kernel starts with slcs_pdl_wait() and is launched with the
-// programmatic-stream-serialization attribute, so the next kernel of a chain
-// is scheduled while the previous one drains and only its ACQBULK waits for
-// the predecessor's completion -- launch latency overlaps instead of adding up
-// (kernels never trigger early, so memory visibility is unchanged).  Set
-// SLCS_NO_PDL=1 to launch plainly.
+// programmatic-stream-serialization attribute.  The wait (griddepcontrol.wait)
+// returns only once the predecessor grid has COMPLETED and its memory is
+// visible.  Kernels do not signal launch_dependents early: an early trigger
+// right after the wait measured slower on B200 (config-2 chain 25.6 -> 27.0
+// ms, threshold 0.82 -> 0.68 of HBM peak).  Set SLCS_NO_PDL=1 to launch
+// plainly.
 __device__ __forceinline__ void slcs_pdl_wait() {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
   cudaGridDependencySynchronize();
@@ -87,6 +88,10 @@ struct Geo {
 };
 
 Geo bool_geo(int w, int h, int batch);
+// valid-bit mask of Bool word j of a row (padding bits/words are zero)
+__device__ __forceinline__ uint32_t valid_mask(int j, int wpr, uint32_t lastmask) {
+  return j < wpr - 1 ? 0xffffffffu : (j == wpr - 1 ? lastmask : 0u);
+}
 Geo u16_geo(int w, int h, int batch);
 Geo label_geo(int w, int h, int batch);
 
@@ -120,13 +125,13 @@ int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
 // k-fold near (dilate) or interior (erode), 1 <= k <= 31 per launch
 int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
                 cudaStream_t st);
-int launch_volume(const uint32_t* a, unsigned long long* counts, const Geo& g, cudaStream_t st);
+// counts (u64) and/or dbl (double) per slice; vscratch = 2*batch zeroed u64
+// (accumulators + done counters), left zeroed by the kernel
+int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
+                  unsigned long long* vscratch, const Geo& g, cudaStream_t st);
 // rows [row0, row0 + g.h) of randomMask(g.w x H, density, Rng(seed)) as bits
 int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned long long seed,
                        double density, cudaStream_t st);
-// counts (u64 per slice) -> doubles (for device-side number values)
-int launch_counts_to_double(const unsigned long long* counts, double* out, int n,
-                            cudaStream_t st);
 
 // Fused elementwise program over bit-packed words (see fused.cu).
 struct FusedOp {
@@ -150,6 +155,7 @@ constexpr int kFusedMaxOut = 4;
 constexpr int kFusedRegs = 8;
 struct FusedProgram {
   int n_ops = 0;
+  int n_bin = 0;  // bool inputs in use (bin[0..n_bin))
   FusedOp ops[kFusedMaxOps];
   const uint32_t* bin[kFusedMaxIn];
   const uint16_t* uin[kFusedMaxIn];
@@ -214,6 +220,7 @@ struct slcs_ctx {
   // small pinned/device scratch for reductions
   unsigned long long* d_counts = nullptr;
   unsigned long long* h_counts = nullptr;
+  unsigned long long* d_vscratch = nullptr;  // 2 * counts_cap, zeroed (launch_volume)
   int counts_cap = 0;
 
   void* alloc(size_t bytes);

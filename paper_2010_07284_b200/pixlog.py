@@ -184,6 +184,17 @@ class DeviceImage:
                                              C.byref(hd)))
         return DeviceImage(hd, device)
 
+    @staticmethod
+    def from_device(ptr: int, kind: PixelKind, width: int, height: int, batch: int = 1,
+                    device: Optional[Device] = None) -> "DeviceImage":
+        """Copy from device memory in the reference dense layout (e.g. a torch tensor's
+        data_ptr()), packing on the device; no host round trip."""
+        device = device or Device.default()
+        hd = C.c_void_p()
+        _check(_lib.load().slcs_image_from_device(device.handle, int(kind), width, height, batch,
+                                                  C.c_void_p(ptr), C.byref(hd)))
+        return DeviceImage(hd, device)
+
     def __repr__(self):
         return f"DeviceImage({self.width}x{self.height},{pixelKindName(self.kind)},batch={self.batch})"
 
