@@ -195,7 +195,7 @@ PRIM_BYTES = {"threshold": 2.125, "not": 0.25, "and": 0.375, "or": 0.375, "near"
               "maxvol": 8.25}  # SURVEY.md §8d algorithmic bytes per pixel
 
 
-def primitive_table(dev, stream, local, n=16384, reps=10, copies=8):
+def primitive_table(dev, stream, local, n=16384, reps=10, copies=8, labels=True):
     """Every primitive at BASELINE config 4's size (n x n) through the device
     program path (C ABI, CUDA graph): one program applies the primitive to
     `copies` distinct inputs (copies x the image > L2, and L2 is flushed by a
@@ -265,16 +265,31 @@ def primitive_table(dev, stream, local, n=16384, reps=10, copies=8):
         ms, per = time_fn(prog.run, R)
         out[name] = {"ms": ms, "launches": per, "plan": prog.plan.strip().splitlines()[:2]}
         del prog
-    for name, fn in {"ccl": lambda: ccl.label(A[0], dev), "reach": lambda: reach(t, A[0], dev),
-                     "maxvol": lambda: maxvol(A[0], dev)}.items():
-        ms, per = time_fn(fn, 1)
-        out[name] = {"ms": ms, "launches": per}
+    if labels:  # u32 labels need W*H < 2^32 - 1 (image.cpp:26-28)
+        for name, fn in {"ccl": lambda: ccl.label(A[0], dev),
+                         "reach": lambda: reach(t, A[0], dev),
+                         "maxvol": lambda: maxvol(A[0], dev)}.items():
+            ms, per = time_fn(fn, 1)
+            out[name] = {"ms": ms, "launches": per}
+    # same-size ceiling: a device copy of one bool image (read + write), timed the same way
+    src = [torch.empty(n * n // 8, dtype=torch.uint8, device=f"cuda:{local}") for _ in range(R)]
+    dst = [torch.empty_like(x) for x in src]
+
+    def copies_fn():
+        for x, y in zip(src, dst):
+            y.copy_(x)
+    copy_ms, _ = time_fn(copies_fn, R)
+    copy_gbs = 2 * (n * n // 8) / (copy_ms / 1e3) / 1e9
+    del src, dst
     for name, d in out.items():
         gbs = PRIM_BYTES[name] * n * n / (d["ms"] / 1e3) / 1e9
         d.update({"ms": round(d["ms"], 4), "gbs": round(gbs, 1), "frac": round(gbs / peak, 3),
                   "bytes_per_px": PRIM_BYTES[name]})
     del flush
-    return {"image": f"{n}x{n}", "inputs": f"{R} distinct inputs per primitive: u16 uniform "
+    return {"image": f"{n}x{n}", "copy_ceiling_gbs": round(copy_gbs, 1),
+            "copy_ceiling_note": "torch copy_ of one bool image (same bytes as ! / near), "
+                                 "timed the same way: the achievable HBM rate at this size",
+            "inputs": f"{R} distinct inputs per primitive: u16 uniform "
                                            "random (torch); randomMask density 0.5 / 0.41; "
                                            "reach target density 0.05",
             "timing": "CUDA events on the program stream around one graph replay of "
@@ -717,9 +732,10 @@ def main():
         "compulsory_frac": 0.375 * px / t_reach / 1e9 / peak,
     }
 
-    prims = None
+    prims = prims5 = None
     if rank == 0 and not args.no_primitives:
         prims = primitive_table(dev, stream, local)
+        prims5 = primitive_table(dev, stream, local, n=65536, reps=5, copies=2, labels=False)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -749,7 +765,7 @@ def main():
             "gpu_launches": launches, "kernels_per_formula": prog.launches,
             "label_cse": cse, "alternate": alt,
             "clocks": clocks.summary(), "e2e": e2e, "roofline": roofline,
-            "cpu_baseline": cpu, "primitives_c4": prims,
+            "cpu_baseline": cpu, "primitives_c4": prims, "primitives_c5": prims5,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -333,16 +333,118 @@ __global__ void __launch_bounds__(128) k_near(const uint32_t* __restrict__ in,
   }
 }
 
+// k >= 2: a strip of S rows streamed through a (2K+1)-row register ring; P new
+// rows are loaded per step (independent loads in flight) so the 2K halo rows
+// are amortised over a long strip instead of being re-read per short strip.
+template <int K, bool ERODE, int S, int P>
+__global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict__ in,
+                                                     uint32_t* __restrict__ out, int h, int wpr,
+                                                     uint32_t lastmask, int pitch4, size_t slice,
+                                                     int nstrips) {
+  slcs_pdl_wait();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = t / pitch4, q = t - s * pitch4;
+  if (s >= nstrips) return;
+  const uint32_t* src = in + size_t(blockIdx.y) * slice;
+  uint4* dst = reinterpret_cast<uint4*>(out + size_t(blockIdx.y) * slice);
+  const int r0 = s * S, j0 = 4 * q;
+  const int rows = min(S, h - r0);
+  const size_t pitch = size_t(pitch4) * 4;
+  if (j0 >= wpr) {
+    for (int i = 0; i < rows; ++i) dst[size_t(r0 + i) * pitch4 + q] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  constexpr uint32_t ID = ERODE ? 0xffffffffu : 0u;
+  uint32_t pad[5];
+#pragma unroll
+  for (int e = 0; e < 5; ++e) pad[e] = ERODE ? ~valid_mask(j0 + e, wpr, lastmask) : 0u;
+  const bool has_l = j0 > 0, has_r = j0 + 4 < wpr;
+  uint32_t vm[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) vm[e] = valid_mask(j0 + e, wpr, lastmask);
+
+  auto hrow = [&](int r, uint32_t (&o)[4]) {
+    uint32_t w[6];
+    if (r < 0 || r >= h) {
+#pragma unroll
+      for (int e = 0; e < 6; ++e) w[e] = ID;
+    } else {
+      const uint32_t* row = src + size_t(r) * pitch;
+      const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + j0));
+      w[0] = has_l ? __ldg(row + j0 - 1) : ID;
+      w[1] = c.x | pad[0];
+      w[2] = c.y | pad[1];
+      w[3] = c.z | pad[2];
+      w[4] = c.w | pad[3];
+      w[5] = has_r ? (__ldg(row + j0 + 4) | pad[4]) : ID;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t acc = w[e + 1];
+#pragma unroll
+      for (int d = 1; d <= K; ++d) {
+        const uint32_t lft = __funnelshift_l(w[e], w[e + 1], d);
+        const uint32_t rgt = __funnelshift_r(w[e + 1], w[e + 2], d);
+        acc = ERODE ? (acc & lft & rgt) : (acc | lft | rgt);
+      }
+      o[e] = acc;
+    }
+  };
+
+  uint32_t ring[2 * K + P][4];
+#pragma unroll
+  for (int i = 0; i < 2 * K; ++i) hrow(r0 - K + i, ring[i]);
+#pragma unroll
+  for (int c = 0; c < S; c += P) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) hrow(r0 + c + K + p, ring[2 * K + p]);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (c + p < rows) {
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t acc = ring[p][e];
+#pragma unroll
+          for (int d = 1; d <= 2 * K; ++d) acc = ERODE ? (acc & ring[p + d][e]) : (acc | ring[p + d][e]);
+          o[e] = acc & vm[e];
+        }
+        dst[size_t(r0 + c + p) * pitch4 + q] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ring[i][e] = ring[i + P][e];
+  }
+}
+
 template <int K, bool ERODE>
 void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
-  constexpr int S = K <= 4 ? 8 : 4;
   const int pitch4 = int(g.pitch / 4);
-  const int nstrips = (g.h + S - 1) / S;
-  const size_t threads = size_t(pitch4) * size_t(nstrips);
   const int block = 128;
-  dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
-  pdl(k_near<K, ERODE, S>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, pitch4, g.slice,
-      nstrips);
+  if (K == 1) {
+    constexpr int S = 4;
+    const int nstrips = (g.h + S - 1) / S;
+    const size_t threads = size_t(pitch4) * size_t(nstrips);
+    dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
+    pdl(k_near<K, ERODE, S>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, pitch4, g.slice,
+        nstrips);
+  } else {
+    // long strips amortise the 2K halo rows; short images keep >= ~2 waves
+    constexpr int P = 4;
+    int S = 32;
+    if (size_t(pitch4) * size_t((g.h + S - 1) / S) * g.batch < 148u * 512u) S = 16;
+    const int nstrips = (g.h + S - 1) / S;
+    const size_t threads = size_t(pitch4) * size_t(nstrips);
+    dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
+    if (S == 32)
+      pdl(k_near_stream<K, ERODE, 32, P>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask,
+          pitch4, g.slice, nstrips);
+    else
+      pdl(k_near_stream<K, ERODE, 16, P>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask,
+          pitch4, g.slice, nstrips);
+  }
 }
 
 template <bool ERODE>

@@ -205,7 +205,7 @@ int launch_fused(const FusedProgram& p, const Geo& gb, const Geo& gu, cudaStream
   } else {
     switch (p.n_bin) {
       case 0:
-      case 1: fused_launch<1, 4>(p, gb, gu, st); break;
+      case 1: fused_launch<1, 8>(p, gb, gu, st); break;
       case 2: fused_launch<2, 4>(p, gb, gu, st); break;
       case 3:
       case 4: fused_launch<4, 2>(p, gb, gu, st); break;
