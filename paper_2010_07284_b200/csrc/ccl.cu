@@ -28,6 +28,11 @@
 //   select / labels / maxvol  per word: every run's global root is P[P[key]]
 #include "slcs_internal.h"
 
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <vector>
+namespace cg = cooperative_groups;
+
 namespace slcs {
 
 KeyGeo key_geo(int w, int h) {
@@ -54,6 +59,7 @@ struct G {
   int s;
   uint32_t cmask;
   uint32_t sb;      // blocks per slice
+  uint32_t lastmask;  // valid bits of word wpr - 1
 };
 
 G make_g(const Geo& gb) {
@@ -69,6 +75,7 @@ G make_g(const Geo& gb) {
   g.s = k.s;
   g.cmask = k.cmask;
   g.sb = uint32_t(k.slice_blocks);
+  g.lastmask = gb.lastmask;
   return g;
 }
 
@@ -245,20 +252,54 @@ struct RunTile {
       k = gp;
     }
   }
+  // Linking priority: a multiplicative hash of the local key (high half) with
+  // the key itself as tie-break -- a random order.  Linking by key order
+  // (root = max pixel) builds long chains along rows/bands and funnels every
+  // union of a dense tile into one hot root slot; random linking keeps trees
+  // O(log n) deep.  Roots are therefore arbitrary representatives; the
+  // canonical max key is recovered separately where labels need it.
+  __device__ __forceinline__ static uint32_t pri(uint32_t k) {
+    return ((k * 0x9E3779B1u) & 0xffff0000u) | k;
+  }
   __device__ __forceinline__ void unite(uint32_t a, uint32_t b) const {
     for (;;) {
       a = find(a);
       b = find(b);
       if (a == b) return;
-      if (a < b) {
+      if (pri(a) < pri(b)) {
         const uint32_t t = a;
         a = b;
         b = t;
       }
-      const uint32_t old = atomicMax(par + slot(b), a);
-      if (old == b) return;
-      b = old;
+      // hang root b under a unless b stopped being a root meanwhile
+      if (atomicCAS(par + slot(b), b, a) == b) return;
     }
+  }
+  // After roots(): the max key of each run's component into the root's slot
+  // (par is free again); returns this thread's per-run component max keys.
+  __device__ void max_keys(int u, uint32_t T, uint32_t B, const uint32_t (&r)[16],
+                           uint32_t (&mk)[16]) const {
+    const int band = u / TWW, w = u % TWW;
+    uint32_t x = T | B;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (!x) break;
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      if (r[i] == key(band, w, T, B, m)) par[slot(r[i])] = 0;
+    }
+    __syncthreads();
+    x = T | B;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (!x) break;
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      atomicMax(par + slot(r[i]), key(band, w, T, B, m));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mk[i] = par[slot(r[i])];
   }
   // Roots of all runs, then unions with the band above (pixel adjacency
   // between B of band-1 and T of this band, incl. the diagonals into the
@@ -290,11 +331,13 @@ struct RunTile {
           a &= ~mu;
           unite(k, key(band - 1, w, Tu, Bu, mu));
         }
-        if ((td & 1u) && w > 0) {
+        // a diagonal link is redundant when the pixel straight above is set:
+        // that pixel's run is linked both ways already (vertical + row link)
+        if ((td & 1u) && w > 0 && !(Bu & 1u)) {
           const uint32_t Tl = sT[uu - 1], Bl = sB[uu - 1];
           if (Bl >> 31) unite(k, key(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31)));
         }
-        if ((td >> 31) && w + 1 < TWW) {
+        if ((td >> 31) && w + 1 < TWW && !(Bu >> 31)) {
           const uint32_t Tr = sT[uu + 1], Br = sB[uu + 1];
           if (Br & 1u) unite(k, key(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0)));
         }
@@ -410,6 +453,8 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
     }
   }
   __syncthreads();
+  uint32_t mk[16];  // MODE_CCL: component max keys (roots are hash-ordered)
+  if (MODE == MODE_CCL && SZ) tile.max_keys(u0, Tw, Bw, rt, mk);
   const size_t tile_id = (size_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   uint32_t* L = lists + tile_id * LT_LIST;
   {
@@ -427,7 +472,9 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
           const uint32_t b = kblk(g, gk);
           if (MODE == MODE_REACH) F[size_t(slice) * g.sb + b] = fl[ks];
           if (MODE == MODE_SIZE) SZ[size_t(slice) * g.sb + b] = lsz[ks];
-          if (MODE == MODE_CCL && SZ) SZ[size_t(slice) * g.sb + b] = gk;  // max key (MK)
+          if (MODE == MODE_CCL && SZ)  // component max key (MK)
+            SZ[size_t(slice) * g.sb + b] =
+                gkey(g, R0 + int(mk[i] >> LKW), C0 + int(mk[i] & lmask));
           if (touch[ks]) L[1 + atomicAdd(&s_cnt, 1)] = hnode(gk);
         }
       }
@@ -471,8 +518,9 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
       load_unit(u, g, k, j, T, B);
       load_unit(u, g, k - 1, j, Tu, Bu);
       uint32_t Tl = 0, Bl = 0, Tr = 0, Br = 0;
-      if (T & 1u) load_unit(u, g, k - 1, j - 1, Tl, Bl);
-      if (T >> 31) load_unit(u, g, k - 1, j + 1, Tr, Br);
+      // diagonals are redundant when the pixel straight above is set
+      if ((T & 1u) && !(Bu & 1u)) load_unit(u, g, k - 1, j - 1, Tl, Bl);
+      if ((T >> 31) && !(Bu >> 31)) load_unit(u, g, k - 1, j + 1, Tr, Br);
       const uint32_t cu = Tu | Bu;
       // the first link of every word goes through the warp dedupe (along a
       // solid stretch of border all words link the same two local roots);
@@ -520,10 +568,10 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
         uint32_t Tul, Bul, Tur, Bur;
         load_unit(u, g, k - 1, jl, Tul, Bul);
         load_unit(u, g, k - 1, jr, Tur, Bur);
-        if ((Tr & 1u) && (Bul >> 31))
+        if ((Tr & 1u) && (Bul >> 31) && !(Bur & 1u))
           gunite(Ps, g, grun(g, k, jr, Tr, Br, run_at(cr, 0)),
                  grun(g, k - 1, jl, Tul, Bul, run_at(Tul | Bul, 31)));
-        if ((Tl >> 31) && (Bur & 1u))
+        if ((Tl >> 31) && (Bur & 1u) && !(Bul >> 31))
           gunite(Ps, g, grun(g, k, jl, Tl, Bl, run_at(cl, 31)),
                  grun(g, k - 1, jr, Tur, Bur, run_at(Tur | Bur, 0)));
       }
@@ -881,6 +929,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict
   __syncthreads();
 
   if constexpr (MODE == 0) {
+    uint32_t mk[16];  // labels are the component max index + 1 (ccl.hpp:52-60)
+    tile.max_keys(u0, Tw, Bw, rt, mk);
     if (!in) return;
     uint32_t* Ls = out + size_t(slice) * size_t(g.W) * size_t(g.H);
     uint32_t labs[16];
@@ -894,8 +944,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict
           const uint32_t m = first_run(x);
           x &= ~m;
           starts |= m & (0u - m);
-          const uint32_t root = rt[q];
-          labs[q] = (root >> SKW) * uint32_t(g.W) + (root & ((1u << SKW) - 1u)) + 1u;
+          labs[q] = (mk[q] >> SKW) * uint32_t(g.W) + (mk[q] & ((1u << SKW) - 1u)) + 1u;
         }
       }
     }
@@ -1024,6 +1073,323 @@ int small_launch(const uint32_t* u, const uint32_t* t, uint32_t* out, const G& g
   return 1;
 }
 
+// ===========================================================================
+// Fused single-launch reach for images whose 256x256-px tiles are all
+// co-resident (<= 2 CTAs per SM, e.g. 4096^2 = 256 tiles on 148 SMs):
+// one cooperative launch with four grid barriers instead of five kernels.
+//   A  tile-local run union-find in shared memory (as k_tile_local); per local
+//      root a record {seeded, touches the tile ring, compact index}; ring
+//      roots get compact ids c = tile * 512 + idx (<= 508 ring roots per tile)
+//      and a node hnode(c) in a small global union-find GP (+ seed flag GF);
+//      runs that touch the ring publish P[key block] = their root's node
+//   B  each tile unites its own top and left borders on GP (atomicMax links)
+//   C  each tile flattens its ring roots (GP[c] = global root) and moves its
+//      seed flags to the global roots
+//   D  select: a run is kept if its (local or global) root is seeded; S | t
+//      goes to `sel` (global, L2-resident)
+//   E  the closing near^KOUT of sel for the tile's own words
+// Data written during the launch by other CTAs is read with ld.global.cg.
+constexpr uint32_t REC_SEED = 1u << 31, REC_RING = 1u << 30, REC_ROOT = 1u << 29, REC_IDX = 511u;
+constexpr int FT_LIST = 512;
+// per-tile words of the `lists` scratch region: LT_LIST for the multi-kernel
+// path, or GP (512 u32) + GF (512 B) for the fused one
+constexpr int FT_WORDS = 640;
+static_assert(FT_WORDS >= LT_LIST && FT_WORDS * 4 >= FT_LIST * 5, "lists region too small");
+
+__device__ __forceinline__ uint32_t cfind(uint32_t* GP, uint32_t v) {
+  for (;;) {
+    const uint32_t p = __ldcg(GP + hkey(v));
+    if (p == v) return v;
+    const uint32_t gp = __ldcg(GP + hkey(p));
+    if (gp == p) return p;
+    __stcg(GP + hkey(v), gp);
+    v = gp;
+  }
+}
+
+__device__ void cunite(uint32_t* GP, uint32_t a, uint32_t b) {
+  for (;;) {
+    a = cfind(GP, a);
+    b = cfind(GP, b);
+    if (a == b) return;
+    if (a < b) {
+      const uint32_t t = a;
+      a = b;
+      b = t;
+    }
+    const uint32_t old = atomicMax(GP + hkey(b), a);
+    if (old == b) return;
+    b = old;
+  }
+}
+
+// node of the ring run m of word j in band k (published by its tile in phase A)
+__device__ __forceinline__ uint32_t cnode(const uint32_t* P, const G& g, int k, int j, uint32_t T,
+                                          uint32_t B, uint32_t m) {
+  int dr, col;
+  run_max(T, B, m, dr, col);
+  return __ldcg(P + kblk(g, gkey(g, 2 * k + dr, 32 * j + col)));
+}
+
+__device__ __forceinline__ void cunite_dedup(uint32_t* GP, uint32_t a, uint32_t b, bool active) {
+  const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31;
+  const uint32_t plo = __shfl_up_sync(mask, lo, 1), phi = __shfl_up_sync(mask, hi, 1);
+  const bool prev_active = lane > 0 && ((mask >> (lane - 1)) & 1u);
+  if (!active || a == b) return;
+  if (prev_active && plo == lo && phi == hi) return;
+  cunite(GP, a, b);
+}
+
+// near^K word (r, j) of a bit image written during this launch (L2 reads)
+template <int K>
+__device__ __forceinline__ uint32_t near_word_cg(const uint32_t* s, const G& g, int r, int j) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int d = -K; d <= K; ++d) {
+    const int rr = r + d;
+    if (rr < 0 || rr >= g.H) continue;
+    const uint32_t* row = s + size_t(rr) * g.pitch;
+    const uint32_t C = __ldcg(row + j);
+    const uint32_t L = j > 0 ? __ldcg(row + j - 1) : 0u;
+    const uint32_t R = j + 1 < g.wpr ? __ldcg(row + j + 1) : 0u;
+    acc |= C;
+#pragma unroll
+    for (int e = 1; e <= K; ++e) acc |= __funnelshift_l(L, C, e) | __funnelshift_r(C, R, e);
+  }
+  return acc;
+}
+
+template <int KOUT>
+__global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* __restrict__ ubits,
+                                                               const uint32_t* __restrict__ tbits,
+                                                               uint32_t* P, uint32_t* GP,
+                                                               uint8_t* GF, uint32_t* sel,
+                                                               uint32_t* __restrict__ out, G g,
+                                                               long long* tstamp) {
+  cg::grid_group grid = cg::this_grid();
+  // diagnostics (SLCS_PHASE_TIMING=1): per-CTA clock64 at phase boundaries
+  int tsn = 0;
+  auto stamp = [&]() {
+    if (tstamp) {
+      __syncthreads();
+      if (threadIdx.x == 0)
+        tstamp[(size_t((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x)) * 16 + tsn] =
+            clock64();
+      ++tsn;
+    }
+  };
+  stamp();
+  extern __shared__ __align__(16) unsigned char lsm[];
+  uint32_t* par = reinterpret_cast<uint32_t*>(lsm);  // LSLOTS: union-find, then records
+  uint32_t* sT = par + LSLOTS;                        // LUNITS
+  uint32_t* sB = sT + LUNITS;                         // LUNITS
+  __shared__ int s_cnt;
+  using T = RunTile<LKW>;
+  const int slice = blockIdx.z;
+  const uint32_t* u = ubits + size_t(slice) * g.slice;
+  const uint32_t* t = tbits + size_t(slice) * g.slice;
+  uint32_t* Ps = P + size_t(slice) * g.sb;
+  uint32_t* ss = sel + size_t(slice) * g.slice;
+  const int u0 = threadIdx.x;
+  const int band = u0 / LTWW, w = u0 % LTWW;
+  const int kb = blockIdx.y * LTNB + band;
+  const int j = blockIdx.x * LTWW + w;
+  const int r = 2 * kb;
+  const bool in = kb < g.BH && j < g.wpr;
+  const bool two = r + 1 < g.H;
+  const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
+  const uint32_t Bw = (in && two) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
+  uint32_t seedT = 0, seedB = 0;
+  if (Tw | Bw) {
+    seedT = Tw & near_word(t, g, r, j);
+    seedB = two ? Bw & near_word(t, g, r + 1, j) : 0u;
+  }
+  sT[u0] = Tw;
+  sB[u0] = Bw;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  stamp();  // 1: loads
+  T tile{par, sT, sB};
+  tile.link(u0, Tw, Bw);
+  stamp();  // 2: link
+  // flatten in place: a run's slot holds its root key, a root's slot holds its
+  // record (REC_ROOT set) -- no per-run root registers stay live afterwards
+  {
+    uint32_t rt[16];
+    tile.roots(u0, Tw, Bw, rt);
+    __syncthreads();
+    uint32_t x = Tw | Bw;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (!x) break;
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      const uint32_t k = T::key(band, w, Tw, Bw, m);
+      par[T::slot(k)] = rt[i] == k ? REC_ROOT : rt[i];
+    }
+  }
+  __syncthreads();
+  stamp();  // 3: roots
+  auto root_of = [&](uint32_t k) {
+    const uint32_t v = par[T::slot(k)];
+    return (v & REC_ROOT) ? k : v;
+  };
+
+  // ---- A: per-root records, compact ids of ring roots, ring runs -> P
+  const uint32_t tile_id = (uint32_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const int R0 = blockIdx.y * LTNB * 2, C0 = blockIdx.x * LTWW * 32;
+  const uint32_t lmask = (1u << LKW) - 1u;
+  auto ring_run = [&](uint32_t m) {
+    return band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31));
+  };
+  for (uint32_t x = Tw | Bw; x;) {
+    const uint32_t m = first_run(x);
+    x &= ~m;
+    const uint32_t marks = (ring_run(m) ? REC_RING : 0u) | (((seedT | seedB) & m) ? REC_SEED : 0u);
+    if (marks) atomicOr(par + T::slot(root_of(T::key(band, w, Tw, Bw, m))), marks);
+  }
+  __syncthreads();
+  for (uint32_t x = Tw | Bw; x;) {
+    const uint32_t m = first_run(x);
+    x &= ~m;
+    const uint32_t k = T::key(band, w, Tw, Bw, m);
+    const uint32_t rec = par[T::slot(k)];
+    if ((rec & REC_ROOT) && (rec & REC_RING)) {
+      const uint32_t idx = uint32_t(atomicAdd(&s_cnt, 1));
+      par[T::slot(k)] = rec | idx;
+      const uint32_t c = tile_id * FT_LIST + idx;
+      __stcg(GP + c, hnode(c));
+      __stcg(GF + c, uint8_t((rec & REC_SEED) ? 1 : 0));
+    }
+  }
+  __syncthreads();
+  for (uint32_t x = Tw | Bw; x;) {
+    const uint32_t m = first_run(x);
+    x &= ~m;
+    if (ring_run(m)) {
+      const uint32_t k = T::key(band, w, Tw, Bw, m);
+      const uint32_t c = tile_id * FT_LIST + (par[T::slot(root_of(k))] & REC_IDX);
+      __stcg(Ps + kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask))), hnode(c));
+    }
+  }
+  stamp();  // 4: records + publish
+  grid.sync();
+  stamp();  // 5: barrier
+
+  // ---- B: unions across this tile's left border (threads 0..127) and top
+  // border (threads 128..135)
+  if (u0 < LTNB) {
+    const int k = blockIdx.y * LTNB + u0;
+    const int jr = blockIdx.x * LTWW, jl = jr - 1;
+    if (blockIdx.x > 0 && k < g.BH) {
+      uint32_t Tl, Bl, Tr, Br;
+      load_unit(u, g, k, jl, Tl, Bl);
+      load_unit(u, g, k, jr, Tr, Br);
+      const uint32_t cl = Tl | Bl, cr = Tr | Br;
+      const bool hlink = (cl >> 31) && (cr & 1u);
+      const uint32_t va = hlink ? cnode(Ps, g, k, jl, Tl, Bl, run_at(cl, 31)) : 0u;
+      const uint32_t vb = hlink ? cnode(Ps, g, k, jr, Tr, Br, run_at(cr, 0)) : 0u;
+      cunite_dedup(GP, va, vb, hlink);
+      if (u0 != 0 && ((Tr & 1u) || (Tl >> 31))) {
+        uint32_t Tul, Bul, Tur, Bur;
+        load_unit(u, g, k - 1, jl, Tul, Bul);
+        load_unit(u, g, k - 1, jr, Tur, Bur);
+        if ((Tr & 1u) && (Bul >> 31) && !(Bur & 1u))
+          cunite(GP, cnode(Ps, g, k, jr, Tr, Br, run_at(cr, 0)),
+                 cnode(Ps, g, k - 1, jl, Tul, Bul, run_at(Tul | Bul, 31)));
+        if ((Tl >> 31) && (Bur & 1u) && !(Bul >> 31))
+          cunite(GP, cnode(Ps, g, k, jl, Tl, Bl, run_at(cl, 31)),
+                 cnode(Ps, g, k - 1, jr, Tur, Bur, run_at(Tur | Bur, 0)));
+      }
+    }
+  } else if (u0 < LTNB + LTWW) {
+    const int k = blockIdx.y * LTNB;
+    const int jj = blockIdx.x * LTWW + (u0 - LTNB);
+    if (blockIdx.y > 0 && jj < g.wpr) {
+      uint32_t T0, B0, Tu, Bu;
+      load_unit(u, g, k, jj, T0, B0);
+      load_unit(u, g, k - 1, jj, Tu, Bu);
+      uint32_t Tl = 0, Bl = 0, Tr = 0, Br = 0;
+      if ((T0 & 1u) && !(Bu & 1u)) load_unit(u, g, k - 1, jj - 1, Tl, Bl);
+      if ((T0 >> 31) && !(Bu >> 31)) load_unit(u, g, k - 1, jj + 1, Tr, Br);
+      const uint32_t cu = Tu | Bu;
+      for (uint32_t x = T0 | B0; x;) {
+        const uint32_t m = first_run(x);
+        x &= ~m;
+        const uint32_t td = T0 & m;
+        if (!td) continue;
+        const uint32_t v = cnode(Ps, g, k, jj, T0, B0, m);
+        for (uint32_t a = dil1(td) & Bu; a;) {
+          const uint32_t mu = run_at(cu, __ffs(a) - 1);
+          a &= ~mu;
+          cunite(GP, v, cnode(Ps, g, k - 1, jj, Tu, Bu, mu));
+        }
+        if ((td & 1u) && (Bl >> 31)) cunite(GP, v, cnode(Ps, g, k - 1, jj - 1, Tl, Bl, run_at(Tl | Bl, 31)));
+        if ((td >> 31) && (Br & 1u)) cunite(GP, v, cnode(Ps, g, k - 1, jj + 1, Tr, Br, run_at(Tr | Br, 0)));
+      }
+    }
+  }
+  stamp();  // 6: merge
+  grid.sync();
+  stamp();  // 7: barrier
+
+  // ---- C: flatten this tile's ring roots, move seed flags to global roots
+  if (u0 < s_cnt) {
+    const uint32_t c = tile_id * FT_LIST + uint32_t(u0);
+    const uint32_t v = hnode(c);
+    uint32_t R = __ldcg(GP + c);
+    while (true) {
+      const uint32_t q = __ldcg(GP + hkey(R));
+      if (q == R) break;
+      R = q;
+    }
+    if (R != v) {
+      __stcg(GP + c, R);
+      if (__ldcg(GF + c)) __stcg(GF + hkey(R), uint8_t(1));
+    }
+  }
+  stamp();  // 8: flatten
+  grid.sync();
+  stamp();  // 9: barrier
+
+  // ---- D: select (S | t) into sel
+  {
+    uint32_t ST = 0, SB = 0;
+    for (uint32_t x = Tw | Bw; x;) {
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      const uint32_t rec = par[T::slot(root_of(T::key(band, w, Tw, Bw, m)))];
+      bool seeded = rec & REC_SEED;
+      if (rec & REC_RING) {
+        const uint32_t R = __ldcg(GP + tile_id * FT_LIST + (rec & REC_IDX));
+        seeded = __ldcg(GF + hkey(R)) != 0;
+      }
+      if (seeded) {
+        ST |= Tw & m;
+        SB |= Bw & m;
+      }
+    }
+    if (in) {
+      __stcg(ss + size_t(r) * g.pitch + j, ST | __ldg(t + size_t(r) * g.pitch + j));
+      if (two) __stcg(ss + size_t(r + 1) * g.pitch + j, SB | __ldg(t + size_t(r + 1) * g.pitch + j));
+    }
+  }
+  stamp();  // 10: select
+  grid.sync();
+  stamp();  // 11: barrier
+
+  // ---- E: closing near^KOUT of the tile's own words; padding words -> 0
+  if (kb < g.BH && j < int(g.pitch)) {
+    uint32_t* o = out + size_t(slice) * g.slice;
+    const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
+    o[size_t(r) * g.pitch + j] = j < g.wpr ? near_word_cg<KOUT>(ss, g, r, j) & vm : 0u;
+    if (two) o[size_t(r + 1) * g.pitch + j] = j < g.wpr ? near_word_cg<KOUT>(ss, g, r + 1, j) & vm : 0u;
+  }
+  stamp();  // 12: near
+}
+
 int grid_blocks(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -1055,7 +1421,7 @@ size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes) {
 size_t ccl_scratch_bytes_large(int w, int h, int batch, bool flags, bool sizes) {
   KeyGeo k = key_geo(w, h);
   size_t n = k.slice_blocks * size_t(batch);
-  size_t b = round_up(n * 4, 256) + round_up(n_tiles(w, h) * size_t(batch) * LT_LIST * 4, 256);
+  size_t b = round_up(n * 4, 256) + round_up(n_tiles(w, h) * size_t(batch) * FT_WORDS * 4, 256);
   if (flags) b += round_up(n, 256);
   if (sizes) b += round_up(n * 4, 256) + round_up(size_t(batch) * 4, 256);
   return b;
@@ -1077,7 +1443,7 @@ void ccl_scratch_carve_large(void* base, int w, int h, int batch, bool flags, bo
   s->parent = reinterpret_cast<uint32_t*>(p);
   p += round_up(n * 4, 256);
   s->lists = reinterpret_cast<uint32_t*>(p);
-  p += round_up(n_tiles(w, h) * size_t(batch) * LT_LIST * 4, 256);
+  p += round_up(n_tiles(w, h) * size_t(batch) * FT_WORDS * 4, 256);
   if (flags) {
     s->flag = p;
     p += round_up(n, 256);
@@ -1213,6 +1579,79 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   return launches + 1;
 }
 
+template <int KOUT>
+bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* out,
+                     uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st) {
+  static int capacity = -1;  // co-resident CTAs on this device
+  const size_t smem = size_t(LSLOTS) * 4 + 2 * size_t(LUNITS) * 4;
+  if (capacity < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaFuncSetAttribute(k_reach_fused<KOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT>, LT_THREADS,
+                                                      smem) != cudaSuccess)
+      per = 0;
+    capacity = per * sms;
+    cudaGetLastError();
+  }
+  dim3 grid(unsigned((g.wpr + LTWW - 1) / LTWW), unsigned((g.BH + LTNB - 1) / LTNB),
+            unsigned(batch));
+  const size_t tiles = size_t(grid.x) * grid.y * grid.z;
+  if (tiles > size_t(capacity)) return false;
+  uint32_t* GP = s.lists;
+  uint8_t* GF = reinterpret_cast<uint8_t*>(s.lists + tiles * FT_LIST);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(LT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static const bool timing = [] {
+    const char* e = std::getenv("SLCS_PHASE_TIMING");
+    return e && *e == '1';
+  }();
+  long long* ts = nullptr;
+  if (timing) cuda_check(cudaMalloc(&ts, tiles * 16 * sizeof(long long)), "timing buffer");
+  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT>, through, target, s.parent, GP, GF,
+                                tmp_bits, out, g, ts),
+             "fused reach launch");
+  if (timing) {  // diagnostics only: per-phase mean / max over CTAs, in clocks
+    std::vector<long long> h(tiles * 16);
+    cuda_check(cudaStreamSynchronize(st), "timing sync");
+    cuda_check(cudaMemcpy(h.data(), ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost),
+               "timing copy");
+    cudaFree(ts);
+    const char* names[] = {"load", "link", "roots", "records", "bar1", "merge", "bar2",
+                           "flatten", "bar3", "select", "bar4", "near"};
+    std::fprintf(stderr, "[fused reach %zu tiles]", tiles);
+    for (int ph = 1; ph <= 12; ++ph) {
+      double sum = 0, mx = 0;
+      for (size_t t = 0; t < tiles; ++t) {
+        const double d = double(h[t * 16 + ph] - h[t * 16 + ph - 1]);
+        sum += d;
+        mx = d > mx ? d : mx;
+      }
+      std::fprintf(stderr, " %s %.0f/%.0f", names[ph - 1], sum / tiles, mx);
+    }
+    std::fprintf(stderr, " (clocks mean/max)\n");
+  }
+  return true;
+}
+
+bool fused_reach_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SLCS_NO_FUSED_REACH");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
                  uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st, int k_out) {
   G g = make_g(gb);
@@ -1221,6 +1660,17 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
     return small_launch<1>(through, target, out, g, gb.batch, st);
   }
   check_key_range(gb, "reach");
+  if (fused_reach_enabled()) {
+    bool done = false;
+    switch (k_out) {
+      case 1: done = reach_fused_try<1>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 2: done = reach_fused_try<2>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 3: done = reach_fused_try<3>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 4: done = reach_fused_try<4>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      default: break;
+    }
+    if (done) return 1;
+  }
   int launches = 0;
   large_local_and_merge(through, target, g, gb.batch, s, MODE_REACH, st, launches);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
