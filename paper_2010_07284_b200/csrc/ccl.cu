@@ -29,6 +29,7 @@
 #include "slcs_internal.h"
 
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 namespace cg = cooperative_groups;
@@ -241,38 +242,47 @@ struct RunTile {
     run_max(T, B, m, dr, col);
     return (uint32_t(2 * band + dr) << KW) | uint32_t(32 * w + col);
   }
-  __device__ __forceinline__ uint32_t find(uint32_t k) const {
+  // Union-find nodes are (priority << 16) | slot: the high half is a hash of
+  // the local key (a random linking order), the low half the parent slot, so
+  // a find step needs no key arithmetic.  Linking by key order (root = max
+  // pixel) builds long chains along rows/bands; random linking keeps trees
+  // O(log n) deep, and atomicMax linking lets concurrent unions on one root
+  // all make progress.  Roots are therefore arbitrary representatives; the
+  // canonical max key is recovered separately where labels need it.
+  __device__ __forceinline__ static uint32_t node(uint32_t k) {
+    uint32_t x = (k * 0x9E37u) & 0xffffu;
+    x ^= x >> 7;
+    return (x << 16) | uint32_t(slot(k));
+  }
+  __device__ __forceinline__ static int nslot(uint32_t v) { return int(v & 0xffffu); }
+  // a representative key of a slot's 2x2 block (top-left pixel)
+  __device__ __forceinline__ static uint32_t bkey(int sl) {
+    return (uint32_t(sl >> BL) << (KW + 1)) | (uint32_t(sl & ((1 << BL) - 1)) << 1);
+  }
+  __device__ __forceinline__ uint32_t find(uint32_t v) const {
     volatile uint32_t* vp = par;
     for (;;) {
-      const uint32_t p = vp[slot(k)];
-      if (p == k) return k;
-      const uint32_t gp = vp[slot(p)];
+      const uint32_t p = vp[nslot(v)];
+      if (p == v) return v;
+      const uint32_t gp = vp[nslot(p)];
       if (gp == p) return p;
-      vp[slot(k)] = gp;
-      k = gp;
+      vp[nslot(v)] = gp;
+      v = gp;
     }
-  }
-  // Linking priority: a multiplicative hash of the local key (high half) with
-  // the key itself as tie-break -- a random order.  Linking by key order
-  // (root = max pixel) builds long chains along rows/bands and funnels every
-  // union of a dense tile into one hot root slot; random linking keeps trees
-  // O(log n) deep.  Roots are therefore arbitrary representatives; the
-  // canonical max key is recovered separately where labels need it.
-  __device__ __forceinline__ static uint32_t pri(uint32_t k) {
-    return ((k * 0x9E3779B1u) & 0xffff0000u) | k;
   }
   __device__ __forceinline__ void unite(uint32_t a, uint32_t b) const {
     for (;;) {
       a = find(a);
       b = find(b);
       if (a == b) return;
-      if (pri(a) < pri(b)) {
+      if (a < b) {
         const uint32_t t = a;
         a = b;
         b = t;
       }
-      // hang root b under a unless b stopped being a root meanwhile
-      if (atomicCAS(par + slot(b), b, a) == b) return;
+      const uint32_t old = atomicMax(par + nslot(b), a);
+      if (old == b) return;
+      b = old;
     }
   }
   // After roots(): the max key of each run's component into the root's slot
@@ -286,7 +296,7 @@ struct RunTile {
       if (!x) break;
       const uint32_t m = first_run(x);
       x &= ~m;
-      if (r[i] == key(band, w, T, B, m)) par[slot(r[i])] = 0;
+      if (r[i] == node(key(band, w, T, B, m))) par[nslot(r[i])] = 0;
     }
     __syncthreads();
     x = T | B;
@@ -295,11 +305,11 @@ struct RunTile {
       if (!x) break;
       const uint32_t m = first_run(x);
       x &= ~m;
-      atomicMax(par + slot(r[i]), key(band, w, T, B, m));
+      atomicMax(par + nslot(r[i]), key(band, w, T, B, m));
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) mk[i] = par[slot(r[i])];
+    for (int i = 0; i < 16; ++i) mk[i] = par[nslot(r[i])];
   }
   // Roots of all runs, then unions with the band above (pixel adjacency
   // between B of band-1 and T of this band, incl. the diagonals into the
@@ -311,16 +321,16 @@ struct RunTile {
       const uint32_t m = first_run(x);
       x &= ~m;
       const uint32_t k = key(band, w, T, B, m);
-      par[slot(k)] = k;
+      par[slot(k)] = node(k);
     }
     __syncthreads();
     for (uint32_t x = T | B; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
-      const uint32_t k = key(band, w, T, B, m);
+      const uint32_t k = node(key(band, w, T, B, m));
       if ((m >> 31) && w + 1 < TWW) {
         const uint32_t T2 = sT[u + 1], B2 = sB[u + 1];
-        if ((T2 | B2) & 1u) unite(k, key(band, w + 1, T2, B2, first_run(T2 | B2)));
+        if ((T2 | B2) & 1u) unite(k, node(key(band, w + 1, T2, B2, first_run(T2 | B2))));
       }
       const uint32_t td = T & m;
       if (band > 0 && td) {
@@ -329,17 +339,17 @@ struct RunTile {
         for (uint32_t a = dil1(td) & Bu; a;) {
           const uint32_t mu = run_at(cu, __ffs(a) - 1);
           a &= ~mu;
-          unite(k, key(band - 1, w, Tu, Bu, mu));
+          unite(k, node(key(band - 1, w, Tu, Bu, mu)));
         }
         // a diagonal link is redundant when the pixel straight above is set:
         // that pixel's run is linked both ways already (vertical + row link)
         if ((td & 1u) && w > 0 && !(Bu & 1u)) {
           const uint32_t Tl = sT[uu - 1], Bl = sB[uu - 1];
-          if (Bl >> 31) unite(k, key(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31)));
+          if (Bl >> 31) unite(k, node(key(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31))));
         }
         if ((td >> 31) && w + 1 < TWW && !(Bu >> 31)) {
           const uint32_t Tr = sT[uu + 1], Br = sB[uu + 1];
-          if (Br & 1u) unite(k, key(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0)));
+          if (Br & 1u) unite(k, node(key(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0))));
         }
       }
     }
@@ -359,7 +369,7 @@ struct RunTile {
       if (!x) break;
       const uint32_t m = first_run(x);
       x &= ~m;
-      r[i] = find(key(band, w, T, B, m));
+      r[i] = find(node(key(band, w, T, B, m)));
     }
   }
 };
@@ -441,10 +451,10 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
-        const uint32_t root = rt[i];
+        const int rs = T::nslot(rt[i]);
+        const uint32_t rk = T::bkey(rs);  // the root's block stands for it globally
         Ps[kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask)))] =
-            gnode(g, R0 + int(root >> LKW), C0 + int(root & lmask));
-        const int rs = T::slot(root);
+            gnode(g, R0 + int(rk >> LKW), C0 + int(rk & lmask));
         if (band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31)))
           touch[rs] = 1;
         if (MODE == MODE_REACH && (((Tw & ntT) | (Bw & ntB)) & m)) fl[rs] = 1;
@@ -466,9 +476,10 @@ __global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __res
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
-        if (rt[i] == k) {  // local root
+        if (rt[i] == T::node(k)) {  // local root
           const int ks = T::slot(k);
-          const uint32_t gk = gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask));
+          const uint32_t bk = T::bkey(ks);
+          const uint32_t gk = gkey(g, R0 + int(bk >> LKW), C0 + int(bk & lmask));
           const uint32_t b = kblk(g, gk);
           if (MODE == MODE_REACH) F[size_t(slice) * g.sb + b] = fl[ks];
           if (MODE == MODE_SIZE) SZ[size_t(slice) * g.sb + b] = lsz[ks];
@@ -828,7 +839,7 @@ __global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t
 }
 
 // maxvol: max size over global roots (a run is a global root iff its block
-// slot points at itself)
+// slot points at a node of its own block)
 __global__ void k_maxvol_max(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
                              const uint32_t* __restrict__ SZ, unsigned int* maxv, G g) {
   slcs_pdl_wait();
@@ -845,8 +856,10 @@ __global__ void k_maxvol_max(const uint32_t* __restrict__ ubits, const uint32_t*
     for (uint32_t x = T | B; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
-      const uint32_t v = grun(g, k, j, T, B, m);
-      if (Ps[gblk(g, v)] == v) best = max(best, Ss[gblk(g, v)]);
+      // a global root's block holds a node of that same block (roots are
+      // represented by their block, not by the run's own key)
+      const uint32_t b = gblk(g, grun(g, k, j, T, B, m));
+      if (gblk(g, Ps[b]) == b) best = max(best, Ss[b]);
     }
   }
 #pragma unroll
@@ -899,7 +912,7 @@ size_t small_smem_bytes() { return size_t(SSLOTS) * 4 + 2 * ST_THREADS * 4 + 256
 
 // mode 0 = labels, 1 = reach, 2 = maxvol
 template <int MODE>
-__global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict__ ubits,
+__global__ void __launch_bounds__(ST_THREADS, 1) k_small(const uint32_t* __restrict__ ubits,
                                                       const uint32_t* __restrict__ tbits,
                                                       uint32_t* __restrict__ out, G g) {
   slcs_pdl_wait();
@@ -976,7 +989,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict
         if (x) {
           const uint32_t m = first_run(x);
           x &= ~m;
-          if (((Tw & ntT) | (Bw & ntB)) & m) par[T::slot(rt[q])] = 1;
+          if (((Tw & ntT) | (Bw & ntB)) & m) par[T::nslot(rt[q])] = 1;
         }
     }
     __syncthreads();
@@ -987,7 +1000,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict
         if (x) {
           const uint32_t m = first_run(x);
           x &= ~m;
-          if (par[T::slot(rt[q])]) {
+          if (par[T::nslot(rt[q])]) {
             ST |= Tw & m;
             SB |= Bw & m;
           }
@@ -1026,7 +1039,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict
         if (x) {
           const uint32_t m = first_run(x);
           x &= ~m;
-          atomicAdd(par + T::slot(rt[q]), uint32_t(__popc(Tw & m) + __popc(Bw & m)));
+          atomicAdd(par + T::nslot(rt[q]), uint32_t(__popc(Tw & m) + __popc(Bw & m)));
         }
     }
     __syncthreads();
@@ -1044,7 +1057,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_small(const uint32_t* __restrict
         if (x) {
           const uint32_t m = first_run(x);
           x &= ~m;
-          if (par[T::slot(rt[q])] == mx) {
+          if (par[T::nslot(rt[q])] == mx) {
             ST |= Tw & m;
             SB |= Bw & m;
           }
@@ -1092,9 +1105,10 @@ int small_launch(const uint32_t* u, const uint32_t* t, uint32_t* out, const G& g
 constexpr uint32_t REC_SEED = 1u << 31, REC_RING = 1u << 30, REC_ROOT = 1u << 29, REC_IDX = 511u;
 constexpr int FT_LIST = 512;
 // per-tile words of the `lists` scratch region: LT_LIST for the multi-kernel
-// path, or GP (512 u32) + GF (512 B) for the fused one
-constexpr int FT_WORDS = 640;
-static_assert(FT_WORDS >= LT_LIST && FT_WORDS * 4 >= FT_LIST * 5, "lists region too small");
+// path, or GP (512 u32) + GF (512 B) per fused tile
+// (fused tiles may be half as tall: two per multi-kernel tile)
+constexpr int FT_WORDS = 1280;
+static_assert(FT_WORDS >= LT_LIST && FT_WORDS * 4 >= 2 * FT_LIST * 5, "lists region too small");
 
 __device__ __forceinline__ uint32_t cfind(uint32_t* GP, uint32_t v) {
   for (;;) {
@@ -1161,30 +1175,34 @@ __device__ __forceinline__ uint32_t near_word_cg(const uint32_t* s, const G& g, 
   return acc;
 }
 
-template <int KOUT>
-__global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* __restrict__ ubits,
+template <int KOUT, int NB>
+__global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(const uint32_t* __restrict__ ubits,
                                                                const uint32_t* __restrict__ tbits,
                                                                uint32_t* P, uint32_t* GP,
                                                                uint8_t* GF, uint32_t* sel,
                                                                uint32_t* __restrict__ out, G g,
                                                                long long* tstamp) {
   cg::grid_group grid = cg::this_grid();
-  // diagnostics (SLCS_PHASE_TIMING=1): per-CTA clock64 at phase boundaries
+  // diagnostics (SLCS_PHASE_TIMING=1): per-CTA %globaltimer (ns) at phase boundaries
   int tsn = 0;
   auto stamp = [&]() {
     if (tstamp) {
       __syncthreads();
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0) {
+        long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
         tstamp[(size_t((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x)) * 16 + tsn] =
-            clock64();
+            ns;
+      }
       ++tsn;
     }
   };
   stamp();
   extern __shared__ __align__(16) unsigned char lsm[];
-  uint32_t* par = reinterpret_cast<uint32_t*>(lsm);  // LSLOTS: union-find, then records
-  uint32_t* sT = par + LSLOTS;                        // LUNITS
-  uint32_t* sB = sT + LUNITS;                         // LUNITS
+  constexpr int UNITS = NB * LTWW, SLOTS = NB * (1 << (LKW - 1));
+  uint32_t* par = reinterpret_cast<uint32_t*>(lsm);  // SLOTS: union-find, then records
+  uint32_t* sT = par + SLOTS;                         // UNITS
+  uint32_t* sB = sT + UNITS;                          // UNITS
   __shared__ int s_cnt;
   using T = RunTile<LKW>;
   const int slice = blockIdx.z;
@@ -1194,7 +1212,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* _
   uint32_t* ss = sel + size_t(slice) * g.slice;
   const int u0 = threadIdx.x;
   const int band = u0 / LTWW, w = u0 % LTWW;
-  const int kb = blockIdx.y * LTNB + band;
+  const int kb = blockIdx.y * NB + band;
   const int j = blockIdx.x * LTWW + w;
   const int r = 2 * kb;
   const bool in = kb < g.BH && j < g.wpr;
@@ -1227,28 +1245,28 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* _
       const uint32_t m = first_run(x);
       x &= ~m;
       const uint32_t k = T::key(band, w, Tw, Bw, m);
-      par[T::slot(k)] = rt[i] == k ? REC_ROOT : rt[i];
+      par[T::slot(k)] = rt[i] == T::node(k) ? REC_ROOT : uint32_t(T::nslot(rt[i]));
     }
   }
   __syncthreads();
   stamp();  // 3: roots
-  auto root_of = [&](uint32_t k) {
+  auto root_of = [&](uint32_t k) {  // the root's slot
     const uint32_t v = par[T::slot(k)];
-    return (v & REC_ROOT) ? k : v;
+    return (v & REC_ROOT) ? uint32_t(T::slot(k)) : v;
   };
 
   // ---- A: per-root records, compact ids of ring roots, ring runs -> P
   const uint32_t tile_id = (uint32_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  const int R0 = blockIdx.y * LTNB * 2, C0 = blockIdx.x * LTWW * 32;
+  const int R0 = blockIdx.y * NB * 2, C0 = blockIdx.x * LTWW * 32;
   const uint32_t lmask = (1u << LKW) - 1u;
   auto ring_run = [&](uint32_t m) {
-    return band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31));
+    return band == 0 || band == NB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31));
   };
   for (uint32_t x = Tw | Bw; x;) {
     const uint32_t m = first_run(x);
     x &= ~m;
     const uint32_t marks = (ring_run(m) ? REC_RING : 0u) | (((seedT | seedB) & m) ? REC_SEED : 0u);
-    if (marks) atomicOr(par + T::slot(root_of(T::key(band, w, Tw, Bw, m))), marks);
+    if (marks) atomicOr(par + root_of(T::key(band, w, Tw, Bw, m)), marks);
   }
   __syncthreads();
   for (uint32_t x = Tw | Bw; x;) {
@@ -1270,7 +1288,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* _
     x &= ~m;
     if (ring_run(m)) {
       const uint32_t k = T::key(band, w, Tw, Bw, m);
-      const uint32_t c = tile_id * FT_LIST + (par[T::slot(root_of(k))] & REC_IDX);
+      const uint32_t c = tile_id * FT_LIST + (par[root_of(k)] & REC_IDX);
       __stcg(Ps + kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask))), hnode(c));
     }
   }
@@ -1280,8 +1298,8 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* _
 
   // ---- B: unions across this tile's left border (threads 0..127) and top
   // border (threads 128..135)
-  if (u0 < LTNB) {
-    const int k = blockIdx.y * LTNB + u0;
+  if (u0 < NB) {
+    const int k = blockIdx.y * NB + u0;
     const int jr = blockIdx.x * LTWW, jl = jr - 1;
     if (blockIdx.x > 0 && k < g.BH) {
       uint32_t Tl, Bl, Tr, Br;
@@ -1304,9 +1322,9 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* _
                  cnode(Ps, g, k - 1, jr, Tur, Bur, run_at(Tur | Bur, 0)));
       }
     }
-  } else if (u0 < LTNB + LTWW) {
-    const int k = blockIdx.y * LTNB;
-    const int jj = blockIdx.x * LTWW + (u0 - LTNB);
+  } else if (u0 < NB + LTWW) {
+    const int k = blockIdx.y * NB;
+    const int jj = blockIdx.x * LTWW + (u0 - NB);
     if (blockIdx.y > 0 && jj < g.wpr) {
       uint32_t T0, B0, Tu, Bu;
       load_unit(u, g, k, jj, T0, B0);
@@ -1360,7 +1378,7 @@ __global__ void __launch_bounds__(LT_THREADS, 2) k_reach_fused(const uint32_t* _
     for (uint32_t x = Tw | Bw; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
-      const uint32_t rec = par[T::slot(root_of(T::key(band, w, Tw, Bw, m)))];
+      const uint32_t rec = par[root_of(T::key(band, w, Tw, Bw, m))];
       bool seeded = rec & REC_SEED;
       if (rec & REC_RING) {
         const uint32_t R = __ldcg(GP + tile_id * FT_LIST + (rec & REC_IDX));
@@ -1579,24 +1597,25 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   return launches + 1;
 }
 
-template <int KOUT>
+template <int KOUT, int NB>
 bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* out,
                      uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st) {
   static int capacity = -1;  // co-resident CTAs on this device
-  const size_t smem = size_t(LSLOTS) * 4 + 2 * size_t(LUNITS) * 4;
+  constexpr int THREADS = NB * LTWW;
+  const size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4;
   if (capacity < 0) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaFuncSetAttribute(k_reach_fused<KOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k_reach_fused<KOUT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem)) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT>, LT_THREADS,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT, NB>, THREADS,
                                                       smem) != cudaSuccess)
       per = 0;
     capacity = per * sms;
     cudaGetLastError();
   }
-  dim3 grid(unsigned((g.wpr + LTWW - 1) / LTWW), unsigned((g.BH + LTNB - 1) / LTNB),
+  dim3 grid(unsigned((g.wpr + LTWW - 1) / LTWW), unsigned((g.BH + NB - 1) / NB),
             unsigned(batch));
   const size_t tiles = size_t(grid.x) * grid.y * grid.z;
   if (tiles > size_t(capacity)) return false;
@@ -1604,7 +1623,7 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   uint8_t* GF = reinterpret_cast<uint8_t*>(s.lists + tiles * FT_LIST);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(LT_THREADS);
+  cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1618,28 +1637,37 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   }();
   long long* ts = nullptr;
   if (timing) cuda_check(cudaMalloc(&ts, tiles * 16 * sizeof(long long)), "timing buffer");
-  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT>, through, target, s.parent, GP, GF,
+  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT, NB>, through, target, s.parent, GP, GF,
                                 tmp_bits, out, g, ts),
              "fused reach launch");
-  if (timing) {  // diagnostics only: per-phase mean / max over CTAs, in clocks
+  if (timing) {  // diagnostics only: timeline of phase ends, min/max over CTAs (us)
     std::vector<long long> h(tiles * 16);
     cuda_check(cudaStreamSynchronize(st), "timing sync");
     cuda_check(cudaMemcpy(h.data(), ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost),
                "timing copy");
     cudaFree(ts);
-    const char* names[] = {"load", "link", "roots", "records", "bar1", "merge", "bar2",
+    const char* names[] = {"start", "load", "link", "roots", "records", "bar1", "merge", "bar2",
                            "flatten", "bar3", "select", "bar4", "near"};
-    std::fprintf(stderr, "[fused reach %zu tiles]", tiles);
-    for (int ph = 1; ph <= 12; ++ph) {
-      double sum = 0, mx = 0;
+    long long t0 = h[0];
+    for (size_t t = 0; t < tiles; ++t) t0 = h[t * 16] < t0 ? h[t * 16] : t0;
+    std::fprintf(stderr, "[fused reach %zu tiles, us since first CTA: min/max]", tiles);
+    for (int ph = 0; ph <= 12; ++ph) {
+      long long mn = h[ph], mx = h[ph];
       for (size_t t = 0; t < tiles; ++t) {
-        const double d = double(h[t * 16 + ph] - h[t * 16 + ph - 1]);
-        sum += d;
-        mx = d > mx ? d : mx;
+        mn = h[t * 16 + ph] < mn ? h[t * 16 + ph] : mn;
+        mx = h[t * 16 + ph] > mx ? h[t * 16 + ph] : mx;
       }
-      std::fprintf(stderr, " %s %.0f/%.0f", names[ph - 1], sum / tiles, mx);
+      std::fprintf(stderr, " %s %.1f/%.1f", names[ph], (mn - t0) / 1e3, (mx - t0) / 1e3);
     }
-    std::fprintf(stderr, " (clocks mean/max)\n");
+    std::fprintf(stderr, "\n");
+    std::vector<std::pair<long long, size_t>> ld;
+    for (size_t t = 0; t < tiles; ++t) ld.push_back({h[t * 16 + 2] - h[t * 16 + 1], t});
+    std::sort(ld.begin(), ld.end());
+    std::fprintf(stderr, "  link us: median %.1f, slowest tiles (x,y):", ld[tiles / 2].first / 1e3);
+    for (size_t q = tiles > 6 ? tiles - 6 : 0; q < tiles; ++q)
+      std::fprintf(stderr, " %.1f@(%zu,%zu)", ld[q].first / 1e3, ld[q].second % grid.x,
+                   (ld[q].second / grid.x) % grid.y);
+    std::fprintf(stderr, "\n");
   }
   return true;
 }
@@ -1661,12 +1689,20 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
   }
   check_key_range(gb, "reach");
   if (fused_reach_enabled()) {
+    static const int nb = [] {
+      const char* e = std::getenv("SLCS_FUSED_NB");
+      return (e && std::atoi(e) == 128) ? 128 : 64;
+    }();
     bool done = false;
-    switch (k_out) {
-      case 1: done = reach_fused_try<1>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 2: done = reach_fused_try<2>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 3: done = reach_fused_try<3>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 4: done = reach_fused_try<4>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+    switch (k_out * 1000 + nb) {
+      case 1064: done = reach_fused_try<1, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 2064: done = reach_fused_try<2, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 3064: done = reach_fused_try<3, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 4064: done = reach_fused_try<4, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 1128: done = reach_fused_try<1, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 2128: done = reach_fused_try<2, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 3128: done = reach_fused_try<3, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+      case 4128: done = reach_fused_try<4, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
       default: break;
     }
     if (done) return 1;
