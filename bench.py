@@ -128,6 +128,26 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
+def profiled_traffic(kernel_prefix):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of a
+    kernel from the newest committed ncu summary under profiles/ (cold-cache,
+    serialised ncu replay), with the file it came from; (None, None) if absent."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json")),
+                   key=os.path.getmtime, reverse=True)
+    for f in files:
+        try:
+            with open(f) as fh:
+                d = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        for per_csv in d.values():
+            for name, row in per_csv.items():
+                if name.split("::")[-1].startswith(kernel_prefix) and row.get("dram_bytes_per_launch"):
+                    return row["dram_bytes_per_launch"], os.path.relpath(f, ROOT) + " [" + name + "]"
+    return None, None
+
+
 def cpu_reference_sample(size, seed, ref_depth, steps=1):
     """The reference's own executor (oracle/_ref) on a bounded chain sample;
     falls back to the C restatement when oracle/_ref is absent."""
@@ -719,11 +739,14 @@ def main():
     t_near = statistics.mean(a.elapsed_time(z) for a, z in ev_n) / 1e3
     reach_share = 500 * t_reach / (ms_per_step / 1e3) if depth == 1000 else None
     achieved = BYTES_PER_PX["reach"] * px / t_reach / 1e9
+    traffic, traffic_src = profiled_traffic("k_reach_fused<1")
     roofline = {
-        "bound": "hbm", "kernel": "reach (union-find primitive: tile-local UF, border merge, "
-                                  "flag propagate, select, near)",
+        "bound": "hbm", "kernel": "reach = k_reach_fused<1,64> (one cooperative launch: tile-local "
+                                  "run union-find, border unions, flag propagation, select, "
+                                  "closing near)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)",
+        "traffic": traffic, "traffic_source": traffic_src,
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)",
         "algorithmic_bytes_per_px": BYTES_PER_PX["reach"], "px_per_launch": px,
         "reach_ms": t_reach * 1e3, "near_ms": t_near * 1e3,
         "near_achieved_gbs": BYTES_PER_PX["near"] * px / t_near / 1e9,
