@@ -1087,33 +1087,39 @@ int small_launch(const uint32_t* u, const uint32_t* t, uint32_t* out, const G& g
 }
 
 // ===========================================================================
-// Fused single-launch reach for images whose 256x256-px tiles are all
-// co-resident (<= 2 CTAs per SM, e.g. 4096^2 = 256 tiles on 148 SMs):
-// one cooperative launch with four grid barriers instead of five kernels.
-//   A  tile-local run union-find in shared memory (as k_tile_local); per local
-//      root a record {seeded, touches the tile ring, compact index}; ring
-//      roots get compact ids c = tile * 512 + idx (<= 508 ring roots per tile)
-//      and a node hnode(c) in a small global union-find GP (+ seed flag GF);
-//      runs that touch the ring publish P[key block] = their root's node
-//   B  each tile unites its own top and left borders on GP (atomicMax links)
-//   C  each tile flattens its ring roots (GP[c] = global root) and moves its
-//      seed flags to the global roots
-//   D  select: a run is kept if its (local or global) root is seeded; S | t
-//      goes to `sel` (global, L2-resident)
-//   E  the closing near^KOUT of sel for the tile's own words
+// Fused single-launch reach for images whose tiles are all co-resident
+// (NB bands x 256 px per CTA, e.g. 4096^2 = 512 tiles of 128x256 px on 148
+// SMs): one cooperative launch with three grid barriers instead of five
+// kernels.
+//   A  the tile's target words (+ a 1-word/1-row halo) are staged in shared
+//      memory and near(t) is taken from there; tile-local run union-find; per
+//      local root a record {seeded, touches the ring, compact index}.  Ring
+//      roots get compact ids c = tile * 512 + idx (<= 508 per tile) and a
+//      node in a small global union-find GP; a seeded ring root starts out
+//      under the virtual root SEED (the largest node value), so "seeded" is
+//      simply "its root is SEED".  Runs that touch the ring publish
+//      P[key block] = c.
+//   B  each tile unites its own left and top borders on GP (atomicMax links).
+//   C  (no barrier) each tile resolves its ring roots (root == SEED?) into
+//      the records, then selects S | t per word from shared memory; the words
+//      go to `sel` (global, for the neighbours' halos) and to shared memory.
+//   D  the closing near^KOUT of the tile from shared memory, halo words of
+//      the neighbouring tiles read from `sel`.
 // Data written during the launch by other CTAs is read with ld.global.cg.
 constexpr uint32_t REC_SEED = 1u << 31, REC_RING = 1u << 30, REC_ROOT = 1u << 29, REC_IDX = 511u;
+constexpr uint32_t SEED = 0xffffffffu;  // no compact id hashes to it (ids < 2^31)
 constexpr int FT_LIST = 512;
 // per-tile words of the `lists` scratch region: LT_LIST for the multi-kernel
-// path, or GP (512 u32) + GF (512 B) per fused tile
-// (fused tiles may be half as tall: two per multi-kernel tile)
+// path, or GP (512 u32) per fused tile (fused tiles may be half as tall: two per
+// multi-kernel tile)
 constexpr int FT_WORDS = 1280;
-static_assert(FT_WORDS >= LT_LIST && FT_WORDS * 4 >= 2 * FT_LIST * 5, "lists region too small");
+static_assert(FT_WORDS >= LT_LIST && FT_WORDS >= 2 * FT_LIST, "lists region too small");
 
 __device__ __forceinline__ uint32_t cfind(uint32_t* GP, uint32_t v) {
   for (;;) {
+    if (v == SEED) return v;
     const uint32_t p = __ldcg(GP + hkey(v));
-    if (p == v) return v;
+    if (p == v || p == SEED) return p;
     const uint32_t gp = __ldcg(GP + hkey(p));
     if (gp == p) return p;
     __stcg(GP + hkey(v), gp);
@@ -1131,18 +1137,18 @@ __device__ void cunite(uint32_t* GP, uint32_t a, uint32_t b) {
       a = b;
       b = t;
     }
-    const uint32_t old = atomicMax(GP + hkey(b), a);
+    const uint32_t old = atomicMax(GP + hkey(b), a);  // b != SEED: SEED is the largest
     if (old == b) return;
     b = old;
   }
 }
 
-// node of the ring run m of word j in band k (published by its tile in phase A)
+// compact node of the ring run m of word j in band k (published in phase A)
 __device__ __forceinline__ uint32_t cnode(const uint32_t* P, const G& g, int k, int j, uint32_t T,
                                           uint32_t B, uint32_t m) {
   int dr, col;
   run_max(T, B, m, dr, col);
-  return __ldcg(P + kblk(g, gkey(g, 2 * k + dr, 32 * j + col)));
+  return hnode(__ldcg(P + kblk(g, gkey(g, 2 * k + dr, 32 * j + col))));
 }
 
 __device__ __forceinline__ void cunite_dedup(uint32_t* GP, uint32_t a, uint32_t b, bool active) {
@@ -1156,18 +1162,25 @@ __device__ __forceinline__ void cunite_dedup(uint32_t* GP, uint32_t a, uint32_t 
   cunite(GP, a, b);
 }
 
-// near^K word (r, j) of a bit image written during this launch (L2 reads)
+// word (r, j) of a bit image or 0 outside the image (halo staging)
+__device__ __forceinline__ uint32_t word_or0(const uint32_t* img, const G& g, int r, int j,
+                                             bool coherent) {
+  if (r < 0 || r >= g.H || j < 0 || j >= g.wpr) return 0u;
+  const uint32_t* p = img + size_t(r) * g.pitch + j;
+  return coherent ? __ldcg(p) : __ldg(p);
+}
+
+// near^K of the word at (row sr, column sc) of a shared-memory window of
+// 10-word rows (columns j0-1 .. j0+8), rows r0 .. r1 of the window valid
 template <int K>
-__device__ __forceinline__ uint32_t near_word_cg(const uint32_t* s, const G& g, int r, int j) {
+__device__ __forceinline__ uint32_t near_smem(const uint32_t* win, int sr, int sc, int r0, int r1) {
   uint32_t acc = 0;
 #pragma unroll
   for (int d = -K; d <= K; ++d) {
-    const int rr = r + d;
-    if (rr < 0 || rr >= g.H) continue;
-    const uint32_t* row = s + size_t(rr) * g.pitch;
-    const uint32_t C = __ldcg(row + j);
-    const uint32_t L = j > 0 ? __ldcg(row + j - 1) : 0u;
-    const uint32_t R = j + 1 < g.wpr ? __ldcg(row + j + 1) : 0u;
+    const int rr = sr + d;
+    if (rr < r0 || rr > r1) continue;
+    const uint32_t* row = win + rr * 10;
+    const uint32_t C = row[sc], L = row[sc - 1], R = row[sc + 1];
     acc |= C;
 #pragma unroll
     for (int e = 1; e <= K; ++e) acc |= __funnelshift_l(L, C, e) | __funnelshift_r(C, R, e);
@@ -1179,7 +1192,7 @@ template <int KOUT, int NB>
 __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(const uint32_t* __restrict__ ubits,
                                                                const uint32_t* __restrict__ tbits,
                                                                uint32_t* P, uint32_t* GP,
-                                                               uint8_t* GF, uint32_t* sel,
+                                                               uint32_t* sel,
                                                                uint32_t* __restrict__ out, G g,
                                                                long long* tstamp) {
   cg::grid_group grid = cg::this_grid();
@@ -1200,9 +1213,13 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();
   extern __shared__ __align__(16) unsigned char lsm[];
   constexpr int UNITS = NB * LTWW, SLOTS = NB * (1 << (LKW - 1));
+  constexpr int TROWS = 2 * NB + 2, SROWS = 2 * NB + 2 * KOUT;
   uint32_t* par = reinterpret_cast<uint32_t*>(lsm);  // SLOTS: union-find, then records
   uint32_t* sT = par + SLOTS;                         // UNITS
   uint32_t* sB = sT + UNITS;                          // UNITS
+  uint32_t* tw = sB + UNITS;                          // TROWS x 10: target + halo
+  uint32_t* sw = tw + TROWS * 10;                     // SROWS x 10: selection + halo
+  uint16_t* ring = reinterpret_cast<uint16_t*>(sw + SROWS * 10);  // FT_LIST: idx -> root slot
   __shared__ int s_cnt;
   using T = RunTile<LKW>;
   const int slice = blockIdx.z;
@@ -1213,27 +1230,35 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   const int u0 = threadIdx.x;
   const int band = u0 / LTWW, w = u0 % LTWW;
   const int kb = blockIdx.y * NB + band;
-  const int j = blockIdx.x * LTWW + w;
+  const int j0 = blockIdx.x * LTWW, j = j0 + w;
+  const int R0 = blockIdx.y * NB * 2;  // first row of the tile
   const int r = 2 * kb;
   const bool in = kb < g.BH && j < g.wpr;
   const bool two = r + 1 < g.H;
   const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
   const uint32_t Bw = (in && two) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
-  uint32_t seedT = 0, seedB = 0;
-  if (Tw | Bw) {
-    seedT = Tw & near_word(t, g, r, j);
-    seedB = two ? Bw & near_word(t, g, r + 1, j) : 0u;
+  // target window: rows R0-1 .. R0+2NB, columns j0-1 .. j0+8 (halo by threads < 20+4NB)
+  tw[(r - R0 + 1) * 10 + w + 1] = word_or0(t, g, r, j, false);
+  tw[(r - R0 + 2) * 10 + w + 1] = word_or0(t, g, r + 1, j, false);
+  if (u0 < 20) {
+    const int hr = u0 < 10 ? R0 - 1 : R0 + 2 * NB, hc = u0 % 10;
+    tw[(hr - R0 + 1) * 10 + hc] = word_or0(t, g, hr, j0 - 1 + hc, false);
+  } else if (u0 < 20 + 4 * NB) {
+    const int q = u0 - 20, side = q / (2 * NB), hr = R0 + q % (2 * NB);
+    tw[(hr - R0 + 1) * 10 + (side ? 9 : 0)] = word_or0(t, g, hr, side ? j0 + 8 : j0 - 1, false);
   }
   sT[u0] = Tw;
   sB[u0] = Bw;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
+  const uint32_t seedT = Tw & near_smem<1>(tw, r - R0 + 1, w + 1, 0, TROWS - 1);
+  const uint32_t seedB = Bw & near_smem<1>(tw, r - R0 + 2, w + 1, 0, TROWS - 1);
   stamp();  // 1: loads
   T tile{par, sT, sB};
   tile.link(u0, Tw, Bw);
   stamp();  // 2: link
-  // flatten in place: a run's slot holds its root key, a root's slot holds its
-  // record (REC_ROOT set) -- no per-run root registers stay live afterwards
+  // flatten in place: a run's slot holds its root's slot, a root's slot holds
+  // its record (REC_ROOT set) -- no per-run root registers stay live afterwards
   {
     uint32_t rt[16];
     tile.roots(u0, Tw, Bw, rt);
@@ -1257,7 +1282,7 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
 
   // ---- A: per-root records, compact ids of ring roots, ring runs -> P
   const uint32_t tile_id = (uint32_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  const int R0 = blockIdx.y * NB * 2, C0 = blockIdx.x * LTWW * 32;
+  const int C0 = j0 * 32;
   const uint32_t lmask = (1u << LKW) - 1u;
   auto ring_run = [&](uint32_t m) {
     return band == 0 || band == NB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31));
@@ -1277,9 +1302,9 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
     if ((rec & REC_ROOT) && (rec & REC_RING)) {
       const uint32_t idx = uint32_t(atomicAdd(&s_cnt, 1));
       par[T::slot(k)] = rec | idx;
+      ring[idx] = uint16_t(T::slot(k));
       const uint32_t c = tile_id * FT_LIST + idx;
-      __stcg(GP + c, hnode(c));
-      __stcg(GF + c, uint8_t((rec & REC_SEED) ? 1 : 0));
+      __stcg(GP + c, (rec & REC_SEED) ? SEED : hnode(c));
     }
   }
   __syncthreads();
@@ -1289,18 +1314,18 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
     if (ring_run(m)) {
       const uint32_t k = T::key(band, w, Tw, Bw, m);
       const uint32_t c = tile_id * FT_LIST + (par[root_of(k)] & REC_IDX);
-      __stcg(Ps + kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask))), hnode(c));
+      __stcg(Ps + kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask))), c);
     }
   }
   stamp();  // 4: records + publish
   grid.sync();
   stamp();  // 5: barrier
 
-  // ---- B: unions across this tile's left border (threads 0..127) and top
-  // border (threads 128..135)
+  // ---- B: unions across this tile's left border (threads 0..NB-1) and top
+  // border (threads NB..NB+7)
   if (u0 < NB) {
     const int k = blockIdx.y * NB + u0;
-    const int jr = blockIdx.x * LTWW, jl = jr - 1;
+    const int jr = j0, jl = jr - 1;
     if (blockIdx.x > 0 && k < g.BH) {
       uint32_t Tl, Bl, Tr, Br;
       load_unit(u, g, k, jl, Tl, Bl);
@@ -1324,7 +1349,7 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
     }
   } else if (u0 < NB + LTWW) {
     const int k = blockIdx.y * NB;
-    const int jj = blockIdx.x * LTWW + (u0 - NB);
+    const int jj = j0 + (u0 - NB);
     if (blockIdx.y > 0 && jj < g.wpr) {
       uint32_t T0, B0, Tu, Bu;
       load_unit(u, g, k, jj, T0, B0);
@@ -1353,59 +1378,60 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   grid.sync();
   stamp();  // 7: barrier
 
-  // ---- C: flatten this tile's ring roots, move seed flags to global roots
+  // ---- C: resolve this tile's ring roots (read-only finds), then select
   if (u0 < s_cnt) {
-    const uint32_t c = tile_id * FT_LIST + uint32_t(u0);
-    const uint32_t v = hnode(c);
-    uint32_t R = __ldcg(GP + c);
-    while (true) {
-      const uint32_t q = __ldcg(GP + hkey(R));
-      if (q == R) break;
-      R = q;
+    uint32_t v = hnode(tile_id * FT_LIST + uint32_t(u0));
+    while (v != SEED) {
+      const uint32_t q = __ldcg(GP + hkey(v));
+      if (q == v) break;
+      v = q;
     }
-    if (R != v) {
-      __stcg(GP + c, R);
-      if (__ldcg(GF + c)) __stcg(GF + hkey(R), uint8_t(1));
-    }
+    if (v == SEED) par[ring[u0]] |= REC_SEED;
   }
-  stamp();  // 8: flatten
-  grid.sync();
-  stamp();  // 9: barrier
-
-  // ---- D: select (S | t) into sel
+  __syncthreads();
+  stamp();  // 8: resolve
   {
     uint32_t ST = 0, SB = 0;
     for (uint32_t x = Tw | Bw; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
-      const uint32_t rec = par[root_of(T::key(band, w, Tw, Bw, m))];
-      bool seeded = rec & REC_SEED;
-      if (rec & REC_RING) {
-        const uint32_t R = __ldcg(GP + tile_id * FT_LIST + (rec & REC_IDX));
-        seeded = __ldcg(GF + hkey(R)) != 0;
-      }
-      if (seeded) {
+      if (par[root_of(T::key(band, w, Tw, Bw, m))] & REC_SEED) {
         ST |= Tw & m;
         SB |= Bw & m;
       }
     }
+    ST |= tw[(r - R0 + 1) * 10 + w + 1];
+    SB |= tw[(r - R0 + 2) * 10 + w + 1];
+    sw[(r - R0 + KOUT) * 10 + w + 1] = ST;
+    sw[(r - R0 + KOUT + 1) * 10 + w + 1] = SB;
     if (in) {
-      __stcg(ss + size_t(r) * g.pitch + j, ST | __ldg(t + size_t(r) * g.pitch + j));
-      if (two) __stcg(ss + size_t(r + 1) * g.pitch + j, SB | __ldg(t + size_t(r + 1) * g.pitch + j));
+      __stcg(ss + size_t(r) * g.pitch + j, ST);
+      if (two) __stcg(ss + size_t(r + 1) * g.pitch + j, SB);
     }
   }
-  stamp();  // 10: select
+  stamp();  // 9: select
   grid.sync();
-  stamp();  // 11: barrier
+  stamp();  // 10: barrier
 
-  // ---- E: closing near^KOUT of the tile's own words; padding words -> 0
+  // ---- D: closing near^KOUT; halo from the neighbours' selections
+  if (u0 < 20 * KOUT) {
+    const int q = u0 % (10 * KOUT), hr = u0 < 10 * KOUT ? R0 - KOUT + q / 10 : R0 + 2 * NB + q / 10;
+    sw[(hr - R0 + KOUT) * 10 + q % 10] = word_or0(ss, g, hr, j0 - 1 + q % 10, true);
+  } else if (u0 < 20 * KOUT + 4 * NB) {
+    const int q = u0 - 20 * KOUT, side = q / (2 * NB), hr = R0 + q % (2 * NB);
+    sw[(hr - R0 + KOUT) * 10 + (side ? 9 : 0)] = word_or0(ss, g, hr, side ? j0 + 8 : j0 - 1, true);
+  }
+  __syncthreads();
   if (kb < g.BH && j < int(g.pitch)) {
     uint32_t* o = out + size_t(slice) * g.slice;
     const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
-    o[size_t(r) * g.pitch + j] = j < g.wpr ? near_word_cg<KOUT>(ss, g, r, j) & vm : 0u;
-    if (two) o[size_t(r + 1) * g.pitch + j] = j < g.wpr ? near_word_cg<KOUT>(ss, g, r + 1, j) & vm : 0u;
+    o[size_t(r) * g.pitch + j] =
+        j < g.wpr ? near_smem<KOUT>(sw, r - R0 + KOUT, w + 1, 0, SROWS - 1) & vm : 0u;
+    if (two)
+      o[size_t(r + 1) * g.pitch + j] =
+          j < g.wpr ? near_smem<KOUT>(sw, r - R0 + KOUT + 1, w + 1, 0, SROWS - 1) & vm : 0u;
   }
-  stamp();  // 12: near
+  stamp();  // 11: near
 }
 
 int grid_blocks(size_t n, int threads) {
@@ -1602,7 +1628,8 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
                      uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st) {
   static int capacity = -1;  // co-resident CTAs on this device
   constexpr int THREADS = NB * LTWW;
-  const size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4;
+  const size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4 +
+                      size_t(2 * NB + 2) * 40 + size_t(2 * NB + 2 * KOUT) * 40 + FT_LIST * 2;
   if (capacity < 0) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
@@ -1620,7 +1647,6 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   const size_t tiles = size_t(grid.x) * grid.y * grid.z;
   if (tiles > size_t(capacity)) return false;
   uint32_t* GP = s.lists;
-  uint8_t* GF = reinterpret_cast<uint8_t*>(s.lists + tiles * FT_LIST);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
@@ -1637,7 +1663,7 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   }();
   long long* ts = nullptr;
   if (timing) cuda_check(cudaMalloc(&ts, tiles * 16 * sizeof(long long)), "timing buffer");
-  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT, NB>, through, target, s.parent, GP, GF,
+  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT, NB>, through, target, s.parent, GP,
                                 tmp_bits, out, g, ts),
              "fused reach launch");
   if (timing) {  // diagnostics only: timeline of phase ends, min/max over CTAs (us)
@@ -1647,11 +1673,11 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
                "timing copy");
     cudaFree(ts);
     const char* names[] = {"start", "load", "link", "roots", "records", "bar1", "merge", "bar2",
-                           "flatten", "bar3", "select", "bar4", "near"};
+                           "resolve", "select", "bar3", "near"};
     long long t0 = h[0];
     for (size_t t = 0; t < tiles; ++t) t0 = h[t * 16] < t0 ? h[t * 16] : t0;
     std::fprintf(stderr, "[fused reach %zu tiles, us since first CTA: min/max]", tiles);
-    for (int ph = 0; ph <= 12; ++ph) {
+    for (int ph = 0; ph <= 11; ++ph) {
       long long mn = h[ph], mx = h[ph];
       for (size_t t = 0; t < tiles; ++t) {
         mn = h[t * 16 + ph] < mn ? h[t * 16 + ph] : mn;
