@@ -324,14 +324,21 @@ struct RunTile {
       par[slot(k)] = node(k);
     }
     __syncthreads();
+    // row links first (disjoint chains along each band), then the band above
+    {
+      const uint32_t c = T | B;
+      if ((c >> 31) && w + 1 < TWW) {
+        const uint32_t T2 = sT[u + 1], B2 = sB[u + 1];
+        if ((T2 | B2) & 1u)
+          unite(node(key(band, w, T, B, run_at(c, 31))),
+                node(key(band, w + 1, T2, B2, first_run(T2 | B2))));
+      }
+    }
+    __syncthreads();
     for (uint32_t x = T | B; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
       const uint32_t k = node(key(band, w, T, B, m));
-      if ((m >> 31) && w + 1 < TWW) {
-        const uint32_t T2 = sT[u + 1], B2 = sB[u + 1];
-        if ((T2 | B2) & 1u) unite(k, node(key(band, w + 1, T2, B2, first_run(T2 | B2))));
-      }
       const uint32_t td = T & m;
       if (band > 0 && td) {
         const int uu = u - TWW;
