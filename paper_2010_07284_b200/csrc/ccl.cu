@@ -249,10 +249,18 @@ struct RunTile {
   // O(log n) deep, and atomicMax linking lets concurrent unions on one root
   // all make progress.  Roots are therefore arbitrary representatives; the
   // canonical max key is recovered separately where labels need it.
-  __device__ __forceinline__ static uint32_t node(uint32_t k) {
-    uint32_t x = (k * 0x9E37u) & 0xffffu;
+  __device__ __forceinline__ static uint32_t snode(uint32_t sl) {
+    uint32_t x = (sl * 0x9E37u) & 0xffffu;
     x ^= x >> 7;
-    return (x << 16) | uint32_t(slot(k));
+    return (x << 16) | sl;
+  }
+  __device__ __forceinline__ static uint32_t node(uint32_t k) { return snode(uint32_t(slot(k))); }
+  // node of run m of word w in `band` without composing the key
+  __device__ __forceinline__ static uint32_t rnode(int band, int w, uint32_t T, uint32_t B,
+                                                  uint32_t m) {
+    const uint32_t bm = B & m;
+    const int col = 31 - __clz(bm ? bm : (T & m));
+    return snode((uint32_t(band) << BL) | (uint32_t(32 * w + col) >> 1));
   }
   __device__ __forceinline__ static int nslot(uint32_t v) { return int(v & 0xffffu); }
   // a representative key of a slot's 2x2 block (top-left pixel)
@@ -270,18 +278,19 @@ struct RunTile {
       v = gp;
     }
   }
-  __device__ __forceinline__ void unite(uint32_t a, uint32_t b) const {
+  // returns a node of the merged set (the winning root at link time)
+  __device__ __forceinline__ uint32_t unite(uint32_t a, uint32_t b) const {
     for (;;) {
       a = find(a);
       b = find(b);
-      if (a == b) return;
+      if (a == b) return a;
       if (a < b) {
         const uint32_t t = a;
         a = b;
         b = t;
       }
       const uint32_t old = atomicMax(par + nslot(b), a);
-      if (old == b) return;
+      if (old == b) return a;
       b = old;
     }
   }
@@ -320,8 +329,8 @@ struct RunTile {
     for (uint32_t x = T | B; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
-      const uint32_t k = key(band, w, T, B, m);
-      par[slot(k)] = node(k);
+      const uint32_t v = rnode(band, w, T, B, m);
+      par[nslot(v)] = v;
     }
     __syncthreads();
     // row links first (disjoint chains along each band), then the band above
@@ -330,33 +339,35 @@ struct RunTile {
       if ((c >> 31) && w + 1 < TWW) {
         const uint32_t T2 = sT[u + 1], B2 = sB[u + 1];
         if ((T2 | B2) & 1u)
-          unite(node(key(band, w, T, B, run_at(c, 31))),
-                node(key(band, w + 1, T2, B2, first_run(T2 | B2))));
+          unite(rnode(band, w, T, B, run_at(c, 31)),
+                rnode(band, w + 1, T2, B2, first_run(T2 | B2)));
       }
     }
     __syncthreads();
-    for (uint32_t x = T | B; x;) {
-      const uint32_t m = first_run(x);
-      x &= ~m;
-      const uint32_t k = node(key(band, w, T, B, m));
-      const uint32_t td = T & m;
-      if (band > 0 && td) {
-        const int uu = u - TWW;
-        const uint32_t Tu = sT[uu], Bu = sB[uu], cu = Tu | Bu;
-        for (uint32_t a = dil1(td) & Bu; a;) {
-          const uint32_t mu = run_at(cu, __ffs(a) - 1);
-          a &= ~mu;
-          unite(k, node(key(band - 1, w, Tu, Bu, mu)));
+    if (band > 0 && T) {
+      const int uu = u - TWW;
+      const uint32_t Tu = sT[uu], Bu = sB[uu], cu = Tu | Bu;
+      for (uint32_t x = T | B; x;) {
+        const uint32_t m = first_run(x);
+        x &= ~m;
+        const uint32_t td = T & m;
+        if (!td) continue;
+        // a: the last known root of this run (saves re-finding from the run)
+        uint32_t a = rnode(band, w, T, B, m);
+        for (uint32_t ov = dil1(td) & Bu; ov;) {
+          const uint32_t mu = run_at(cu, __ffs(ov) - 1);
+          ov &= ~mu;
+          a = unite(a, rnode(band - 1, w, Tu, Bu, mu));
         }
         // a diagonal link is redundant when the pixel straight above is set:
         // that pixel's run is linked both ways already (vertical + row link)
         if ((td & 1u) && w > 0 && !(Bu & 1u)) {
           const uint32_t Tl = sT[uu - 1], Bl = sB[uu - 1];
-          if (Bl >> 31) unite(k, node(key(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31))));
+          if (Bl >> 31) a = unite(a, rnode(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31)));
         }
         if ((td >> 31) && w + 1 < TWW && !(Bu >> 31)) {
           const uint32_t Tr = sT[uu + 1], Br = sB[uu + 1];
-          if (Br & 1u) unite(k, node(key(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0))));
+          if (Br & 1u) a = unite(a, rnode(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0)));
         }
       }
     }
@@ -376,7 +387,7 @@ struct RunTile {
       if (!x) break;
       const uint32_t m = first_run(x);
       x &= ~m;
-      r[i] = find(node(key(band, w, T, B, m)));
+      r[i] = find(rnode(band, w, T, B, m));
     }
   }
 };
