@@ -801,58 +801,84 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
   return lab;
 }
 
-// labels: per word, each run's pixels get linear(global root) + 1
-__global__ void k_tile_labels(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
-                              const uint32_t* __restrict__ MKall, uint32_t* __restrict__ L, G g) {
+// labels: each run's pixels get linear(component max key) + 1.  A warp owns 32
+// consecutive words of one band: lanes resolve their runs' labels into a
+// per-warp shared table (stride 17, conflict-free), then the warp writes each
+// output row cooperatively -- lane l stores pixels 4l..4l+3 of every 128-px
+// stretch, so each warp store is 512 contiguous bytes (the label image is the
+// 4 B/px bulk of the CCL traffic).
+constexpr int TL_WARPS = 8;
+__global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* __restrict__ ubits,
+                                                             const uint32_t* __restrict__ P,
+                                                             const uint32_t* __restrict__ MKall,
+                                                             uint32_t* __restrict__ L, G g) {
   slcs_pdl_wait();
+  __shared__ uint32_t tab[TL_WARPS][32 * 17];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t* MK = MKall + size_t(slice) * g.sb;
   uint32_t* Ls = L + size_t(slice) * size_t(g.W) * size_t(g.H);
-  const uint32_t n = uint32_t(g.BH) * uint32_t(g.wpr);
+  uint32_t* tb = tab[wib];
+  const int groups = (g.wpr + 31) / 32;
+  const size_t nw = size_t(g.BH) * size_t(groups);
   const bool vec = (g.W & 3) == 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int k = int(i / uint32_t(g.wpr)), j = int(i - uint32_t(k) * uint32_t(g.wpr));
-    const size_t row = size_t(2 * k) * g.pitch + j;
+  for (size_t wg = size_t(blockIdx.x) * TL_WARPS + wib; wg < nw; wg += size_t(gridDim.x) * TL_WARPS) {
+    const int k = int(wg / size_t(groups)), gi = int(wg - size_t(k) * groups);
+    const int j = gi * 32 + lane;
     const bool two = 2 * k + 1 < g.H;
-    const uint32_t T = __ldg(u + row), B = two ? __ldg(u + row + g.pitch) : 0u;
-    uint32_t labs[16];
+    uint32_t T = 0, B = 0;
+    if (j < g.wpr) {
+      const size_t row = size_t(2 * k) * g.pitch + j;
+      T = __ldg(u + row);
+      B = two ? __ldg(u + row + g.pitch) : 0u;
+    }
     uint32_t starts = 0;
     {
       uint32_t x = T | B;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        labs[q] = 0;
-        if (x) {
-          const uint32_t m = first_run(x);
-          x &= ~m;
-          starts |= m & (0u - m);
-          labs[q] = linear_label(g, MK[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))]);
-        }
+        if (!x) break;
+        const uint32_t m = first_run(x);
+        x &= ~m;
+        starts |= m & (0u - m);
+        tb[lane * 17 + q] = linear_label(g, MK[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))]);
       }
     }
-    const int c0 = 32 * j;
-    const int ncol = min(32, g.W - c0);
+    __syncwarp();
+    const size_t c0 = size_t(gi) * 1024;
     for (int rr = 0; rr < (two ? 2 : 1); ++rr) {
       const uint32_t bits = rr ? B : T;
       uint32_t* dst = Ls + size_t(2 * k + rr) * g.W + c0;
-      if (vec && ncol == 32) {
+      if (vec) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint32_t v[4];
+        for (int it = 0; it < 8; ++it) {
+          const int wi = it * 4 + (lane >> 3), x0 = (lane & 7) * 4;
+          const uint32_t wb = __shfl_sync(0xffffffffu, bits, wi);
+          const uint32_t ws = __shfl_sync(0xffffffffu, starts, wi);
+          const size_t p = size_t(it) * 128 + size_t(lane) * 4;
+          if (c0 + p < size_t(g.W)) {
+            uint32_t v[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int x = 4 * q + e;
-            v[e] = ((bits >> x) & 1u) ? pick16(labs, __popc(starts & ((2u << x) - 1u)) - 1) : 0u;
+            for (int e = 0; e < 4; ++e) {
+              const int x = x0 + e;
+              v[e] = ((wb >> x) & 1u) ? tb[wi * 17 + __popc(ws & ((2u << x) - 1u)) - 1] : 0u;
+            }
+            *reinterpret_cast<uint4*>(dst + p) = make_uint4(v[0], v[1], v[2], v[3]);
           }
-          reinterpret_cast<uint4*>(dst)[q] = make_uint4(v[0], v[1], v[2], v[3]);
         }
       } else {
-        for (int x = 0; x < ncol; ++x)
-          dst[x] = ((bits >> x) & 1u) ? pick16(labs, __popc(starts & ((2u << x) - 1u)) - 1) : 0u;
+        for (int it = 0; it < 32; ++it) {
+          const uint32_t wb = __shfl_sync(0xffffffffu, bits, it);
+          const uint32_t ws = __shfl_sync(0xffffffffu, starts, it);
+          const size_t p = size_t(it) * 32 + lane;
+          if (c0 + p < size_t(g.W))
+            dst[p] = ((wb >> lane) & 1u) ? tb[it * 17 + __popc(ws & ((2u << lane) - 1u)) - 1] : 0u;
+        }
       }
     }
+    __syncwarp();
   }
 }
 
@@ -1636,8 +1662,10 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   if (ccl_small_path(gb.w, gb.h)) return small_launch<0>(bits, nullptr, labels, g, gb.batch, st);
   int launches = 0;
   large_local_and_merge(bits, nullptr, g, gb.batch, s, MODE_CCL, st, launches);
-  dim3 lg(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
-  pdl(k_tile_labels, lg, 256, 0, st, bits, s.parent, s.size, labels, g);
+  const size_t warps = size_t(g.BH) * size_t((g.wpr + 31) / 32);
+  dim3 lg(unsigned(std::min<size_t>((warps + TL_WARPS - 1) / TL_WARPS, 148 * 16)),
+          unsigned(gb.batch));
+  pdl(k_tile_labels, lg, TL_WARPS * 32, 0, st, bits, s.parent, s.size, labels, g);
   return launches + 1;
 }
 
