@@ -254,3 +254,21 @@ def test_batched_program(dev):
         vI = O.threshold(0, imgs[s], 56360)
         ref = O.logical_or(O.maxvol(O.grow(hI, vI)), O.surrounded(hI, vI))
         assert np.array_equal(got[s], ref), s
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 5])
+def test_reach_closing_radius_absorbs_following_nears(dev, k):
+    # reach followed by k nears: the planner folds them into the reach's closing
+    # near (k_out = k + 1; the fused kernel handles k_out <= 4, larger radii
+    # fall back to a separate stencil) -- every variant must equal the oracle
+    img = O.blob_noise(1200, 900, 11)
+    t = O.threshold(0, img, 62258)
+    b = O.threshold(0, img, 56360)
+    expr = "reach(t, b)"
+    ref = O.reach(t, b)
+    for _ in range(k):
+        expr = f"near({expr})"
+        ref = O.dilate(ref)
+    rep = run_text(f'load t = "t.png"\nload b = "b.png"\nsave "o.png" {expr}\n',
+                   {"t.png": t, "b.png": b})
+    assert np.array_equal(out_of(rep, "o.png"), ref)

@@ -235,3 +235,22 @@ def test_device_random_mask_matches_reference_stream(dev):
         # a band starting mid-image continues the same stream
         band = random_mask_device(w, 7, d, seed, 5, dev).numpy()
         assert np.array_equal(band, full[5:12])
+
+
+def test_volume_async_writes_device_counts(dev):
+    # slcs_volume_async: counts land in device memory in stream order, and the
+    # self-resetting accumulators give the same count on every call
+    import ctypes as C
+
+    import torch
+
+    from paper_2010_07284_b200 import _lib
+    rng = O.Rng(77)
+    a = np.stack([O.random_mask(333, 211, d, rng) for d in (0.1, 0.5, 0.9)])
+    img = DeviceImage.upload(a, PixelKind.Bool, dev)
+    out = torch.zeros(3, dtype=torch.int64, device="cuda:0")
+    lib = _lib.load()
+    for _ in range(3):
+        assert lib.slcs_volume_async(dev.handle, img.handle, C.c_void_p(out.data_ptr())) == 0
+        dev.synchronize()
+        assert out.cpu().tolist() == [int(x.sum()) for x in a]

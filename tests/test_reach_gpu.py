@@ -157,3 +157,13 @@ def test_batched_reach(dev):
                     DeviceImage.upload(u, PixelKind.Bool, dev)).numpy()
         for i in range(3):
             assert np.array_equal(got[i], O.reach(t[i], u[i]))
+
+
+def test_reach_beyond_fused_capacity_uses_tiled_kernels(dev):
+    # 6144 x 4096 = 768 fused tiles (> 2 x 148 x 2 co-resident 512-thread CTAs):
+    # the multi-kernel tiled path; 4096 x 4096 = 512 tiles stays fused
+    for w, h in ((6144, 4096), (4096, 4096)):
+        rng = O.Rng(w + h)
+        t = O.random_mask(w, h, 0.002, rng)
+        u = O.random_mask(w, h, 0.45, rng)
+        assert np.array_equal(reach(B(t), B(u)).data, O.reach(t, u))
