@@ -1672,11 +1672,11 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
 template <int KOUT, int NB>
 bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* out,
                      uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st) {
-  static int capacity = -1;  // co-resident CTAs on this device
   constexpr int THREADS = NB * LTWW;
-  const size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4 +
-                      size_t(2 * NB + 2) * 40 + size_t(2 * NB + 2 * KOUT) * 40 + FT_LIST * 2;
-  if (capacity < 0) {
+  constexpr size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4 +
+                          size_t(2 * NB + 2) * 40 + size_t(2 * NB + 2 * KOUT) * 40 + FT_LIST * 2;
+  // co-resident CTAs on this device (thread-safe one-time initialisation)
+  static const int capacity = [] {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1685,9 +1685,9 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT, NB>, THREADS,
                                                       smem) != cudaSuccess)
       per = 0;
-    capacity = per * sms;
     cudaGetLastError();
-  }
+    return per * sms;
+  }();
   dim3 grid(unsigned((g.wpr + LTWW - 1) / LTWW), unsigned((g.BH + NB - 1) / NB),
             unsigned(batch));
   const size_t tiles = size_t(grid.x) * grid.y * grid.z;
@@ -1763,7 +1763,7 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
   if (fused_reach_enabled()) {
     static const int nb = [] {
       const char* e = std::getenv("SLCS_FUSED_NB");
-      return (e && std::atoi(e) == 128) ? 128 : 64;
+      return (e && std::atoi(e) == 128) ? 128 : 64;  // A/B switch; 32 measured slower
     }();
     bool done = false;
     switch (k_out * 1000 + nb) {
