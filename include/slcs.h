@@ -103,6 +103,19 @@ int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch
 int slcs_image_storage(const slcs_image* img, void** dev, size_t* row_pitch_bytes,
                        size_t* slice_bytes);
 
+/* ---- image ingest / egress (png_io, proj/src/png_io.cpp:30-144) ----------
+ * loadPng: 8/16-bit grey, grey+alpha, RGB or RGBA (Adam7 allowed) -> U16, the
+ * first channel, 8-bit samples widened by v*257; palette images and other bit
+ * depths fail with the reference's messages.  savePng: Bool -> 16-bit grey
+ * (true = 65535), U16 verbatim, labels -> 8-bit RGB (slcs_label_color).
+ * Decoding of the byte stream (zlib) is host work; the per-pixel conversion
+ * runs on the device. */
+int slcs_png_load(slcs_ctx* ctx, const char* path, slcs_image** out);
+int slcs_png_decode(slcs_ctx* ctx, const void* bytes, size_t n, slcs_image** out);
+int slcs_png_save(slcs_ctx* ctx, const slcs_image* img, const char* path);
+/* labelColor (png_io.cpp:75-90): lowbias32 hash of a packed label, null -> black */
+void slcs_label_color(uint32_t packed, uint8_t rgb[3]);
+
 /* ---- primitives: each returns a NEW image (*out, refcount 1) --------------
  * Boolean operands that are U16 are coerced by `p > 0` (boolArg,
  * executor.cpp:43-50).  Label images are rejected. */

@@ -254,6 +254,100 @@ def surrounded(a, b):
     return logical_and(a, logical_not(reach(logical_not(logical_or(a, b)), logical_not(b))))
 
 
+# --- png_io (proj/src/png_io.cpp) -- restated; libpng is absent here ---
+
+def label_color(packed: int) -> tuple[int, int, int]:
+    """labelColor (png_io.cpp:75-90): lowbias32 hash, null -> black, black reserved."""
+    if packed == 0:
+        return 0, 0, 0
+    h = packed & 0xFFFFFFFF
+    h ^= h >> 16
+    h = (h * 0x7FEB352D) & 0xFFFFFFFF
+    h ^= h >> 15
+    h = (h * 0x846CA68B) & 0xFFFFFFFF
+    h ^= h >> 16
+    rgb = ((h >> 16) & 255, (h >> 8) & 255, h & 255)
+    return (rgb[0], rgb[1], 1) if rgb == (0, 0, 0) else rgb
+
+
+def png_first_channel_u16(samples: np.ndarray, depth: int) -> np.ndarray:
+    """loadPng's sample mapping (png_io.cpp:60-72): first channel; 8-bit -> v*257."""
+    ch = samples[..., 0] if samples.ndim == 3 else samples
+    return ch.astype(np.uint16) if depth == 16 else (ch.astype(np.uint16) * 257).astype(np.uint16)
+
+
+_ADAM7 = ((0, 0, 8, 8), (0, 4, 8, 8), (4, 0, 8, 4), (0, 2, 4, 4), (2, 0, 4, 2), (0, 1, 2, 2),
+          (1, 0, 2, 1))
+
+
+def png_encode(samples: np.ndarray, depth: int, color: int, filters=(0,), interlace: bool = False,
+               chunk_split: int = 0) -> bytes:
+    """A plain PNG writer for fixtures (ISO 15948): `samples` (H, W[, C]) of uint8/uint16,
+    row filters cycled from `filters` (0 None .. 4 Paeth), optional Adam7, optional
+    IDAT split every `chunk_split` bytes.  Test infrastructure only."""
+    import struct
+    import zlib
+    a = samples if samples.ndim == 3 else samples[..., None]
+    h, w, ch = a.shape
+    bps = depth // 8
+    if depth == 16:
+        raw = a.astype(">u2").view(np.uint8).reshape(h, w * ch * 2)
+    else:
+        raw = a.astype(np.uint8).reshape(h, w * ch)
+    bpp = ch * bps
+
+    def filt(rows):
+        out, prev, k = bytearray(), None, 0
+        for r in rows:
+            r = r.astype(np.int32)
+            p = np.zeros_like(r) if prev is None else prev
+            ft = filters[k % len(filters)]
+            k += 1
+            a_ = np.concatenate([np.zeros(bpp, np.int32), r[:-bpp]]) if len(r) > bpp else np.zeros_like(r)
+            c_ = np.concatenate([np.zeros(bpp, np.int32), p[:-bpp]]) if len(p) > bpp else np.zeros_like(p)
+            if ft == 0:
+                f = r
+            elif ft == 1:
+                f = r - a_
+            elif ft == 2:
+                f = r - p
+            elif ft == 3:
+                f = r - ((a_ + p) >> 1)
+            else:
+                pp = a_ + p - c_
+                pa, pb, pc = np.abs(pp - a_), np.abs(pp - p), np.abs(pp - c_)
+                pred = np.where((pa <= pb) & (pa <= pc), a_, np.where(pb <= pc, p, c_))
+                f = r - pred
+            out.append(ft)
+            out += (f & 255).astype(np.uint8).tobytes()
+            prev = r
+        return bytes(out)
+
+    if not interlace:
+        data = filt(list(raw))
+    else:
+        data = b""
+        for y0, x0, dy, dx in _ADAM7:
+            sub = a[y0::dy, x0::dx]
+            if sub.size == 0:
+                continue
+            sr = (sub.astype(">u2").view(np.uint8) if depth == 16 else sub.astype(np.uint8))
+            data += filt(list(sr.reshape(sub.shape[0], -1)))
+    z = zlib.compress(data, 6)
+
+    def chunk(t, body):
+        return struct.pack(">I", len(body)) + t + body + struct.pack(">I", zlib.crc32(t + body))
+
+    out = b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", struct.pack(">IIBBBBB", w, h, depth, color, 0,
+                                                                0, 1 if interlace else 0))
+    if chunk_split:
+        for i in range(0, len(z), chunk_split):
+            out += chunk(b"IDAT", z[i:i + chunk_split])
+    else:
+        out += chunk(b"IDAT", z)
+    return out + chunk(b"IEND", b"")
+
+
 # --- the reference itself (oracle/_ref) ---
 
 class Reference:

@@ -8,9 +8,9 @@ are the host layer that turns ImgQL text into a device-resident program.
 """
 from . import _lib  # noqa: F401
 from .pixlog import (CmpOp, Device, DeviceImage, ImageBuffer, PixelKind, RunError,  # noqa: F401
-                     ccl, grow, interior, kernels, kNullLabel, mask, maxvol, packLabel, reach,
-                     surrounded, touch, unpackLabel)
+                     ccl, decodePng, grow, interior, kernels, kNullLabel, labelColor, loadPng,
+                     mask, maxvol, packLabel, reach, savePng, surrounded, touch, unpackLabel)
 
 __all__ = ["CmpOp", "Device", "DeviceImage", "ImageBuffer", "PixelKind", "RunError", "ccl",
-           "grow", "interior", "kernels", "kNullLabel", "mask", "maxvol", "packLabel", "reach",
-           "surrounded", "touch", "unpackLabel"]
+           "decodePng", "grow", "interior", "kernels", "kNullLabel", "labelColor", "loadPng",
+           "mask", "maxvol", "packLabel", "reach", "savePng", "surrounded", "touch", "unpackLabel"]

@@ -52,7 +52,7 @@ def build(verbose: bool = False) -> str:
                 sys.stderr.write(log)
     objs = [o for o, _ in results]
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "shared", "-lcuda",
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "shared", "-lcuda", "-lz",
                "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -52,6 +52,10 @@ _SIGS = {
     "slcs_interior_k": (i32, [vp, vp, i32, pvp]),
     "slcs_volume": (i32, [vp, vp, C.POINTER(i64)]),
     "slcs_volume_async": (i32, [vp, vp, vp]),
+    "slcs_png_load": (i32, [vp, cstr, pvp]),
+    "slcs_png_decode": (i32, [vp, vp, sz, pvp]),
+    "slcs_png_save": (i32, [vp, vp, cstr]),
+    "slcs_label_color": (None, [C.c_uint32, vp]),
     "slcs_ccl": (i32, [vp, vp, pvp]),
     "slcs_reach": (i32, [vp, vp, vp, pvp]),
     "slcs_maxvol": (i32, [vp, vp, pvp]),

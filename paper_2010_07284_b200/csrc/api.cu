@@ -3,6 +3,7 @@
 // texts, and host-in/host-out wrappers with the kernels::/ccl::/reach
 // signatures.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <new>
 
@@ -836,3 +837,81 @@ int slcs_h_reach(slcs_ctx* ctx, const uint8_t* target, const uint8_t* through, i
 }
 
 }  // extern "C"
+
+// ---- png_io (proj/src/png_io.cpp:30-144) ---------------------------------------
+namespace {
+
+slcs_image* png_to_image(slcs_ctx* ctx, const uint8_t* bytes, size_t n) {
+  PngInfo info;
+  const std::vector<uint8_t> raw = png_decode(bytes, n, info);
+  Ref img(new_image(ctx, SLCS_U16, info.w, info.h, 1));
+  void* staging = ctx->alloc(raw.size());
+  cuda_check(cudaMemcpyAsync(staging, raw.data(), raw.size(), cudaMemcpyHostToDevice, ctx->stream),
+             "png upload");
+  ctx->launches += launch_png_to_u16(static_cast<const uint8_t*>(staging), info,
+                                     static_cast<uint16_t*>(img.p->data), img.p->geo, ctx->stream);
+  ctx->release(staging);
+  // `raw` is pageable host memory: the copy must finish before it is freed
+  cuda_check(cudaStreamSynchronize(ctx->stream), "png upload");
+  return img.release();
+}
+
+}  // namespace
+
+int slcs_png_decode(slcs_ctx* ctx, const void* bytes, size_t n, slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out || !bytes) fail(SLCS_ERR_ARG, "null argument");
+    *out = png_to_image(ctx, static_cast<const uint8_t*>(bytes), n);
+  });
+}
+
+int slcs_png_load(slcs_ctx* ctx, const char* path, slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out || !path) fail(SLCS_ERR_ARG, "null argument");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(SLCS_ERR_RUN, std::string("cannot open file for reading: ") + path);
+    std::vector<uint8_t> bytes;
+    uint8_t buf[1 << 16];
+    for (size_t k; (k = std::fread(buf, 1, sizeof buf, f)) > 0;) bytes.insert(bytes.end(), buf, buf + k);
+    std::fclose(f);
+    try {
+      *out = png_to_image(ctx, bytes.data(), bytes.size());
+    } catch (const Error& e) {
+      const std::string m = e.what();
+      if (m.rfind("unsupported PNG", 0) == 0) fail(e.code, m + " (" + path + ")");
+      throw;
+    }
+  });
+}
+
+int slcs_png_save(slcs_ctx* ctx, const slcs_image* img, const char* path) {
+  return guard([&] {
+    LOCKED(ctx);
+    need_img(img);
+    if (!path) fail(SLCS_ERR_ARG, "null path");
+    if (img->geo.batch != 1) fail(SLCS_ERR_SHAPE, "savePng: one image per file (batch must be 1)");
+    const Geo& g = img->geo;
+    const int bytes_px = img->kind == SLCS_LABEL ? 3 : 2;
+    const size_t n = size_t(g.h) * (size_t(g.w) * bytes_px + 1);
+    void* rows = ctx->alloc(n);
+    ctx->launches += launch_png_rows(img->data, img->kind, g, static_cast<uint8_t*>(rows),
+                                     ctx->stream);
+    std::vector<uint8_t> host(n);
+    cuda_check(cudaMemcpyAsync(host.data(), rows, n, cudaMemcpyDeviceToHost, ctx->stream),
+               "png rows");
+    ctx->release(rows);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "png rows");
+    const std::vector<uint8_t> file =
+        png_encode(host.data(), g.w, g.h, img->kind == SLCS_LABEL ? 8 : 16,
+                   img->kind == SLCS_LABEL ? 2 : 0);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(SLCS_ERR_RUN, std::string("cannot open file for writing: ") + path);
+    const size_t wrote = std::fwrite(file.data(), 1, file.size(), f);
+    std::fclose(f);
+    if (wrote != file.size()) fail(SLCS_ERR_RUN, std::string("short write: ") + path);
+  });
+}
+
+void slcs_label_color(uint32_t packed, uint8_t rgb[3]) { png_label_color(packed, rgb); }

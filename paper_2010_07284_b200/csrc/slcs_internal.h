@@ -206,6 +206,19 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
                          uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
                          uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out = 1);
 
+// ---- PNG ingest/egress (png.cu) --------------------------------------------------
+struct PngInfo {
+  int w = 0, h = 0, depth = 8, channels = 1;
+};
+// container + inflate + unfilter (+ Adam7) on the host: raw samples, rows of w*channels
+std::vector<uint8_t> png_decode(const uint8_t* data, size_t n, PngInfo& info);
+// rows: h x (1 + w*channels*depth/8) filtered bytes; color 0 (grey) or 2 (RGB)
+std::vector<uint8_t> png_encode(const uint8_t* rows, int w, int h, int depth, int color);
+int launch_png_to_u16(const uint8_t* raw, const PngInfo& info, uint16_t* out, const Geo& gu,
+                      cudaStream_t st);
+int launch_png_rows(const void* img, int kind, const Geo& g, uint8_t* rows, cudaStream_t st);
+void png_label_color(uint32_t packed, uint8_t rgb[3]);
+
 }  // namespace slcs
 
 // ---- opaque handle definitions -------------------------------------------------

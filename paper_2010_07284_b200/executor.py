@@ -3,13 +3,15 @@
 Mirrors ``executor::run`` (proj/src/executor.cpp:231-282, RunOptions /
 RunReport at executor.hpp:16-50) but evaluates the whole DAG through
 ``slcs_program_*`` (csrc/program.cu): one fused, liveness-planned CUDA graph
-instead of one CPU task per node.  ``load`` reads images supplied by the
-caller (the PNG layer, png_io.cpp, is outside this path); ``save`` keeps the
-result on the device and exposes it by path.
+instead of one CPU task per node.  ``load`` takes images supplied by the
+caller or, with ``RunOptions.baseDir``, reads PNG files (png_io.cpp via
+csrc/png.cu); ``save`` keeps the result on the device, exposes it by path and,
+with ``baseDir``, writes the PNG.
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional, Union
@@ -19,7 +21,7 @@ import numpy as np
 from . import _lib
 from .imgql import TaskGraph, compile_text
 from .pixlog import (_DTYPE, Device, DeviceImage, ImageBuffer, PixelKind, RunError, _check,
-                     pixelKindName)
+                     loadPng, pixelKindName, savePng)
 
 FLAG_GRAPH = 1
 FLAG_NO_FUSION = 2
@@ -37,6 +39,9 @@ class RunOptions:
     fusion: bool = True
     cuda_graph: bool = True
     label_cse: bool = True
+    # RunOptions::baseDir (executor.hpp:16-26): when set, `load` paths not supplied
+    # in `images` are read as PNG from here and every `save` writes its PNG here
+    baseDir: Optional[str] = None
 
 
 @dataclass
@@ -146,6 +151,8 @@ def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) ->
     for name in prog.load_names:
         if name in images:
             prog.bind(name, images[name])
+        elif options.baseDir is not None:
+            prog.bind(name, loadPng(os.path.join(options.baseDir, name), prog.device))
     rep = RunReport(taskCount=graph.node_count())
     t0 = time.perf_counter()
     err: Optional[RunError] = None
@@ -164,6 +171,8 @@ def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) ->
         if t.opcode == "save":
             rep.savedFiles.append(t.payload)
             rep.outputs[t.payload] = v
+            if options.baseDir is not None:
+                savePng(os.path.join(options.baseDir, t.payload), v, prog.device)
         else:
             if isinstance(v, DeviceImage):
                 desc = f"image({v.width}x{v.height},{pixelKindName(v.kind)})"

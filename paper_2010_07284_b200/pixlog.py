@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import threading
 from typing import Optional, Union
 
@@ -449,6 +450,38 @@ def random_mask_device(w: int, h: int, density: float, seed: int, row0: int = 0,
     _check(_lib.load().slcs_random_mask(device.handle, w, h, row0, seed, float(density),
                                         C.byref(out)))
     return DeviceImage(out, device)
+
+
+def loadPng(path: str, device: Optional[Device] = None) -> DeviceImage:
+    """png_io loadPng (proj/src/png_io.cpp:30-73): a U16 device image (first channel,
+    8-bit samples widened by v*257)."""
+    device = device or Device.default()
+    out = C.c_void_p()
+    _check(_lib.load().slcs_png_load(device.handle, os.fsencode(path), C.byref(out)))
+    return DeviceImage(out, device)
+
+
+def decodePng(data: bytes, device: Optional[Device] = None) -> DeviceImage:
+    """loadPng from an in-memory PNG byte stream."""
+    device = device or Device.default()
+    out = C.c_void_p()
+    buf = C.create_string_buffer(data, len(data))
+    _check(_lib.load().slcs_png_decode(device.handle, buf, len(data), C.byref(out)))
+    return DeviceImage(out, device)
+
+
+def savePng(path: str, img: Image, device: Optional[Device] = None) -> None:
+    """png_io savePng (png_io.cpp:95-143): Bool -> 16-bit grey 0/65535, U16 verbatim,
+    labels -> 8-bit RGB via labelColor."""
+    d, _ = _dev(img, device)
+    _check(_lib.load().slcs_png_save(d.device.handle, d.handle, os.fsencode(path)))
+
+
+def labelColor(packed: int) -> tuple[int, int, int]:
+    """labelColor (png_io.cpp:75-90): lowbias32 colour of a packed label, null -> black."""
+    rgb = (C.c_uint8 * 3)()
+    _lib.load().slcs_label_color(packed & 0xFFFFFFFF, rgb)
+    return rgb[0], rgb[1], rgb[2]
 
 
 def mask(pattern: str) -> ImageBuffer:
