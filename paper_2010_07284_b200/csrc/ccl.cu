@@ -396,9 +396,9 @@ struct RunTile {
 // Large-image path: 256x256-px tiles (128 bands x 8 words = 1024 threads).
 constexpr int LKW = 8;
 constexpr int LTWW = 8;
-constexpr int LTNB = 128;
-constexpr int LUNITS = LTNB * LTWW;              // 1024
-constexpr int LSLOTS = LTNB * (1 << (LKW - 1));  // 16384 blocks per tile
+constexpr int LTNB = 64;
+constexpr int LUNITS = LTNB * LTWW;              // 512
+constexpr int LSLOTS = LTNB * (1 << (LKW - 1));  // 8192 blocks per tile
 constexpr int LT_LIST = 520;                     // count + <= 512 ring roots
 constexpr int LT_THREADS = LUNITS;
 
@@ -409,7 +409,7 @@ enum { MODE_CCL = 0, MODE_REACH = 1, MODE_SIZE = 2 };
 // the local roots touching the tile ring -- the only ones a border union can
 // link, hence the only ones root_flatten visits.
 template <int MODE>
-__global__ void __launch_bounds__(LT_THREADS) k_tile_local(const uint32_t* __restrict__ ubits,
+__global__ void __launch_bounds__(LT_THREADS, 2048 / LT_THREADS) k_tile_local(const uint32_t* __restrict__ ubits,
                                                            const uint32_t* __restrict__ tbits,
                                                            uint32_t* __restrict__ P,
                                                            uint8_t* __restrict__ F,
