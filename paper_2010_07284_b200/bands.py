@@ -31,7 +31,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .pixlog import Device, DeviceImage, PixelKind, RunError, _check, kernels
+from .pixlog import Device, DeviceImage, PixelKind, RunError, _check, kernels, reach
 
 
 def band_rows(h: int, world: int, rank: int) -> tuple[int, int]:
@@ -249,16 +249,36 @@ def _extend(cur: DeviceImage, above, below, fill: int):
     return (_vstack(parts) if len(parts) > 1 else cur), off
 
 
+def _rows_bytes(img: DeviceImage, r0: int, n: int) -> np.ndarray:
+    return _rows(img, r0, n).numpy().reshape(n, -1)
+
+
 def near_banded(comm: Comm, band: DeviceImage, k: int = 1, erode: bool = False) -> DeviceImage:
-    """near^k (or interior^k) of the full image, restricted to this band."""
+    """near^k (or interior^k) of the full image, restricted to this band: one exchange
+    of k halo rows with each neighbour, then one fused near^k launch (csrc k_near*).
+    Every branch is taken uniformly by all ranks (each exchange is a collective)."""
     dev, h = band.device, band.height
-    cur = band
-    for _ in range(k):  # one halo row per step keeps the exchange tiny (W bits)
-        above, below = comm.neighbours(_row_bytes(cur, 0), _row_bytes(cur, h - 1))
-        ext, off = _extend(cur, above, below, 1 if erode else 0)
-        ext = kernels.erode(ext, dev) if erode else kernels.dilate(ext, dev)
-        cur = _rows(ext, off, h) if ext.height != h else ext
-    return cur
+    op = kernels.erodeK if erode else kernels.dilateK
+    if comm.world == 1:  # the band is the whole image: no halo
+        return op(band, k, dev)
+    if k > 1 and min(comm.allgather(h)) < k:
+        # some band is thinner than the halo: every rank takes k single steps
+        # (the decision must be uniform -- each step is a collective exchange)
+        cur = band
+        for _ in range(k):
+            cur = near_banded(comm, cur, 1, erode)
+        return cur
+    above, below = comm.neighbours(_rows_bytes(band, 0, k), _rows_bytes(band, h - k, k))
+    parts, off = [], 0
+    if above is not None:
+        parts.append(DeviceImage.upload(above, PixelKind.Bool, dev))
+        off = above.shape[0]
+    parts.append(band)
+    if below is not None:
+        parts.append(DeviceImage.upload(below, PixelKind.Bool, dev))
+    ext = _vstack(parts) if len(parts) > 1 else band
+    out = op(ext, k, dev)
+    return _rows(out, off, h) if out.height != h else out
 
 
 def volume_banded(comm: Comm, band: DeviceImage) -> int:
@@ -269,6 +289,8 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
     """reach(target, through) of the full image, restricted to this band."""
     L = _lib.load()
     dev, w, h = target.device, target.width, target.height
+    if comm.world == 1:  # the band is the whole image
+        return reach(target, through, dev)
     above, below = comm.neighbours(_row_bytes(target, 0), _row_bytes(target, h - 1))
     t_ext, off = _extend(target, above, below, 0)
     zero = np.zeros((1, w), np.uint8)

@@ -47,3 +47,21 @@ def test_banded_reach_blob_giant_component(dev):
         out = LocalGroup(world).run(lambda c, b: reach_banded(c, b[0], b[1]).numpy(),
                                     list(zip(tb, ub)))
         assert np.array_equal(np.concatenate(out), O.reach(t, u))
+
+
+@pytest.mark.parametrize("world,h", [(2, 300), (4, 10), (3, 7)])
+@pytest.mark.parametrize("k", [3, 4])
+def test_banded_near_k_halo_exchange(dev, world, h, k):
+    # k halo rows per neighbour and one fused near^k / interior^k launch; bands
+    # thinner than k (h=10 over 4 bands) fall back to single steps
+    rng = O.Rng(world * 100 + h + k)
+    u = O.random_mask(257, h, 0.3, rng)
+    ub = split(dev, u, world)
+    grp = LocalGroup(world)
+    ref_n, ref_e = u, u
+    for _ in range(k):
+        ref_n, ref_e = O.dilate(ref_n), O.erode(ref_e)
+    got = grp.run(lambda c, b: near_banded(c, b, k).numpy(), ub)
+    assert np.array_equal(np.concatenate(got), ref_n)
+    got = grp.run(lambda c, b: near_banded(c, b, k, erode=True).numpy(), ub)
+    assert np.array_equal(np.concatenate(got), ref_e)
