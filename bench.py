@@ -113,11 +113,27 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+# BENCH_DIST_BACKEND=gloo (test only): run the N>1 code path with several ranks on
+# one GPU (ranks share devices round-robin); the driver's runs use NCCL, one GPU each
+DIST_BACKEND = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if DIST_BACKEND != "nccl":
+        import torch
+        local %= max(1, torch.cuda.device_count())
     return ws, rank, local
+
+
+def init_dist(local):
+    import torch
+    if DIST_BACKEND == "nccl":
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.distributed.init_process_group(DIST_BACKEND)
 
 
 def measured_peak_gbs():
@@ -587,7 +603,7 @@ def main():
         import torch
         torch.cuda.set_device(local)
         if ws > 1:
-            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+            init_dist(local)
         if args.config == "c4":
             c4_config(args, ws, rank, local)
         elif args.config == "c5":
@@ -604,7 +620,7 @@ def main():
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     from paper_2010_07284_b200 import (Device, DeviceImage, PixelKind, kernels, reach)
     from paper_2010_07284_b200 import synth as S
     from paper_2010_07284_b200.executor import Program
