@@ -332,16 +332,26 @@ struct RunTile {
       const uint32_t v = rnode(band, w, T, B, m);
       par[nslot(v)] = v;
     }
-    __syncthreads();
-    // row links first (disjoint chains along each band), then the band above
+    // Row links without union-find: a run crossing word boundaries is one chain
+    // of pieces along the band, and the band's TWW words are TWW consecutive
+    // lanes.  A segmented scan over those lanes hands every continuing piece the
+    // node of the chain's leftmost piece, which it points at directly.
     {
+      static_assert(32 % TWW == 0, "a band's words must share a warp");
       const uint32_t c = T | B;
-      if ((c >> 31) && w + 1 < TWW) {
-        const uint32_t T2 = sT[u + 1], B2 = sB[u + 1];
-        if ((T2 | B2) & 1u)
-          unite(rnode(band, w, T, B, run_at(c, 31)),
-                rnode(band, w + 1, T2, B2, first_run(T2 | B2)));
+      const uint32_t prev_c = __shfl_up_sync(0xffffffffu, c, 1, TWW);
+      const bool cont = w > 0 && (c & 1u) && (prev_c >> 31);
+      const uint32_t first = c ? rnode(band, w, T, B, first_run(c)) : 0u;
+      const uint32_t last = c ? rnode(band, w, T, B, run_at(c, 31 - __clz(c))) : 0u;
+      const bool single = c && first == last;
+      uint32_t rep_first = first, rep_last = last;
+#pragma unroll
+      for (int step = 1; step < TWW; ++step) {
+        const uint32_t left = __shfl_up_sync(0xffffffffu, rep_last, 1, TWW);
+        if (cont) rep_first = left;
+        rep_last = single ? rep_first : last;
       }
+      if (cont) par[nslot(first)] = rep_first;
     }
     __syncthreads();
     if (band > 0 && T) {
