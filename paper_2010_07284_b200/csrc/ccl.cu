@@ -354,6 +354,11 @@ struct RunTile {
       if (cont) par[nslot(first)] = rep_first;
     }
     __syncthreads();
+    // Links to the band above.  Each lane's first (run, upper run) pair is held
+    // back and deduplicated across the warp: inside a blob all 8 words of a band
+    // link the same two row chains, and one union suffices.
+    bool have = false;
+    uint32_t fa = 0, fb = 0;
     if (band > 0 && T) {
       const int uu = u - TWW;
       const uint32_t Tu = sT[uu], Bu = sB[uu], cu = Tu | Bu;
@@ -364,22 +369,43 @@ struct RunTile {
         if (!td) continue;
         // a: the last known root of this run (saves re-finding from the run)
         uint32_t a = rnode(band, w, T, B, m);
+        auto link_to = [&](uint32_t b) {
+          if (!have) {
+            have = true;
+            fa = a;
+            fb = b;
+          } else {
+            a = unite(a, b);
+          }
+        };
         for (uint32_t ov = dil1(td) & Bu; ov;) {
           const uint32_t mu = run_at(cu, __ffs(ov) - 1);
           ov &= ~mu;
-          a = unite(a, rnode(band - 1, w, Tu, Bu, mu));
+          link_to(rnode(band - 1, w, Tu, Bu, mu));
         }
         // a diagonal link is redundant when the pixel straight above is set:
         // that pixel's run is linked both ways already (vertical + row link)
         if ((td & 1u) && w > 0 && !(Bu & 1u)) {
           const uint32_t Tl = sT[uu - 1], Bl = sB[uu - 1];
-          if (Bl >> 31) a = unite(a, rnode(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31)));
+          if (Bl >> 31) link_to(rnode(band - 1, w - 1, Tl, Bl, run_at(Tl | Bl, 31)));
         }
         if ((td >> 31) && w + 1 < TWW && !(Bu >> 31)) {
           const uint32_t Tr = sT[uu + 1], Br = sB[uu + 1];
-          if (Br & 1u) a = unite(a, rnode(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0)));
+          if (Br & 1u) link_to(rnode(band - 1, w + 1, Tr, Br, run_at(Tr | Br, 0)));
         }
       }
+    }
+    {
+      // compare the pair's current parents (row-chain representatives or later
+      // ancestors -- either way the same sets) with the previous lane's; an equal
+      // pair is united by that lane (or, transitively, by an earlier one)
+      const uint32_t pa = have ? par[nslot(fa)] : 0u, pb = have ? par[nslot(fb)] : 0u;
+      const uint32_t lo = pa < pb ? pa : pb, hi = pa < pb ? pb : pa;
+      const int lane = threadIdx.x & 31;
+      const uint32_t plo = __shfl_up_sync(0xffffffffu, lo, 1);
+      const uint32_t phi = __shfl_up_sync(0xffffffffu, hi, 1);
+      const bool phave = __shfl_up_sync(0xffffffffu, have ? 1u : 0u, 1) != 0u;
+      if (have && !(lane > 0 && phave && plo == lo && phi == hi)) unite(fa, fb);
     }
     __syncwarp();
     __syncthreads();
