@@ -1268,7 +1268,10 @@ __device__ __forceinline__ uint32_t near_smem(const uint32_t* win, int sr, int s
   return acc;
 }
 
-template <int KOUT, int NB>
+// TK: the target operand is near^TK(tbits) (nears folded into the reach by the
+// program planner; the window then carries a TK+1 halo).  KOUT = 0 emits the
+// selection S | t itself (no closing near: the consumer folds it as its TK).
+template <int KOUT, int NB, int TK>
 __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(const uint32_t* __restrict__ ubits,
                                                                const uint32_t* __restrict__ tbits,
                                                                uint32_t* P, uint32_t* GP,
@@ -1293,7 +1296,8 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();
   extern __shared__ __align__(16) unsigned char lsm[];
   constexpr int UNITS = NB * LTWW, SLOTS = NB * (1 << (LKW - 1));
-  constexpr int TROWS = 2 * NB + 2, SROWS = 2 * NB + 2 * KOUT;
+  constexpr int TH = TK + 1;  // target window halo rows
+  constexpr int TROWS = 2 * NB + 2 * TH, SROWS = KOUT > 0 ? 2 * NB + 2 * KOUT : 1;
   uint32_t* par = reinterpret_cast<uint32_t*>(lsm);  // SLOTS: union-find, then records
   uint32_t* sT = par + SLOTS;                         // UNITS
   uint32_t* sB = sT + UNITS;                          // UNITS
@@ -1317,22 +1321,59 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   const bool two = r + 1 < g.H;
   const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
   const uint32_t Bw = (in && two) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
-  // target window: rows R0-1 .. R0+2NB, columns j0-1 .. j0+8 (halo by threads < 20+4NB)
-  tw[(r - R0 + 1) * 10 + w + 1] = word_or0(t, g, r, j, false);
-  tw[(r - R0 + 2) * 10 + w + 1] = word_or0(t, g, r + 1, j, false);
-  if (u0 < 20) {
-    const int hr = u0 < 10 ? R0 - 1 : R0 + 2 * NB, hc = u0 % 10;
-    tw[(hr - R0 + 1) * 10 + hc] = word_or0(t, g, hr, j0 - 1 + hc, false);
-  } else if (u0 < 20 + 4 * NB) {
-    const int q = u0 - 20, side = q / (2 * NB), hr = R0 + q % (2 * NB);
-    tw[(hr - R0 + 1) * 10 + (side ? 9 : 0)] = word_or0(t, g, hr, side ? j0 + 8 : j0 - 1, false);
+  // target window: rows R0-TH .. R0+2NB+TH-1, columns j0-1 .. j0+8 (halo words by
+  // threads < 20TH + 4NB).  With TK > 0 the window holds the operand before its
+  // folded nears and tbits may be written by the previous kernel of a chain.
+  tw[(r - R0 + TH) * 10 + w + 1] = word_or0(t, g, r, j, false);
+  tw[(r - R0 + TH + 1) * 10 + w + 1] = word_or0(t, g, r + 1, j, false);
+  if (u0 < 20 * TH) {
+    const int q = u0 % (10 * TH);
+    const int hr = u0 < 10 * TH ? R0 - TH + q / 10 : R0 + 2 * NB + q / 10;
+    tw[(hr - R0 + TH) * 10 + q % 10] = word_or0(t, g, hr, j0 - 1 + q % 10, false);
+  } else if (u0 < 20 * TH + 4 * NB) {
+    const int q = u0 - 20 * TH, side = q / (2 * NB), hr = R0 + q % (2 * NB);
+    tw[(hr - R0 + TH) * 10 + (side ? 9 : 0)] = word_or0(t, g, hr, side ? j0 + 8 : j0 - 1, false);
   }
   sT[u0] = Tw;
   sB[u0] = Bw;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
-  const uint32_t seedT = Tw & near_smem<1>(tw, r - R0 + 1, w + 1, 0, TROWS - 1);
-  const uint32_t seedB = Bw & near_smem<1>(tw, r - R0 + 2, w + 1, 0, TROWS - 1);
+  // the target operand t = near^TK(window) at this unit's two words, and the
+  // seeds through & near(t) = through & near^(TK+1)(window).  The box stencil is
+  // separable: vertical ORs of the (L, C, R) column words first (shared by the
+  // two rows and by both radii), then one horizontal pass per result.
+  uint32_t tT, tB, seedT, seedB;
+  {
+    const int base = r - R0;  // window row of r - TH
+    uint3 rows[2 * TH + 2];
+#pragma unroll
+    for (int i = 0; i < 2 * TH + 2; ++i) {
+      const uint32_t* wr = tw + (base + i) * 10 + w;
+      rows[i] = make_uint3(wr[0], wr[1], wr[2]);
+    }
+    auto orv = [](uint3 a, uint3 b) { return make_uint3(a.x | b.x, a.y | b.y, a.z | b.z); };
+    auto hdil = [](uint3 v, int k) {
+      uint32_t acc = v.y;
+#pragma unroll
+      for (int e = 1; e <= TH; ++e)
+        if (e <= k) acc |= __funnelshift_l(v.x, v.y, e) | __funnelshift_r(v.y, v.z, e);
+      return acc;
+    };
+    // rows[TH] is row r, rows[TH + 1] is row r + 1
+    uint3 inner = rows[TH];  // rows r - TK + 1 .. r + TK (shared core of both rows)
+#pragma unroll
+    for (int d = 1; d < TK; ++d) inner = orv(inner, orv(rows[TH - d], rows[TH + d]));
+    if (TK > 0) inner = orv(inner, rows[TH + TK]);
+    // row r: rows r-TK .. r+TK; row r+1: rows r-TK+1 .. r+TK+1
+    const uint3 vT = TK > 0 ? orv(inner, rows[TH - TK]) : rows[TH];
+    const uint3 vB = TK > 0 ? orv(inner, rows[TH + TK + 1]) : rows[TH + 1];
+    tT = TK > 0 ? hdil(vT, TK) : rows[TH].y;
+    tB = TK > 0 ? hdil(vB, TK) : rows[TH + 1].y;
+    const uint3 sTv = orv(orv(vT, rows[TH - TK - 1]), rows[TH + TK + 1]);
+    const uint3 sBv = orv(orv(vB, rows[TH - TK]), rows[2 * TH + 1]);  // rows r-TK .. r+TK+2
+    seedT = Tw & hdil(sTv, TK + 1);
+    seedB = Bw & hdil(sBv, TK + 1);
+  }
   stamp();  // 1: loads
   T tile{par, sT, sB};
   tile.link(u0, Tw, Bw);
@@ -1480,8 +1521,18 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
         SB |= Bw & m;
       }
     }
-    ST |= tw[(r - R0 + 1) * 10 + w + 1];
-    SB |= tw[(r - R0 + 2) * 10 + w + 1];
+    ST |= tT;
+    SB |= tB;
+    if constexpr (KOUT == 0) {
+      // the selection is the result (its consumer applies the closing near)
+      if (kb < g.BH && j < int(g.pitch)) {
+        uint32_t* o = out + size_t(slice) * g.slice;
+        o[size_t(r) * g.pitch + j] = in ? ST : 0u;
+        if (two) o[size_t(r + 1) * g.pitch + j] = in ? SB : 0u;
+      }
+      stamp();  // 9: select
+      return;
+    }
     sw[(r - R0 + KOUT) * 10 + w + 1] = ST;
     sw[(r - R0 + KOUT + 1) * 10 + w + 1] = SB;
     if (in) {
@@ -1494,6 +1545,7 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();  // 10: barrier
 
   // ---- D: closing near^KOUT; halo from the neighbours' selections
+  constexpr int KO = KOUT > 0 ? KOUT : 1;  // (KOUT == 0 returned above)
   if (u0 < 20 * KOUT) {
     const int q = u0 % (10 * KOUT), hr = u0 < 10 * KOUT ? R0 - KOUT + q / 10 : R0 + 2 * NB + q / 10;
     sw[(hr - R0 + KOUT) * 10 + q % 10] = word_or0(ss, g, hr, j0 - 1 + q % 10, true);
@@ -1506,10 +1558,10 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
     uint32_t* o = out + size_t(slice) * g.slice;
     const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
     o[size_t(r) * g.pitch + j] =
-        j < g.wpr ? near_smem<KOUT>(sw, r - R0 + KOUT, w + 1, 0, SROWS - 1) & vm : 0u;
+        j < g.wpr ? near_smem<KO>(sw, r - R0 + KOUT, w + 1, 0, SROWS - 1) & vm : 0u;
     if (two)
       o[size_t(r + 1) * g.pitch + j] =
-          j < g.wpr ? near_smem<KOUT>(sw, r - R0 + KOUT + 1, w + 1, 0, SROWS - 1) & vm : 0u;
+          j < g.wpr ? near_smem<KO>(sw, r - R0 + KOUT + 1, w + 1, 0, SROWS - 1) & vm : 0u;
   }
   stamp();  // 11: near
 }
@@ -1705,20 +1757,21 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   return launches + 1;
 }
 
-template <int KOUT, int NB>
+template <int KOUT, int NB, int TK>
 bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* out,
                      uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st) {
   constexpr int THREADS = NB * LTWW;
   constexpr size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4 +
-                          size_t(2 * NB + 2) * 40 + size_t(2 * NB + 2 * KOUT) * 40 + FT_LIST * 2;
+                          size_t(2 * NB + 2 * (TK + 1)) * 40 +
+                          size_t(KOUT > 0 ? 2 * NB + 2 * KOUT : 1) * 40 + FT_LIST * 2;
   // co-resident CTAs on this device (thread-safe one-time initialisation)
   static const int capacity = [] {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaFuncSetAttribute(k_reach_fused<KOUT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem)) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT, NB>, THREADS,
+    if (cudaFuncSetAttribute(k_reach_fused<KOUT, NB, TK>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT, NB, TK>, THREADS,
                                                       smem) != cudaSuccess)
       per = 0;
     cudaGetLastError();
@@ -1745,7 +1798,7 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   }();
   long long* ts = nullptr;
   if (timing) cuda_check(cudaMalloc(&ts, tiles * 16 * sizeof(long long)), "timing buffer");
-  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT, NB>, through, target, s.parent, GP,
+  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT, NB, TK>, through, target, s.parent, GP,
                                 tmp_bits, out, g, ts),
              "fused reach launch");
   if (timing) {  // diagnostics only: timeline of phase ends, min/max over CTAs (us)
@@ -1789,12 +1842,15 @@ bool fused_reach_enabled() {
 }
 
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
-                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st, int k_out) {
+                 uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st, int k_out,
+                 int tk) {
   G g = make_g(gb);
   if (ccl_small_path(gb.w, gb.h)) {
-    if (k_out != 1) fail(SLCS_ERR_ARG, "reach: closing radius > 1 needs the tiled path");
+    if (k_out != 1 || tk != 0)
+      fail(SLCS_ERR_ARG, "reach: folded nears need the tiled path");
     return small_launch<1>(through, target, out, g, gb.batch, st);
   }
+  if (k_out < 0 || k_out > 8 || tk < 0 || tk > 8) fail(SLCS_ERR_ARG, "reach: near radius out of range");
   check_key_range(gb, "reach");
   if (fused_reach_enabled()) {
     static const int nb = [] {
@@ -1802,25 +1858,36 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
       return (e && std::atoi(e) == 128) ? 128 : 64;  // A/B switch; 32 measured slower
     }();
     bool done = false;
-    switch (k_out * 1000 + nb) {
-      case 1064: done = reach_fused_try<1, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 2064: done = reach_fused_try<2, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 3064: done = reach_fused_try<3, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 4064: done = reach_fused_try<4, 64>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 1128: done = reach_fused_try<1, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 2128: done = reach_fused_try<2, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 3128: done = reach_fused_try<3, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
-      case 4128: done = reach_fused_try<4, 128>(target, through, out, tmp_bits, g, gb.batch, s, st); break;
+#define SLCS_FUSED(KO, NBV, TKV)                                                                \
+  case (KO) * 10000 + (NBV) * 10 + (TKV):                                                      \
+    done = reach_fused_try<KO, NBV, TKV>(target, through, out, tmp_bits, g, gb.batch, s, st); \
+    break;
+    switch (k_out * 10000 + nb * 10 + tk) {
+      SLCS_FUSED(0, 64, 0) SLCS_FUSED(0, 64, 1) SLCS_FUSED(0, 64, 2)
+      SLCS_FUSED(1, 64, 0) SLCS_FUSED(1, 64, 1) SLCS_FUSED(1, 64, 2)
+      SLCS_FUSED(2, 64, 0) SLCS_FUSED(2, 64, 1) SLCS_FUSED(2, 64, 2)
+      SLCS_FUSED(3, 64, 0) SLCS_FUSED(3, 64, 1) SLCS_FUSED(3, 64, 2)
+      SLCS_FUSED(4, 64, 0) SLCS_FUSED(4, 64, 1) SLCS_FUSED(4, 64, 2)
+      SLCS_FUSED(1, 128, 0) SLCS_FUSED(2, 128, 0)
       default: break;
     }
+#undef SLCS_FUSED
     if (done) return 1;
   }
+  // tiled multi-kernel path.  Folded target nears are applied first (into `out`,
+  // which is free until the end: the select reads and writes each word in place)
   int launches = 0;
-  large_local_and_merge(through, target, g, gb.batch, s, MODE_REACH, st, launches);
+  const uint32_t* tgt = target;
+  if (tk > 0) {
+    launches += launch_near(target, out, gb, tk, false, st);
+    tgt = out;
+  }
+  large_local_and_merge(through, tgt, g, gb.batch, s, MODE_REACH, st, launches);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
-  pdl(k_reach_select, sg, 256, 0, st, through, target, s.parent, s.flag, tmp_bits, g);
+  uint32_t* dst = k_out > 0 ? tmp_bits : out;
+  pdl(k_reach_select, sg, 256, 0, st, through, tgt, s.parent, s.flag, dst, g);
   launches += 1;
-  launches += launch_near(tmp_bits, out, gb, k_out, false, st);
+  if (k_out > 0) launches += launch_near(tmp_bits, out, gb, k_out, false, st);
   return launches;
 }
 

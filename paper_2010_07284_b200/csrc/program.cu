@@ -91,6 +91,7 @@ struct LG {
   std::vector<int> in;  // LG inputs (images)
   int expr = -1;        // LG_EW root expression
   int k = 1;
+  int tk = 0;  // LG_REACH: the target operand is near^tk(in[0]); k = 0 emits the selection
   bool erode = false;
   int cmp = 0;
   char aop = '+';
@@ -716,6 +717,33 @@ struct slcs_program {
       }
     }
 
+    // ---- nears folded into reach targets: the fused reach stages its target
+    // window with a wider halo and applies near^tk itself (tk <= 2), and a
+    // reach whose only consumer is another reach's target emits its selection
+    // t | S (k = 0) -- the consumer applies the closing near^k as part of its tk.
+    // The chain near -> reach -> near -> reach ... becomes one launch per reach.
+    if (fuse) {
+      for (LG& n : lgs) n.consumers = 0;
+      for (const LG& n : lgs)
+        if (!n.dead)
+          for (int q : n.in) lgs[q].consumers++;
+      for (LG& n : lgs) {
+        if (n.dead || n.kind != LG_REACH || n.gen_idx >= 0 || ccl_small_path(n.w, n.h)) continue;
+        LG& m = lgs[n.in[0]];
+        if (m.kind == LG_NEAR && !m.erode && m.consumers == 1 && !m.output &&
+            n.tk + m.k <= 2) {
+          n.tk += m.k;
+          n.in[0] = m.in[0];
+          m.dead = true;
+        } else if (m.kind == LG_REACH && !m.dead && m.gen_idx < 0 && m.consumers == 1 &&
+                   !m.output && m.k >= 1 && n.tk + m.k <= 2 && m.w == n.w && m.h == n.h &&
+                   m.batch == n.batch && n.in[1] != n.in[0]) {
+          n.tk += m.k;
+          m.k = 0;
+        }
+      }
+    }
+
     // ---- memory plan over live nodes in order
     std::vector<int> order;
     for (size_t q = 0; q < lgs.size(); ++q)
@@ -829,6 +857,8 @@ struct slcs_program {
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
       if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
+      if (n.kind == LG_REACH && n.tk > 0) os << " target near^" << n.tk;
+      if (n.kind == LG_REACH && n.k == 0) os << " emits selection";
       if (n.kind == LG_REACH && n.k > 1) os << " closing near^" << n.k;
       os << " " << n.w << "x" << n.h;
       if (n.batch > 1) os << "x" << n.batch;
@@ -954,7 +984,7 @@ struct slcs_program {
                               : reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + sb);
           launches += launch_reach(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
                                    static_cast<const uint32_t*>(lgs[n.in[1]].ptr),
-                                   static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st, n.k);
+                                   static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st, n.k, n.tk);
           break;
         }
         case LG_MAXVOL: {

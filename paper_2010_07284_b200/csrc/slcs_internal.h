@@ -181,10 +181,12 @@ void ccl_scratch_carve_large(void* base, int w, int h, int batch, bool flags, bo
                              CclScratch* s);
 int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch& s,
                cudaStream_t st);
-// k_out: radius of the closing near (1 = reach; > 1 absorbs following nears)
+// k_out: radius of the closing near (1 = reach; > 1 absorbs following nears;
+// 0 = emit the selection t | S, its consumer folds the closing near as its tk).
+// tk: the target operand is near^tk(target) (nears folded into the reach).
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
                  uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st,
-                 int k_out = 1);
+                 int k_out = 1, int tk = 0);
 int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
                   cudaStream_t st);
 // row bands: reach in phases (large path always)
