@@ -523,14 +523,16 @@ def c4_config(args, ws, rank, local):
 
 
 def c5_config(args, ws, rank, local):
-    """c5: a 65536^2 random mask in row bands, one per rank (weak in pixels per GPU
-    only at N=1 vs N>1 on the same image: the image is fixed -> strong scaling).
-    Per step: near^4 (halo exchange), volume (all-reduce), reach (cross-band merge)."""
+    """c5: a 65536^2 random mask in row bands, one per rank (the image is fixed ->
+    strong scaling).  Per step: near^4 (one k-row halo exchange), volume (sum over
+    ranks), reach (cross-band flag merge) and ccl::label as global 64-bit labels
+    (cross-band label merge; at N=1 the image is run as two in-process bands,
+    since 65536^2 labels do not fit the reference's 32-bit packing)."""
     import torch
 
     from paper_2010_07284_b200 import Device
-    from paper_2010_07284_b200.bands import (TorchComm, band_rows, near_banded, reach_banded,
-                                             volume_banded)
+    from paper_2010_07284_b200.bands import (LocalGroup, TorchComm, band_rows, ccl_banded,
+                                             near_banded, reach_banded, volume_banded)
     from paper_2010_07284_b200.pixlog import random_mask_device
 
     stream = torch.cuda.Stream(device=local)
@@ -555,11 +557,22 @@ def c5_config(args, ws, rank, local):
 
     comm = TorchComm() if ws > 1 else _Solo()
 
+    if ws == 1 and n * n >= 0xFFFFFFFE:
+        from paper_2010_07284_b200.bands import _rows
+        halves = [_rows(mask, 0, n // 2), _rows(mask, n // 2, n - n // 2)]
+
+        def labels():
+            return LocalGroup(2).run(ccl_banded, halves)
+    else:
+        def labels():
+            return ccl_banded(comm, mask)
+
     def step():
         x = near_banded(comm, mask, 4)
         v = volume_banded(comm, x)
         r = reach_banded(comm, target, mask)
-        return v, r
+        lab = labels()
+        return v, r, lab
 
     for _ in range(max(1, min(args.warmup, 2))):
         step()
@@ -577,7 +590,7 @@ def c5_config(args, ws, rank, local):
         tt = torch.tensor([t], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t = float(tt.item())
-    ops = 4 + 1 + 1
+    ops = 4 + 1 + 1 + 1
     if rank == 0:
         print(json.dumps({
             "metric": "Gpixel-ops/s", "value": ops * n * n * args.steps / t / 1e9,
@@ -586,7 +599,7 @@ def c5_config(args, ws, rank, local):
             "vs_baseline": None, "dtype": "u1 (bit-packed)", "data": "synthetic",
             "config": {"workload": f"BASELINE config 5: {n}x{n} random mask (density "
                                    f"{args.density}) in {ws} row band(s): near^4 + volume + "
-                                   f"reach (target density 0.05)",
+                                   f"reach (target density 0.05) + ccl::label (64-bit labels)",
                        "rows_per_rank": r1 - r0, "timing": "host wall clock around synced "
                                                            "steps (includes exchanges), max over ranks"},
             "gpu_launches": dev.launches - l0, "clocks": clocks.summary(),

@@ -103,6 +103,16 @@ int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch
 int slcs_image_storage(const slcs_image* img, void** dev, size_t* row_pitch_bytes,
                        size_t* slice_bytes);
 
+/* Row-band CCL: global 64-bit labels of one band from its
+ * band-local labels (`labels`: a LABEL image, local max index + 1).  Every
+ * non-zero label becomes row0*W + label, except the `nkeys` sorted labels in
+ * `keys_dev` (device memory) that take `vals_dev[k]` -- the canonical label of
+ * a component merged across band borders.  `out_dev`: W*H uint64 in device
+ * memory, written in stream order. */
+int slcs_ccl_band_relabel(slcs_ctx* ctx, const slcs_image* labels, uint64_t row0,
+                          const uint32_t* keys_dev, const uint64_t* vals_dev, int nkeys,
+                          uint64_t* out_dev);
+
 /* ---- image ingest / egress (png_io, proj/src/png_io.cpp:30-144) ----------
  * loadPng: 8/16-bit grey, grey+alpha, RGB or RGBA (Adam7 allowed) -> U16, the
  * first channel, 8-bit samples widened by v*257; palette images and other bit

@@ -53,6 +53,7 @@ _SIGS = {
     "slcs_volume": (i32, [vp, vp, C.POINTER(i64)]),
     "slcs_volume_async": (i32, [vp, vp, vp]),
     "slcs_png_load": (i32, [vp, cstr, pvp]),
+    "slcs_ccl_band_relabel": (i32, [vp, vp, C.c_uint64, vp, vp, i32, vp]),
     "slcs_png_decode": (i32, [vp, vp, sz, pvp]),
     "slcs_png_save": (i32, [vp, vp, cstr]),
     "slcs_label_color": (None, [C.c_uint32, vp]),

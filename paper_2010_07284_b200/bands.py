@@ -102,6 +102,48 @@ def resolve_border_flags(rows: list) -> list:
     return [root[newly & (band == r)] for r in range(nb)]
 
 
+def merge_band_labels(rows: list, width: int) -> list:
+    """Cross-band CCL label merge.  rows[r] = (first_row_labels,
+    last_row_labels, height) of band r, labels band-local (local max index + 1,
+    0 = background).  Band r's global labels are local + row0_r * W.  Components
+    that touch across a band border (8-connectivity: column offsets -1, 0, +1)
+    are united and take the largest global label of the union -- the canonical
+    label of the whole-image ccl::label (max index + 1, ccl.hpp:52-60).  Returns,
+    per band, (keys: sorted local labels (uint32), vals: new global labels
+    (uint64)) for the labels whose global value changes."""
+    nb = len(rows)
+    row0 = np.cumsum([0] + [int(r[2]) for r in rows[:-1]]).astype(np.uint64)
+    W = np.uint64(width)
+    src, dst = [], []
+    for r in range(nb - 1):
+        a = np.asarray(rows[r][1], np.uint64)
+        b = np.asarray(rows[r + 1][0], np.uint64)
+        for d in (-1, 0, 1):
+            lo, hi = max(0, -d), min(width, width - d)
+            m = (a[lo:hi] > 0) & (b[lo + d:hi + d] > 0)
+            if m.any():
+                src.append(a[lo:hi][m] + row0[r] * W)
+                dst.append(b[lo + d:hi + d][m] + row0[r + 1] * W)
+    if not src:
+        return [(np.zeros(0, np.uint32), np.zeros(0, np.uint64)) for _ in range(nb)]
+    src, dst = np.concatenate(src), np.concatenate(dst)
+    ids, inv = np.unique(np.concatenate([src, dst]), return_inverse=True)
+    comp = _components(ids.size, inv[:src.size], inv[src.size:])
+    cmax = np.zeros(comp.max() + 1, np.uint64)
+    np.maximum.at(cmax, comp, ids)
+    new = cmax[comp]
+    changed = new != ids
+    out = []
+    for r in range(nb):
+        lo_id = row0[r] * W
+        hi_id = lo_id + np.uint64(int(rows[r][2])) * W
+        mine = changed & (ids > lo_id) & (ids <= hi_id)
+        keys = (ids[mine] - lo_id).astype(np.uint32)
+        order = np.argsort(keys)
+        out.append((keys[order], new[mine][order]))
+    return out
+
+
 def _components(n: int, src: np.ndarray, dst: np.ndarray) -> np.ndarray:
     """Connected components of the undirected border graph (scipy csgraph)."""
     from scipy.sparse import coo_matrix
@@ -318,3 +360,31 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
         L.slcs_reach_state_destroy(st)
     sel_band = _rows(sel_ext, off, h) if sel_ext.height != h else sel_ext
     return near_banded(comm, sel_band, 1)
+
+
+def ccl_banded(comm: Comm, band: DeviceImage):
+    """ccl::label of the full image, restricted to this band, as global 64-bit labels
+    (a torch.int64 tensor on the band's device): band-local union-find labels, one
+    exchange of the first/last label rows, the cross-band merge above, and a device
+    relabel (slcs_ccl_band_relabel).  Equal to the single-image labels where those
+    fit in 32 bits; 65536^2 (config 5) needs the 64-bit form."""
+    import torch
+
+    from .pixlog import ccl
+    dev, w, h = band.device, band.width, band.height
+    local = ccl.label(band, dev)
+    first = _rows(local, 0, 1).numpy().reshape(-1)
+    last = _rows(local, h - 1, 1).numpy().reshape(-1)
+    rows = comm.allgather((first, last, h))
+    keys, vals = merge_band_labels(rows, w)[comm.rank]
+    row0 = sum(int(r[2]) for r in rows[:comm.rank])
+    tdev = torch.device("cuda", dev.device)
+    out = torch.empty((h, w), dtype=torch.int64, device=tdev)
+    k = torch.from_numpy(keys.astype(np.int32)).to(tdev) if keys.size else None
+    v = torch.from_numpy(vals.astype(np.int64)).to(tdev) if vals.size else None
+    torch.cuda.synchronize(tdev)  # the uploads are on torch's stream
+    _check(_lib.load().slcs_ccl_band_relabel(
+        dev.handle, local.handle, row0, None if k is None else k.data_ptr(),
+        None if v is None else v.data_ptr(), int(keys.size), out.data_ptr()))
+    dev.synchronize()
+    return out

@@ -915,3 +915,20 @@ int slcs_png_save(slcs_ctx* ctx, const slcs_image* img, const char* path) {
 }
 
 void slcs_label_color(uint32_t packed, uint8_t rgb[3]) { png_label_color(packed, rgb); }
+
+int slcs_ccl_band_relabel(slcs_ctx* ctx, const slcs_image* labels, uint64_t row0,
+                          const uint32_t* keys_dev, const uint64_t* vals_dev, int nkeys,
+                          uint64_t* out_dev) {
+  return guard([&] {
+    LOCKED(ctx);
+    need_img(labels);
+    if (labels->kind != SLCS_LABEL) fail(SLCS_ERR_KIND, "band relabel expects a label image");
+    if (!out_dev || (nkeys > 0 && (!keys_dev || !vals_dev))) fail(SLCS_ERR_ARG, "null argument");
+    const Geo& g = labels->geo;
+    const size_t n = size_t(g.w) * size_t(g.h) * size_t(g.batch);
+    ctx->launches += launch_relabel_u64(
+        static_cast<const uint32_t*>(labels->data), n, (unsigned long long)(row0) * g.w, keys_dev,
+        reinterpret_cast<const unsigned long long*>(vals_dev), nkeys,
+        reinterpret_cast<unsigned long long*>(out_dev), ctx->stream);
+  });
+}

@@ -1566,6 +1566,38 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();  // 11: near
 }
 
+// ---- row-band CCL: band-local labels -> global 64-bit labels ---------------------
+// A band's labels are the reference's packed form for the band alone
+// (local max index + 1).  Globally the same component's label is the local one
+// plus row0 * W; components that cross band borders take the merged
+// component's max (the canonical label), looked up in a sorted key table.
+__global__ void k_relabel_u64(const uint32_t* __restrict__ lab, size_t n, unsigned long long offset,
+                              const uint32_t* __restrict__ keys,
+                              const unsigned long long* __restrict__ vals, int nkeys,
+                              unsigned long long* __restrict__ out) {
+  slcs_pdl_wait();
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t l = lab[i];
+    unsigned long long v = 0;
+    if (l) {
+      v = offset + l;
+      int lo = 0, hi = nkeys - 1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t k = __ldg(keys + mid);
+        if (k == l) {
+          v = __ldg(vals + mid);
+          break;
+        }
+        if (k < l) lo = mid + 1;
+        else hi = mid - 1;
+      }
+    }
+    out[i] = v;
+  }
+}
+
 int grid_blocks(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -1904,6 +1936,14 @@ int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
   pdl(k_maxvol_select, sg, 256, 0, st, bits, s.parent, s.size, s.maxv, out, g);
   return launches + 2;
+}
+
+int launch_relabel_u64(const uint32_t* lab, size_t n, unsigned long long offset,
+                       const uint32_t* keys, const unsigned long long* vals, int nkeys,
+                       unsigned long long* out, cudaStream_t st) {
+  pdl(k_relabel_u64, unsigned(std::min<size_t>((n + 255) / 256, 148 * 32)), 256, 0, st, lab, n,
+      offset, keys, vals, nkeys, out);
+  return 1;
 }
 
 }  // namespace slcs

@@ -208,6 +208,11 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
                          uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
                          uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out = 1);
 
+// row-band CCL: out[i] = 0 | vals[k] if lab[i] == keys[k] (keys sorted) | offset + lab[i]
+int launch_relabel_u64(const uint32_t* lab, size_t n, unsigned long long offset,
+                       const uint32_t* keys, const unsigned long long* vals, int nkeys,
+                       unsigned long long* out, cudaStream_t st);
+
 // ---- PNG ingest/egress (png.cu) --------------------------------------------------
 struct PngInfo {
   int w = 0, h = 0, depth = 8, channels = 1;

@@ -127,3 +127,27 @@ def test_two_process_gloo_banded_reach():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert np.array_equal(O.dilate(O.logical_or(t, S)), O.reach(t, u))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+@pytest.mark.parametrize("w,h,d", [(97, 61, 0.41), (64, 200, 0.55), (33, 17, 0.7)])
+def test_cross_band_label_merge_matches_whole_image(world, w, h, d):
+    # band-local oracle labels + merge_band_labels + the relabel rule must give the
+    # whole-image ccl::label labels (canonical max index + 1)
+    from paper_2010_07284_b200.bands import band_rows, merge_band_labels
+    a = O.random_mask(w, h, d, O.Rng(w * h + world))
+    bands = [a[slice(*band_rows(h, world, r))] for r in range(world)]
+    local = [O.flood_fill_label(b).astype(np.uint64) for b in bands]
+    rows = [(l[0], l[-1], l.shape[0]) for l in local]
+    maps = merge_band_labels(rows, w)
+    row0 = 0
+    out = []
+    for l, (keys, vals) in zip(local, maps):
+        g = np.where(l > 0, l + np.uint64(row0 * w), 0).astype(np.uint64)
+        if keys.size:
+            idx = np.searchsorted(keys, l.astype(np.uint32))
+            hit = (idx < keys.size) & (keys[np.minimum(idx, keys.size - 1)] == l)
+            g = np.where(hit, vals[np.minimum(idx, keys.size - 1)], g)
+        out.append(g)
+        row0 += l.shape[0]
+    assert np.array_equal(np.concatenate(out), O.flood_fill_label(a).astype(np.uint64))

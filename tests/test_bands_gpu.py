@@ -65,3 +65,25 @@ def test_banded_near_k_halo_exchange(dev, world, h, k):
     assert np.array_equal(np.concatenate(got), ref_n)
     got = grp.run(lambda c, b: near_banded(c, b, k, erode=True).numpy(), ub)
     assert np.array_equal(np.concatenate(got), ref_e)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("w,h,ud", [(1000, 1000, 0.41), (600, 517, 0.5)])
+def test_banded_ccl_equals_single_image_labels(dev, world, w, h, ud):
+    from paper_2010_07284_b200 import ccl
+    from paper_2010_07284_b200.bands import ccl_banded
+    u = O.random_mask(w, h, ud, O.Rng(w + h + 7 * world))
+    ub = split(dev, u, world)
+    got = LocalGroup(world).run(lambda c, b: ccl_banded(c, b).cpu().numpy(), ub)
+    want = ccl.label(DeviceImage.upload(u, PixelKind.Bool, dev)).numpy().astype(np.int64)
+    assert np.array_equal(np.concatenate(got), want)
+
+
+def test_banded_ccl_blob_and_64bit_offsets(dev):
+    # a giant blob component crossing every band; labels of the lower bands exceed
+    # the band-local range, exercising the 64-bit global offsets
+    from paper_2010_07284_b200.bands import ccl_banded
+    img = O.blob_noise(1024, 1024, 1)
+    u = O.threshold(0, img, 56360)
+    got = LocalGroup(6).run(lambda c, b: ccl_banded(c, b).cpu().numpy(), split(dev, u, 6))
+    assert np.array_equal(np.concatenate(got), O.flood_fill_label(u).astype(np.int64))
