@@ -8,6 +8,9 @@
   x0 = img >. 62258, x(2k+1) = near(x(2k)), x(2k+2) = reach(x(2k+1), b),
   b = img >. 56360.
 * ``segmentation_spec`` -- the frozen config-3 spec.
+* ``spiral`` -- synth::generate(Spiral) (proj/src/synth.cpp:83-124) with the
+  Bresenham step conditions corrected (the reference's drawSegment never
+  terminates).
 
 Tests check every generator against the C oracle / reference checksums.
 """
@@ -107,6 +110,56 @@ def blob_noise(w: int, h: int, seed: int) -> np.ndarray:
         px[rr * w + c2] = 57500 + draw() % 3501
         placed += 1
     return px.reshape(h, w)
+
+
+def _draw_segment(px: np.ndarray, r0: int, c0: int, r1: int, c1: int) -> None:
+    """drawSegment (synth.cpp:83-101) with the error terms tested against the
+    right axes (`e2 > -dr` -> step c, `e2 < dc` -> step r), i.e. standard Bresenham."""
+    h, w = px.shape
+    dr, dc = abs(r1 - r0), abs(c1 - c0)
+    sr, sc = (1 if r0 < r1 else -1), (1 if c0 < c1 else -1)
+    err = dc - dr
+    while True:
+        if 0 <= r0 < h and 0 <= c0 < w:
+            px[r0, c0] = 65535
+        if r0 == r1 and c0 == c1:
+            return
+        e2 = 2 * err
+        if e2 > -dr:
+            err -= dr
+            c0 += sc
+        if e2 < dc:
+            err += dc
+            r0 += sr
+
+
+def _lround(x: float) -> int:
+    """std::lround: halves away from zero."""
+    import math
+    return int(math.copysign(math.floor(abs(x) + 0.5), x))
+
+
+def spiral(w: int, h: int, seed: int) -> np.ndarray:
+    """synth::generate(Spiral) (synth.cpp:103-124): an Archimedean spiral of
+    16-px spacing with a seeded phase, drawn as one connected 8-connected curve."""
+    import math
+    px = np.zeros((h, w), np.uint16)
+    rng = Rng(seed)
+    spacing = 16.0
+    a = spacing / (2.0 * math.pi)
+    cr, cc = h / 2.0, w / 2.0
+    max_r = min(w, h) / 2.0 - 4.0
+    phase = rng.unit() * 2.0 * math.pi
+    theta = 0.0
+    pr, pc = int(round(cr)), int(round(cc))
+    while a * theta < max_r:
+        r = a * theta
+        qr = _lround(cr + r * math.sin(theta + phase))
+        qc = _lround(cc + r * math.cos(theta + phase))
+        _draw_segment(px, pr, pc, qr, qc)
+        pr, pc = qr, qc
+        theta += 0.5 / max(r, 1.0)
+    return px
 
 
 def near_reach_chain(depth: int, through_thr: float = 56360, target_thr: float = 62258,

@@ -159,3 +159,11 @@ def test_race_stress_many_masks(dev, w, h, n):
             from paper_2010_07284_b200 import reach
             got = reach(DeviceImage.upload(t, PixelKind.Bool, dev), da).numpy()
             assert np.array_equal(got, O.reach(t, a)), (i, d)
+
+
+@pytest.mark.parametrize("n,seed", [(512, 1), (2048, 3), (4096, 7)])
+def test_generated_spirals_vs_flood_fill(dev, n, seed):
+    # synth.spiral (corrected synth.cpp:83-124): one thin curve across every tile
+    from paper_2010_07284_b200 import synth as S
+    a = (S.spiral(n, n, seed) > 0).astype(np.uint8)
+    assert np.array_equal(labels(a), O.flood_fill_label(a))

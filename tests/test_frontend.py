@@ -7,6 +7,7 @@ Error cases follow proj/tests/test_frontend.cpp / test_task_graph.cpp.
 import json
 import os
 
+import numpy as np
 import pytest
 
 from paper_2010_07284_b200 import imgql as Q
@@ -84,3 +85,15 @@ def test_payload_text_matches_to_chars():
     assert Q.payload_text(1e300) == "1e+300"
     assert Q.payload_text(1e-7) == "1e-07"
     assert Q.payload_text("a.png") == '"a.png"'
+
+
+def test_corrected_spiral_is_one_long_component():
+    # synth::generate(Spiral) with the Bresenham fix: deterministic, a single
+    # 8-connected curve (the reference generator never terminates)
+    import oracle as O
+    from paper_2010_07284_b200 import synth as S
+    a = S.spiral(300, 260, 5)
+    assert np.array_equal(a, S.spiral(300, 260, 5))
+    m = (a > 0).astype(np.uint8)
+    assert m.sum() > 1500
+    assert len(np.unique(O.flood_fill_label(m))) == 2  # background + one component
