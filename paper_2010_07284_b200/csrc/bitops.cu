@@ -419,8 +419,185 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
   }
 }
 
+// ---- near / interior for wide images: bulk-async (TMA engine) slabs -----------
+// A persistent CTA walks slabs of R output rows x the full row.  Rows are
+// contiguous in HBM, so a slab's R + 2K input rows are ONE cp.async.bulk copy
+// into shared memory, completed on an mbarrier; the next slab's copy is in
+// flight while this one is computed (two stages).  Threads then stream their
+// 16 B column groups down 4-row chunks from shared memory (register ring, one
+// horizontal pass per row) and store uint4 words to HBM.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kBulkRC = 4;  // output rows per thread work item
+
+template <int K, bool ERODE>
+__global__ void __launch_bounds__(256) k_near_bulk(const uint32_t* __restrict__ in,
+                                                   uint32_t* __restrict__ out, int h, int wpr,
+                                                   uint32_t lastmask, int pitch4, size_t slice,
+                                                   int R, int slabs_per_slice, int total) {
+  slcs_pdl_wait();
+  extern __shared__ __align__(128) unsigned char smem[];
+  const size_t pitch = size_t(pitch4) * 4;
+  const int rows_in = R + 2 * K;
+  const size_t stage_words = size_t(rows_in) * pitch;
+  uint32_t* buf0 = reinterpret_cast<uint32_t*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * stage_words * 4);
+  constexpr uint32_t ID = ERODE ? 0xffffffffu : 0u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int slab, int st) {  // thread 0
+    const int sl = slab / slabs_per_slice, r0 = (slab % slabs_per_slice) * R;
+    const int lo = max(0, r0 - K), hi = min(h, r0 + R + K);
+    const unsigned bytes = unsigned(size_t(hi - lo) * pitch * 4);
+    mbar_expect_tx(&bar[st], bytes);
+    bulk_g2s(buf0 + st * stage_words + size_t(lo - (r0 - K)) * pitch,
+             in + size_t(sl) * slice + size_t(lo) * pitch, bytes, &bar[st]);
+  };
+  if (threadIdx.x == 0 && int(blockIdx.x) < total) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int slab = blockIdx.x; slab < total; slab += gridDim.x, ++it) {
+    const int st = it & 1;
+    if (threadIdx.x == 0 && slab + int(gridDim.x) < total) issue(slab + gridDim.x, st ^ 1);
+    const int sl = slab / slabs_per_slice, r0 = (slab % slabs_per_slice) * R;
+    uint32_t* b = buf0 + st * stage_words;
+    // rows outside the image (not part of the copy) read as the identity
+    const int top = max(0, K - r0), bot = max(0, r0 + R + K - h);
+    for (size_t q = threadIdx.x; q < size_t(top) * pitch; q += blockDim.x) b[q] = ID;
+    for (size_t q = threadIdx.x; q < size_t(bot) * pitch; q += blockDim.x)
+      b[size_t(rows_in - bot) * pitch + q] = ID;
+    mbar_wait(&bar[st], unsigned(it >> 1) & 1u);
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(out + size_t(sl) * slice);
+    const int items = pitch4 * (R / kBulkRC);
+    for (int item = threadIdx.x; item < items; item += blockDim.x) {
+      const int q = item % pitch4, c = item / pitch4;
+      const int j0 = 4 * q;
+      const int rr0 = c * kBulkRC;  // first output row of the chunk, slab-relative
+      if (r0 + rr0 >= h) continue;
+      if (j0 >= wpr) {
+        for (int i = 0; i < kBulkRC && r0 + rr0 + i < h; ++i)
+          dst[size_t(r0 + rr0 + i) * pitch4 + q] = make_uint4(0, 0, 0, 0);
+        continue;
+      }
+      uint32_t pad[5], vm[4];
+#pragma unroll
+      for (int e = 0; e < 5; ++e) pad[e] = ERODE ? ~valid_mask(j0 + e, wpr, lastmask) : 0u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) vm[e] = valid_mask(j0 + e, wpr, lastmask);
+      const bool has_l = j0 > 0, has_r = j0 + 4 < wpr;
+      uint32_t hr[kBulkRC + 2 * K][4];
+#pragma unroll
+      for (int i = 0; i < kBulkRC + 2 * K; ++i) {
+        const uint32_t* row = b + size_t(rr0 + i) * pitch;  // buffer row = slab row - K
+        const uint4 cw = *reinterpret_cast<const uint4*>(row + j0);
+        uint32_t w[6];
+        w[0] = has_l ? row[j0 - 1] : ID;
+        w[1] = cw.x | pad[0];
+        w[2] = cw.y | pad[1];
+        w[3] = cw.z | pad[2];
+        w[4] = cw.w | pad[3];
+        w[5] = has_r ? (row[j0 + 4] | pad[4]) : ID;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t acc = w[e + 1];
+#pragma unroll
+          for (int d = 1; d <= K; ++d) {
+            const uint32_t lft = __funnelshift_l(w[e], w[e + 1], d);
+            const uint32_t rgt = __funnelshift_r(w[e + 1], w[e + 2], d);
+            acc = ERODE ? (acc & lft & rgt) : (acc | lft | rgt);
+          }
+          hr[i][e] = acc;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kBulkRC; ++i) {
+        if (r0 + rr0 + i < h) {
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t acc = hr[i][e];
+#pragma unroll
+            for (int d = 1; d <= 2 * K; ++d) acc = ERODE ? (acc & hr[i + d][e]) : (acc | hr[i + d][e]);
+            o[e] = acc & vm[e];
+          }
+          dst[size_t(r0 + rr0 + i) * pitch4 + q] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    }
+    __syncthreads();  // stage st is reused by the copy issued two slabs later
+  }
+}
+
+// slab height for the bulk path: R + 2K input rows in <= 52 KB per stage (two
+// stages, two CTAs per SM), R a multiple of the 4-row chunk; 0 when rows are too
+// wide or the image too small.  Used for K = 1 (near / interior): for K >= 2 the
+// 2K halo rows per slab cost more than the streaming kernel's long strips
+// (measured: near^4 at 16384^2 0.39 -> 0.32 of peak on the bulk path).
+inline int bulk_slab_rows(const Geo& g, int k) {
+  const size_t rowbytes = g.pitch * 4;
+  if (k != 1 || g.pitch < 128 || size_t(g.h) * size_t(g.batch) < 512) return 0;
+  int R = int(53248 / rowbytes) - 2 * k;
+  R = std::min(R, 32) / kBulkRC * kBulkRC;
+  return R >= kBulkRC ? R : 0;
+}
+
+template <int K, bool ERODE>
+bool near_bulk_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
+  static const bool off = [] {
+    const char* e = std::getenv("SLCS_NO_BULK_NEAR");
+    return e && *e && *e != '0';
+  }();
+  const int R = bulk_slab_rows(g, K);
+  if (off || R == 0) return false;
+  const size_t smem = 2 * size_t(R + 2 * K) * g.pitch * 4 + 16;
+  static const bool attr = [] {
+    cudaFuncSetAttribute(k_near_bulk<K, ERODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         112 * 1024);
+    return true;
+  }();
+  (void)attr;
+  const int per_slice = (g.h + R - 1) / R;
+  const int total = per_slice * g.batch;
+  const int ctas = std::min(total, 148 * 2);
+  pdl(k_near_bulk<K, ERODE>, ctas, 256, smem, st, a, out, g.h, g.wpr, g.lastmask,
+      int(g.pitch / 4), g.slice, R, per_slice, total);
+  return true;
+}
+
 template <int K, bool ERODE>
 void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
+  if (near_bulk_launch<K, ERODE>(a, out, g, st)) return;
   const int pitch4 = int(g.pitch / 4);
   const int block = 128;
   if (K == 1) {

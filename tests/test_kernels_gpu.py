@@ -254,3 +254,22 @@ def test_volume_async_writes_device_counts(dev):
         assert lib.slcs_volume_async(dev.handle, img.handle, C.c_void_p(out.data_ptr())) == 0
         dev.synchronize()
         assert out.cpu().tolist() == [int(x.sum()) for x in a]
+
+
+@pytest.mark.parametrize("w,h,batch", [(4096, 515, 1), (4129, 600, 1), (8192 + 7, 257, 1),
+                                       (4096, 130, 4), (16384, 64, 9)])
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_wide_images_bulk_slab_near(dev, w, h, batch, k):
+    # rows >= 4096 px take the bulk-async slab kernel (one cp.async.bulk per slab,
+    # identity rows at the image edges, slabs crossing slice boundaries in a batch)
+    rng = O.Rng(w * 7 + h + k + batch)
+    a = np.stack([rm(w, h, 0.02, rng) for _ in range(batch)])
+    e = np.stack([rm(w, h, 0.98, rng) for _ in range(batch)])
+    got_d = kernels.dilateK(DeviceImage.upload(a, PixelKind.Bool, dev), k).numpy().reshape(a.shape)
+    got_e = kernels.erodeK(DeviceImage.upload(e, PixelKind.Bool, dev), k).numpy().reshape(e.shape)
+    for i in range(batch):
+        ed, ee = a[i], e[i]
+        for _ in range(k):
+            ed, ee = O.dilate(ed), O.erode(ee)
+        assert np.array_equal(got_d[i], ed)
+        assert np.array_equal(got_e[i], ee)
