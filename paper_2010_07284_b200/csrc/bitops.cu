@@ -639,7 +639,7 @@ void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaSt
   }
 }
 
-// volume: one launch.  4 independent uint4 loads in flight per thread,
+// volume: one launch.  8 independent uint4 loads in flight per thread,
 // popcount, warp + block reduction, one u64 atomic per CTA into a per-slice
 // accumulator; the slice's last CTA (done counter) publishes the count (u64
 // and/or double) and resets accumulator and counter to zero, so no memset
@@ -652,13 +652,13 @@ __global__ void k_volume(const uint4* __restrict__ a, size_t slice4, unsigned lo
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long local = 0;
-  for (; q + 3 * stride < slice4; q += 4 * stride) {
-    uint4 x[4];
+  for (; q + 7 * stride < slice4; q += 8 * stride) {
+    uint4 x[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = __ldg(src + q + u * stride);
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(src + q + u * stride);
     unsigned c = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) c += __popc(x[u].x) + __popc(x[u].y) + __popc(x[u].z) + __popc(x[u].w);
+    for (int u = 0; u < 8; ++u) c += __popc(x[u].x) + __popc(x[u].y) + __popc(x[u].z) + __popc(x[u].w);
     local += c;
   }
   for (; q < slice4; q += stride) {
@@ -796,8 +796,8 @@ int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erod
 int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
                   unsigned long long* vscratch, const Geo& g, cudaStream_t st) {
   size_t n4 = g.slice / 4;
-  int gx = grid_for(n4, kThreads * 4, 148 * 4);
-  if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 4 + g.batch - 1) / g.batch));
+  int gx = grid_for(n4, kThreads * 8, 148 * 8);
+  if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 8 + g.batch - 1) / g.batch));
   dim3 grid(unsigned(gx), unsigned(g.batch));
   unsigned int* done = reinterpret_cast<unsigned int*>(vscratch + g.batch);
   pdl(k_volume, grid, kThreads, 0, st, reinterpret_cast<const uint4*>(a), n4, vscratch, done,
