@@ -249,11 +249,10 @@ struct RunTile {
   // O(log n) deep, and atomicMax linking lets concurrent unions on one root
   // all make progress.  Roots are therefore arbitrary representatives; the
   // canonical max key is recovered separately where labels need it.
-  __device__ __forceinline__ static uint32_t snode(uint32_t sl) {
-    uint32_t x = (sl * 0x9E37u) & 0xffffu;
-    x ^= x >> 7;
-    return (x << 16) | sl;
-  }
+  // priority = the slot's bits reversed (a van der Corput order: along any run
+  // of consecutive slots the maxima are spread like a ruler sequence, so chains
+  // link into O(log n)-deep trees) -- two instructions instead of a hash
+  __device__ __forceinline__ static uint32_t snode(uint32_t sl) { return __brev(sl) | sl; }
   __device__ __forceinline__ static uint32_t node(uint32_t k) { return snode(uint32_t(slot(k))); }
   // node of run m of word w in `band` without composing the key
   __device__ __forceinline__ static uint32_t rnode(int band, int w, uint32_t T, uint32_t B,
