@@ -1303,6 +1303,10 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   uint32_t* tw = sB + UNITS;                          // TROWS x 10: target + halo
   uint32_t* sw = tw + TROWS * 10;                     // SROWS x 10: selection + halo
   uint16_t* ring = reinterpret_cast<uint16_t*>(sw + SROWS * 10);  // FT_LIST: idx -> root slot
+  // the neighbour tiles' border words, prefetched in phase A for phase B: per
+  // band the left tile's last word (T, B), then the upper tile's last band at
+  // words j0-1 .. j0+8 (T, B)
+  uint32_t* nbw = reinterpret_cast<uint32_t*>(ring + FT_LIST);  // 2 * NB + 20
   __shared__ int s_cnt;
   using T = RunTile<LKW>;
   const int slice = blockIdx.z;
@@ -1332,6 +1336,17 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   } else if (u0 < 20 * TH + 4 * NB) {
     const int q = u0 - 20 * TH, side = q / (2 * NB), hr = R0 + q % (2 * NB);
     tw[(hr - R0 + TH) * 10 + (side ? 9 : 0)] = word_or0(t, g, hr, side ? j0 + 8 : j0 - 1, false);
+  }
+  if (u0 < NB) {  // inputs only: safe to read before any barrier
+    uint32_t a = 0, b = 0;
+    if (blockIdx.x > 0) load_unit(u, g, blockIdx.y * NB + u0, j0 - 1, a, b);
+    nbw[2 * u0] = a;
+    nbw[2 * u0 + 1] = b;
+  } else if (u0 < NB + 10) {
+    uint32_t a = 0, b = 0;
+    if (blockIdx.y > 0) load_unit(u, g, blockIdx.y * NB - 1, j0 - 1 + (u0 - NB), a, b);
+    nbw[2 * NB + 2 * (u0 - NB)] = a;
+    nbw[2 * NB + 2 * (u0 - NB) + 1] = b;
   }
   sT[u0] = Tw;
   sB[u0] = Bw;
@@ -1428,10 +1443,13 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
     }
   }
   __syncthreads();
-  for (uint32_t x = Tw | Bw; x;) {
+  // publish only what the right and lower neighbours read in phase B: runs of
+  // the last band and word-7 runs reaching bit 31 (this tile's own border side
+  // comes from its records)
+  for (uint32_t x = (band == NB - 1 || w == LTWW - 1) ? (Tw | Bw) : 0u; x;) {
     const uint32_t m = first_run(x);
     x &= ~m;
-    if (ring_run(m)) {
+    if (band == NB - 1 || (m >> 31)) {
       const uint32_t k = T::key(band, w, Tw, Bw, m);
       const uint32_t c = tile_id * FT_LIST + (par[root_of(k)] & REC_IDX);
       __stcg(Ps + kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask))), c);
@@ -1442,48 +1460,57 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();  // 5: barrier
 
   // ---- B: unions across this tile's left border (threads 0..NB-1) and top
-  // border (threads NB..NB+7)
+  // border (threads NB..NB+7).  This tile's side comes from shared memory (words
+  // and root records), the neighbour's words were prefetched in phase A; only
+  // the neighbour's published compact ids (P) are read from L2 here.
+  auto own_cnode = [&](int bnd, int ww, uint32_t T, uint32_t B, uint32_t m) {
+    return hnode(tile_id * FT_LIST + (par[root_of(T::key(bnd, ww, T, B, m))] & REC_IDX));
+  };
   if (u0 < NB) {
     const int k = blockIdx.y * NB + u0;
     const int jr = j0, jl = jr - 1;
     if (blockIdx.x > 0 && k < g.BH) {
-      uint32_t Tl, Bl, Tr, Br;
-      load_unit(u, g, k, jl, Tl, Bl);
-      load_unit(u, g, k, jr, Tr, Br);
+      const uint32_t Tl = nbw[2 * u0], Bl = nbw[2 * u0 + 1];
+      const uint32_t Tr = sT[u0 * LTWW], Br = sB[u0 * LTWW];
       const uint32_t cl = Tl | Bl, cr = Tr | Br;
       const bool hlink = (cl >> 31) && (cr & 1u);
       const uint32_t va = hlink ? cnode(Ps, g, k, jl, Tl, Bl, run_at(cl, 31)) : 0u;
-      const uint32_t vb = hlink ? cnode(Ps, g, k, jr, Tr, Br, run_at(cr, 0)) : 0u;
+      const uint32_t vb = hlink ? own_cnode(u0, 0, Tr, Br, run_at(cr, 0)) : 0u;
       cunite_dedup(GP, va, vb, hlink);
       if (u0 != 0 && ((Tr & 1u) || (Tl >> 31))) {
-        uint32_t Tul, Bul, Tur, Bur;
-        load_unit(u, g, k - 1, jl, Tul, Bul);
-        load_unit(u, g, k - 1, jr, Tur, Bur);
+        const uint32_t Tul = nbw[2 * u0 - 2], Bul = nbw[2 * u0 - 1];
+        const uint32_t Tur = sT[(u0 - 1) * LTWW], Bur = sB[(u0 - 1) * LTWW];
         if ((Tr & 1u) && (Bul >> 31) && !(Bur & 1u))
-          cunite(GP, cnode(Ps, g, k, jr, Tr, Br, run_at(cr, 0)),
+          cunite(GP, own_cnode(u0, 0, Tr, Br, run_at(cr, 0)),
                  cnode(Ps, g, k - 1, jl, Tul, Bul, run_at(Tul | Bul, 31)));
         if ((Tl >> 31) && (Bur & 1u) && !(Bul >> 31))
           cunite(GP, cnode(Ps, g, k, jl, Tl, Bl, run_at(cl, 31)),
-                 cnode(Ps, g, k - 1, jr, Tur, Bur, run_at(Tur | Bur, 0)));
+                 own_cnode(u0 - 1, 0, Tur, Bur, run_at(Tur | Bur, 0)));
       }
     }
   } else if (u0 < NB + LTWW) {
     const int k = blockIdx.y * NB;
-    const int jj = j0 + (u0 - NB);
+    const int wo = u0 - NB, jj = j0 + wo;
     if (blockIdx.y > 0 && jj < g.wpr) {
-      uint32_t T0, B0, Tu, Bu;
-      load_unit(u, g, k, jj, T0, B0);
-      load_unit(u, g, k - 1, jj, Tu, Bu);
+      const uint32_t T0 = sT[wo], B0 = sB[wo];
+      const uint32_t* up = nbw + 2 * NB + 2 * (wo + 1);  // upper band, word jj
+      const uint32_t Tu = up[0], Bu = up[1];
       uint32_t Tl = 0, Bl = 0, Tr = 0, Br = 0;
-      if ((T0 & 1u) && !(Bu & 1u)) load_unit(u, g, k - 1, jj - 1, Tl, Bl);
-      if ((T0 >> 31) && !(Bu >> 31)) load_unit(u, g, k - 1, jj + 1, Tr, Br);
+      if ((T0 & 1u) && !(Bu & 1u)) {
+        Tl = up[-2];
+        Bl = up[-1];
+      }
+      if ((T0 >> 31) && !(Bu >> 31)) {
+        Tr = up[2];
+        Br = up[3];
+      }
       const uint32_t cu = Tu | Bu;
       for (uint32_t x = T0 | B0; x;) {
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t td = T0 & m;
         if (!td) continue;
-        const uint32_t v = cnode(Ps, g, k, jj, T0, B0, m);
+        const uint32_t v = own_cnode(0, wo, T0, B0, m);
         for (uint32_t a = dil1(td) & Bu; a;) {
           const uint32_t mu = run_at(cu, __ffs(a) - 1);
           a &= ~mu;
@@ -1794,7 +1821,8 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   constexpr int THREADS = NB * LTWW;
   constexpr size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4 +
                           size_t(2 * NB + 2 * (TK + 1)) * 40 +
-                          size_t(KOUT > 0 ? 2 * NB + 2 * KOUT : 1) * 40 + FT_LIST * 2;
+                          size_t(KOUT > 0 ? 2 * NB + 2 * KOUT : 1) * 40 + FT_LIST * 2 +
+                          size_t(2 * NB + 20) * 4;
   // co-resident CTAs on this device (thread-safe one-time initialisation)
   static const int capacity = [] {
     int dev = 0, sms = 0, per = 0;
