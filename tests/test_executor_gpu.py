@@ -272,3 +272,51 @@ def test_reach_closing_radius_absorbs_following_nears(dev, k):
     rep = run_text(f'load t = "t.png"\nload b = "b.png"\nsave "o.png" {expr}\n',
                    {"t.png": t, "b.png": b})
     assert np.array_equal(out_of(rep, "o.png"), ref)
+
+
+CHAIN_SHAPES = [
+    "near(reach(near(near(a)), b))",                      # target near^2 folded, closing near^2
+    "reach(reach(a, b), b)",                              # selection emitted, consumer tk = 1
+    "near(reach(reach(near(a), b), b))",                  # tk 1 -> selection -> tk 1, k_out 2
+    "reach(near(reach(near(reach(a, b)), b)), b)",        # tk 2 twice
+    "reach(near(near(near(a))), b)",                      # tk 3: beyond the fused window
+    "reach(reach(a, b), reach(a, b))",                    # shared reach: no selection emit
+    "near(reach(a, b)) | reach(near(a), b)",              # two consumers of near(a)
+]
+
+
+@needs_ref
+@pytest.mark.parametrize("shape", CHAIN_SHAPES)
+@pytest.mark.parametrize("cse", [False, True])
+def test_reach_folding_shapes_vs_reference_executor(dev, shape, cse):
+    # the planner's reach/near folds (tk, emitted selections, closing radii) on the
+    # fused cooperative kernel, checked against the reference's own executor
+    R = O.Reference(workers=4)
+    img = O.blob_noise(700, 500, 21)
+    spec = ('load img = "img.png"\nlet a = img >. 62258\nlet b = img >. 56360\n'
+            f'save "o.png" {shape}\n')
+    want = R.run(spec, {"img.png": img}, STDLIB, ["o.png"])["outputs"]["o.png"]
+    prog = Program(compile_text(spec))
+    prog.set_input_host("img.png", img, PixelKind.U16)
+    out = [i for i, t in enumerate(prog.graph.nodes) if t.opcode == "save"][0]
+    for graph in (True, False):
+        prog.run(cuda_graph=graph, label_cse=cse)
+        got = np.zeros(img.shape, np.uint8)
+        prog.download(out, got)
+        assert np.array_equal(got, want), (shape, cse, graph, prog.plan)
+
+
+@needs_ref
+def test_random_formulas_vs_reference_executor_large(dev):
+    # the fused/folded paths on random nestings at a size above the small-image path
+    R = O.Reference(workers=4)
+    w, h = 640, 480
+    rng = O.Rng(4242)
+    imgA = O.blob_noise(w, h, 13)
+    imgB = O.blob_noise(w, h, 17)
+    for i in range(8):
+        f = random_formula(rng, 4 + rng.below(8))
+        spec = f'load imgA = "a.png"\nload imgB = "b.png"\nsave "o.png" {f}\n'
+        want = R.run(spec, {"a.png": imgA, "b.png": imgB}, STDLIB, ["o.png"])["outputs"]["o.png"]
+        rep = run_text(spec, {"a.png": imgA, "b.png": imgB}, RunOptions())
+        assert np.array_equal(out_of(rep, "o.png"), want), (i, f)
