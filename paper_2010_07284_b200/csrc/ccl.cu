@@ -563,7 +563,6 @@ __device__ __forceinline__ void load_unit(const uint32_t* u, const G& g, int k, 
 // against the band above (all three column offsets).  Part B: the word pair
 // straddling every vertical tile border (the horizontal link, and the two
 // diagonals into the band above when that band is in the same tile row).
-template <int PART>
 __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G g, int nhb,
                              int nvb) {
   slcs_pdl_wait();
@@ -571,9 +570,8 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t nA = uint32_t(nhb) * uint32_t(g.wpr), nB = uint32_t(nvb) * uint32_t(g.BH);
-  // PART 0: horizontal borders only, 1: vertical only, 2: both in one grid
-  const uint32_t lo = PART == 1 ? nA : 0u, hi = PART == 0 ? nA : nA + nB;
-  for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+  // units [0, nA): horizontal tile borders; [nA, nA + nB): vertical ones
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nA + nB;
        i += gridDim.x * blockDim.x) {
     if (i < nA) {
       const int t = int(i / uint32_t(g.wpr)), j = int(i - uint32_t(t) * uint32_t(g.wpr));
@@ -1723,7 +1721,7 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
   const size_t links = size_t(nhb) * g.wpr + size_t(nvb) * g.BH;
   if (links) {
     dim3 mg(unsigned(grid_blocks(links, 256)), unsigned(batch));
-    pdl(k_tile_merge<2>, mg, 256, 0, st, u, s.parent, g, nhb, nvb);
+    pdl(k_tile_merge, mg, 256, 0, st, u, s.parent, g, nhb, nvb);
     ++launches;
     const int ntiles = int(grid.x * grid.y);
     dim3 fg(unsigned((ntiles * 32 + 255) / 256), unsigned(batch));
