@@ -1912,7 +1912,8 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
   if (fused_reach_enabled()) {
     static const int nb = [] {
       const char* e = std::getenv("SLCS_FUSED_NB");
-      return (e && std::atoi(e) == 128) ? 128 : 64;  // A/B switch; 32 measured slower
+      // A/B switch; 32-band tiles measured equal (10.72 vs 10.62 ms on the chain)
+      return (e && std::atoi(e) == 128) ? 128 : 64;
     }();
     bool done = false;
 #define SLCS_FUSED(KO, NBV, TKV)                                                                \
