@@ -869,14 +869,21 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
     }
     uint32_t starts = 0;
     {
-      uint32_t x = T | B;
+      // runs of a word mostly share their local root (one piece of a large
+      // component): the last (local root -> label) pair skips two dependent loads
+      uint32_t x = T | B, last_lr = 0xffffffffu, last_lab = 0;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         if (!x) break;
         const uint32_t m = first_run(x);
         x &= ~m;
         starts |= m & (0u - m);
-        tb[lane * 17 + q] = linear_label(g, MK[gblk(g, groot(Ps, g, grun(g, k, j, T, B, m)))]);
+        const uint32_t lr = Ps[gblk(g, grun(g, k, j, T, B, m))];
+        if (lr != last_lr) {
+          last_lr = lr;
+          last_lab = linear_label(g, MK[gblk(g, Ps[gblk(g, lr)])]);
+        }
+        tb[lane * 17 + q] = last_lab;
       }
     }
     __syncwarp();
