@@ -144,13 +144,13 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
-def profiled_traffic(kernel_prefix):
+def profiled_traffic(kernel_prefix, kind="traffic"):
     """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of a
-    kernel from the newest committed ncu summary under profiles/ (cold-cache,
-    serialised ncu replay), with the file it came from; (None, None) if absent."""
+    kernel from the newest committed ncu summary profiles/r*_<kind>_*.json
+    (serialised ncu replay), with the file it came from; (None, None) if absent."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json")),
-                   key=os.path.getmtime, reverse=True)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{kind}_*.json")),
+                   key=lambda f: os.path.basename(f), reverse=True)
     for f in files:
         try:
             with open(f) as fh:
@@ -504,6 +504,15 @@ def c4_config(args, ws, rank, local):
                    "kind": "reference", "sample": f"ccl::label on a {m}x{m} random mask "
                                                   f"(density {args.density})",
                    "ms": t_cpu * 1e3}
+    # DRAM bytes of one ccl::label (its four kernels) from the newest committed
+    # 16384^2 ncu breakdown (--cache-control none), or null
+    ccl_traffic, ccl_src = None, None
+    if n == 16384:
+        parts = [profiled_traffic(k, "kernels_c4") for k in
+                 ("k_tile_local<0", "k_tile_merge", "k_root_flatten", "k_tile_labels")]
+        if all(t for t, _ in parts):
+            ccl_traffic = sum(t for t, _ in parts)
+            ccl_src = parts[0][1].split(" [")[0] + " (sum of the four ccl kernels)"
     if rank == 0:
         print(json.dumps({
             "metric": "Gpixel-ops/s", "value": 2 * px / (tc + tr) / 1e9, "unit": "Gpixel-ops/s",
@@ -517,8 +526,8 @@ def c4_config(args, ws, rank, local):
             "roofline": {"bound": "hbm", "kernel": "ccl::label (tile-local UF, merge, flatten, "
                                                    "labels)",
                          "achieved": 4.125 * px / tc / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": 4.125 * px / tc / 1e9 / peak, "traffic": None,
-                         "peak_source": pk},
+                         "frac": 4.125 * px / tc / 1e9 / peak, "traffic": ccl_traffic,
+                         "traffic_source": ccl_src, "peak_source": pk},
             "cpu_baseline": cpu}), flush=True)
 
 
