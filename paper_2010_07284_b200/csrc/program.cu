@@ -48,7 +48,7 @@ int pguard(F&& f) {
 
 enum Op {
   OP_CONST, OP_LOAD, OP_SAVE, OP_PRINT, OP_INTENSITY, OP_NEAR, OP_NOT, OP_AND, OP_OR, OP_REACH,
-  OP_THRESH, OP_ARITH, OP_VOLUME, OP_MAXVOL
+  OP_THRESH, OP_ARITH, OP_VOLUME, OP_MAXVOL, OP_COMPONENTS
 };
 
 struct PTask {
@@ -82,7 +82,7 @@ struct Expr {
 };
 
 enum LK { LG_INPUT, LG_EW, LG_NEAR, LG_REACH, LG_MAXVOL, LG_VOLUME, LG_ARITH, LG_THRESH_DEV,
-          LG_LABELS };
+          LG_LABELS, LG_CCL };
 
 struct LG {
   LK kind;
@@ -150,6 +150,7 @@ bool parse_opcode(const std::string& s, Op& op, int& sub) {
       {"<=.", {OP_THRESH, SLCS_LE}}, {"=.", {OP_THRESH, SLCS_EQ}},
       {"+", {OP_ARITH, '+'}},     {"-", {OP_ARITH, '-'}},     {"*", {OP_ARITH, '*'}},
       {"/", {OP_ARITH, '/'}},     {"volume", {OP_VOLUME, 0}}, {"maxvol", {OP_MAXVOL, 0}},
+      {"components", {OP_COMPONENTS, 0}},
   };
   auto it = table.find(s);
   if (it == table.end()) return false;
@@ -622,6 +623,26 @@ struct slcs_program {
             v.lg = add_lg(g);
             break;
           }
+          case OP_COMPONENTS: {
+            // components(x): the canonical ccl::label image (ccl.hpp:52-60) as a
+            // value -- new, like maxvol; label images are saved as RGB (png_io)
+            Val& x = bool_arg(t.deps[0]);
+            int a = x.type == VT_U16 ? materialize_expr(as_expr(x, fuse), x.w, x.h, x.batch)
+                                     : materialize(x);
+            if ((unsigned long long)x.w * (unsigned long long)x.h >= 0xfffffffeull)
+              throw Error(SLCS_ERR_TOO_LARGE, "image too large for packed coordinate labels");
+            LG g;
+            g.kind = LG_CCL;
+            g.type = VT_LABEL;
+            g.w = x.w;
+            g.h = x.h;
+            g.batch = x.batch;
+            g.in = {a};
+            v.type = VT_LABEL;
+            shape_from(x);
+            v.lg = add_lg(g);
+            break;
+          }
           case OP_MAXVOL:
           case OP_VOLUME: {
             Val& x = bool_arg(t.deps[0]);
@@ -808,7 +829,7 @@ struct slcs_program {
         size_t s = ccl_scratch_bytes(n.w, n.h, n.batch, true, false);
         if (!ccl_small_path(n.w, n.h)) s += bool_geo(n.w, n.h, n.batch).slice * n.batch * 4;
         scratch_need = std::max(scratch_need, s);
-      } else if (n.kind == LG_MAXVOL) {
+      } else if (n.kind == LG_MAXVOL || n.kind == LG_CCL) {
         scratch_need = std::max(scratch_need, ccl_scratch_bytes(n.w, n.h, n.batch, false, true));
       } else if (n.kind == LG_NEAR && n.k > 8) {
         scratch_need = std::max(scratch_need, n.bytes);
@@ -852,7 +873,7 @@ struct slcs_program {
     for (int q : order) {
       const LG& n = lgs[q];
       static const char* kn[] = {"input", "fused", "near", "reach", "maxvol", "volume", "arith",
-                                 "threshold(dev)", "labels"};
+                                 "threshold(dev)", "labels", "components"};
       os << "  step " << q << ": " << kn[n.kind];
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
@@ -985,6 +1006,13 @@ struct slcs_program {
           launches += launch_reach(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
                                    static_cast<const uint32_t*>(lgs[n.in[1]].ptr),
                                    static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st, n.k, n.tk);
+          break;
+        }
+        case LG_CCL: {
+          CclScratch cs;  // sizes hold the components' max keys
+          ccl_scratch_carve(scratch, n.w, n.h, n.batch, false, true, &cs);
+          launches += launch_ccl(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
+                                 static_cast<uint32_t*>(n.ptr), gb, cs, st);
           break;
         }
         case LG_MAXVOL: {

@@ -11,7 +11,9 @@ task graphs handed to the device program are node-for-node the reference's:
   by-name macro substitution in the caller's scope, ``intern`` hash-consing
   so dependencies always have smaller ids, imports processed once).
 
-The builtin table gains one opcode the reference lacks: ``maxvol`` (arity 1).
+The builtin table gains two opcodes the reference lacks: ``maxvol`` and
+``components`` (the ccl::label image of a mask, saved as an RGB label PNG),
+both of arity 1.
 """
 from __future__ import annotations
 
@@ -397,7 +399,7 @@ class TaskGraph:
 
 BUILTINS = {"near": 1, "reach": 2, "intensity": 1, "volume": 1, "!": 1, "&": 2, "|": 2, "+": 2,
             "-": 2, "*": 2, "/": 2, ">.": 2, ">=.": 2, "<.": 2, "<=.": 2, "=.": 2,
-            "maxvol": 1}
+            "maxvol": 1, "components": 1}
 
 Resolver = Callable[[str], str]
 

@@ -320,3 +320,28 @@ def test_random_formulas_vs_reference_executor_large(dev):
         want = R.run(spec, {"a.png": imgA, "b.png": imgB}, STDLIB, ["o.png"])["outputs"]["o.png"]
         rep = run_text(spec, {"a.png": imgA, "b.png": imgB}, RunOptions())
         assert np.array_equal(out_of(rep, "o.png"), want), (i, f)
+
+
+@pytest.mark.parametrize("w,h", [(200, 150), (700, 500)])
+def test_components_opcode_labels_and_errors(dev, w, h):
+    # components(x) (new, like maxvol): the canonical ccl::label image of a mask
+    img = O.blob_noise(w, h, 9)
+    a = O.threshold(0, img, 40000)
+    rep = run_text('load img = "img.png"\nlet c = components(img >. 40000)\n'
+                   'save "c.png" c\nprint "lab" c\n', {"img.png": img})
+    assert np.array_equal(rep.outputs["c.png"].numpy(), O.flood_fill_label(a))
+    assert rep.printLines == [f"lab=image({w}x{h},label)"]
+    with pytest.raises(RunError, match="expects a boolean image, got label"):
+        run_text('load img = "img.png"\nsave "o.png" near(components(img >. 1))\n',
+                 {"img.png": img})
+
+
+def test_components_saved_as_label_colours(dev, tmp_path):
+    from PIL import Image
+    img = O.blob_noise(96, 64, 2)
+    Image.fromarray(img).save(tmp_path / "in.png")
+    run_text('load img = "in.png"\nsave "lab.png" components(img >. 45000)\n', {},
+             RunOptions(baseDir=str(tmp_path)))
+    lab = O.flood_fill_label(O.threshold(0, img, 45000))
+    want = np.array([[O.label_color(int(x)) for x in row] for row in lab], np.uint8)
+    assert np.array_equal(np.array(Image.open(tmp_path / "lab.png").convert("RGB")), want)
