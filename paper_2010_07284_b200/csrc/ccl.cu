@@ -869,21 +869,44 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
     }
     uint32_t starts = 0;
     {
-      // runs of a word mostly share their local root (one piece of a large
-      // component): the last (local root -> label) pair skips two dependent loads
-      uint32_t x = T | B, last_lr = 0xffffffffu, last_lab = 0;
+      // Three rounds of independent loads (run -> local root -> global root ->
+      // max key) instead of a dependent chain per run.  Runs of a word mostly
+      // share their local root (one piece of a large component), so a repeat
+      // of the previous run's root skips its loads.
+      uint32_t v[16];
+      uint32_t x = T | B;
+      int nr = 0;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        if (!x) break;
-        const uint32_t m = first_run(x);
-        x &= ~m;
-        starts |= m & (0u - m);
-        const uint32_t lr = Ps[gblk(g, grun(g, k, j, T, B, m))];
-        if (lr != last_lr) {
-          last_lr = lr;
-          last_lab = linear_label(g, MK[gblk(g, Ps[gblk(g, lr)])]);
+        v[q] = 0;
+        if (x) {
+          const uint32_t m = first_run(x);
+          x &= ~m;
+          starts |= m & (0u - m);
+          v[q] = Ps[gblk(g, grun(g, k, j, T, B, m))];
+          nr = q + 1;
         }
-        tb[lane * 17 + q] = last_lab;
+      }
+      uint32_t w[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const bool fresh = q < nr && (q == 0 || v[q] != v[q - 1]);
+        w[q] = fresh ? Ps[gblk(g, v[q])] : 0u;
+      }
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if (q < nr && v[q] == v[q - 1]) w[q] = w[q - 1];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const bool fresh = q < nr && (q == 0 || w[q] != w[q - 1]);
+        v[q] = fresh ? MK[gblk(g, w[q])] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q >= nr) break;
+        if (q > 0 && w[q] == w[q - 1]) v[q] = v[q - 1];
+        else v[q] = linear_label(g, v[q]);
+        tb[lane * 17 + q] = v[q];
       }
     }
     __syncwarp();
