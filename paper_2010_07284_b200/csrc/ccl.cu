@@ -677,6 +677,36 @@ __device__ __forceinline__ uint32_t groot(const uint32_t* P, const G& g, uint32_
   return P[gblk(g, P[gblk(g, v)])];
 }
 
+// The global root block of each run of word (k, j), in run order, as two
+// rounds of independent loads instead of a dependent chain per run.  Runs of a
+// word mostly share their local root (one piece of a large component), so a
+// repeat of the previous run's local root skips its second load.
+__device__ __forceinline__ int run_root_blocks(const uint32_t* Ps, const G& g, int k, int j,
+                                               uint32_t T, uint32_t B, uint32_t (&v)[16]) {
+  uint32_t x = T | B;
+  int nr = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    v[q] = 0;
+    if (x) {
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      v[q] = Ps[gblk(g, grun(g, k, j, T, B, m))];
+      nr = q + 1;
+    }
+  }
+  uint32_t w[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    w[q] = (q < nr && (q == 0 || v[q] != v[q - 1])) ? Ps[gblk(g, v[q])] : 0u;
+#pragma unroll
+  for (int q = 1; q < 16; ++q)
+    if (q < nr && v[q] == v[q - 1]) w[q] = w[q - 1];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = gblk(g, w[q]);
+  return nr;
+}
+
 // reach: out = target | through-runs whose global root holds a seed.
 // Thread = word (band k, word j), j fastest: each warp stores 128 B per row.
 __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
@@ -869,44 +899,19 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
     }
     uint32_t starts = 0;
     {
-      // Three rounds of independent loads (run -> local root -> global root ->
-      // max key) instead of a dependent chain per run.  Runs of a word mostly
-      // share their local root (one piece of a large component), so a repeat
-      // of the previous run's root skips its loads.
-      uint32_t v[16];
-      uint32_t x = T | B;
-      int nr = 0;
+      // run -> global root block -> max key, one load round each (see
+      // run_root_blocks); runs sharing a root share its label
+      uint32_t rb[16], lab[16];
+      const int nr = run_root_blocks(Ps, g, k, j, T, B, rb);
+      starts = (T | B) & ~((T | B) << 1);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        v[q] = 0;
-        if (x) {
-          const uint32_t m = first_run(x);
-          x &= ~m;
-          starts |= m & (0u - m);
-          v[q] = Ps[gblk(g, grun(g, k, j, T, B, m))];
-          nr = q + 1;
-        }
-      }
-      uint32_t w[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const bool fresh = q < nr && (q == 0 || v[q] != v[q - 1]);
-        w[q] = fresh ? Ps[gblk(g, v[q])] : 0u;
-      }
-#pragma unroll
-      for (int q = 1; q < 16; ++q)
-        if (q < nr && v[q] == v[q - 1]) w[q] = w[q - 1];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const bool fresh = q < nr && (q == 0 || w[q] != w[q - 1]);
-        v[q] = fresh ? MK[gblk(g, w[q])] : 0u;
-      }
+      for (int q = 0; q < 16; ++q)
+        lab[q] = (q < nr && (q == 0 || rb[q] != rb[q - 1])) ? MK[rb[q]] : 0u;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         if (q >= nr) break;
-        if (q > 0 && w[q] == w[q - 1]) v[q] = v[q - 1];
-        else v[q] = linear_label(g, v[q]);
-        tb[lane * 17 + q] = v[q];
+        lab[q] = (q > 0 && rb[q] == rb[q - 1]) ? lab[q - 1] : linear_label(g, lab[q]);
+        tb[lane * 17 + q] = lab[q];
       }
     }
     __syncwarp();
