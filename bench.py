@@ -489,6 +489,34 @@ def c4_config(args, ws, rank, local):
     tc = sum(a.elapsed_time(b) for a, b in ec) / 1e3 / args.steps
     tr = sum(a.elapsed_time(b) for a, b in er) / 1e3 / args.steps
     px = n * n
+    # SURVEY §8(d) C4 densities: the other two masks, same timing (not in `value`)
+    sweep = {}
+    for dens in (0.41, 0.5, 0.7):
+        if abs(dens - args.density) < 1e-9:
+            sweep[str(dens)] = {"ccl_ms": tc * 1e3, "reach_ms": tr * 1e3}
+            continue
+        m2 = random_mask_device(n, n, dens, 1, 0, dev)
+        for _ in range(2):
+            ccl.label(m2, dev)
+            reach(target, m2, dev)
+        tcs, trs = [], []
+        for _ in range(args.steps):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            flush.zero_()
+            ev[0].record(stream)
+            lab = ccl.label(m2, dev)
+            ev[1].record(stream)
+            del lab
+            flush.zero_()
+            ev[2].record(stream)
+            r = reach(target, m2, dev)
+            ev[3].record(stream)
+            del r
+            torch.cuda.synchronize()
+            tcs.append(ev[0].elapsed_time(ev[1]))
+            trs.append(ev[2].elapsed_time(ev[3]))
+        sweep[str(dens)] = {"ccl_ms": sum(tcs) / len(tcs), "reach_ms": sum(trs) / len(trs)}
+        del m2
     peak, pk = measured_peak_gbs()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -521,7 +549,7 @@ def c4_config(args, ws, rank, local):
             "vs_baseline": None, "dtype": "u1 -> u32 labels", "data": "synthetic",
             "config": {"workload": f"BASELINE config 4: ccl::label + reach on a {n}x{n} random "
                                    f"mask, density {args.density} (target density 0.05)",
-                       "ccl_ms": tc * 1e3, "reach_ms": tr * 1e3},
+                       "ccl_ms": tc * 1e3, "reach_ms": tr * 1e3, "densities": sweep},
             "gpu_launches": dev.launches - l0, "clocks": clocks.summary(),
             "roofline": {"bound": "hbm", "kernel": "ccl::label (tile-local UF, merge, flatten, "
                                                    "labels)",
