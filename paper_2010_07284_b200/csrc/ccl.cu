@@ -1024,7 +1024,7 @@ size_t small_smem_bytes() { return size_t(SSLOTS) * 4 + 2 * ST_THREADS * 4 + 256
 
 // mode 0 = labels, 1 = reach, 2 = maxvol
 template <int MODE>
-__global__ void __launch_bounds__(ST_THREADS, 1) k_small(const uint32_t* __restrict__ ubits,
+__global__ void __launch_bounds__(ST_THREADS, 2) k_small(const uint32_t* __restrict__ ubits,
                                                       const uint32_t* __restrict__ tbits,
                                                       uint32_t* __restrict__ out, G g) {
   slcs_pdl_wait();
