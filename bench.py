@@ -42,8 +42,10 @@ def parse():
     p.add_argument("--size", type=int, default=4096)
     p.add_argument("--depth", type=int, default=1000)
     p.add_argument("--seed", type=int, default=1)
-    p.add_argument("--ref-depth", type=int, default=4,
-                   help="chain depth of one bounded CPU-reference sample")
+    p.add_argument("--ref-depth", type=int, default=20,
+                   help="chain depth of one bounded CPU-reference sample (~10 s on 16 "
+                        "threads; its per-node rate is within 4%% of the full depth-1000 "
+                        "run, profiles/r01f_cpu_reference.json)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-primitives", action="store_true",
