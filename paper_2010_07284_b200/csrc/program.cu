@@ -100,6 +100,7 @@ struct LG {
   int gen_idx = -1;  // LG_REACH against an LG_LABELS input (label CSE)
   std::string name;  // LG_INPUT
   bool dead = false, output = false;
+  int group = -1;  // LG_EW: leader of its multi-output launch (sibling merge)
   int consumers = 0, last_use = -1;
   size_t bytes = 0, offset = 0;
   void* ptr = nullptr;
@@ -281,6 +282,30 @@ struct slcs_program {
     leaves(e, b, u);
     return exprs[e].ops + 2 <= kFusedMaxOps && exprs[e].need <= kFusedRegs &&
            int(b.size()) <= kFusedMaxIn && int(u.size()) <= kFusedMaxIn;
+  }
+
+  // can these LG_EW steps (in order) run as one multi-output listing?
+  bool group_fits(const std::vector<int>& grp) const {
+    std::vector<int> b, u;
+    int ops = 0, need = 0, saved = 0;
+    for (size_t i = 0; i < grp.size(); ++i) {
+      const int e = lgs[grp[i]].expr;
+      leaves(e, b, u);
+      ops += exprs[e].ops + 1;  // + its store
+      need = std::max(need, exprs[e].need);
+      for (size_t k = i + 1; k < grp.size(); ++k)  // read by a later member: forwarded
+        if (std::find(lgs[grp[k]].in.begin(), lgs[grp[k]].in.end(), grp[i]) !=
+            lgs[grp[k]].in.end()) {
+          ++saved;
+          ++ops;  // the copy into its saved register
+          break;
+        }
+    }
+    int nb = 0;  // bool leaves that are not members (members are forwarded)
+    for (int q : b)
+      if (std::find(grp.begin(), grp.end(), q) == grp.end()) ++nb;
+    return ops <= kFusedMaxOps && need + saved <= kFusedRegs && nb <= kFusedMaxIn &&
+           int(u.size()) <= kFusedMaxIn;
   }
 
   // materialise a pending expression as an LG_EW node (or return its leaf)
@@ -765,13 +790,48 @@ struct slcs_program {
       }
     }
 
-    // ---- memory plan over live nodes in order
     std::vector<int> order;
     for (size_t q = 0; q < lgs.size(); ++q)
       if (!lgs[q].dead && lgs[q].kind != LG_INPUT) order.push_back(int(q));
+
+    // ---- sibling merge: adjacent elementwise steps of one shape run as one
+    // multi-output listing (a u16 image thresholded twice is read once, and a
+    // member that a later member reads is forwarded in a register)
+    for (LG& n : lgs) n.group = -1;
+    if (fuse) {
+      for (size_t i = 0; i < order.size();) {
+        const LG& lead = lgs[order[i]];
+        size_t j = i + 1;
+        if (lead.kind == LG_EW) {
+          std::vector<int> grp{order[i]};
+          while (j < order.size() && int(grp.size()) < kFusedMaxOut) {
+            const LG& c = lgs[order[j]];
+            if (c.kind != LG_EW || c.w != lead.w || c.h != lead.h || c.batch != lead.batch)
+              break;
+            grp.push_back(order[j]);
+            if (!group_fits(grp)) {
+              grp.pop_back();
+              break;
+            }
+            ++j;
+          }
+          if (grp.size() > 1)
+            for (int q : grp) lgs[q].group = order[i];
+        }
+        i = j;
+      }
+    }
+
+    // ---- memory plan over live nodes in order; a sibling group is one step
+    // (all its outputs are allocated before any of its inputs is recycled)
+    std::vector<int> stepv(order.size());
+    for (size_t pos = 0; pos < order.size(); ++pos) {
+      const LG& n = lgs[order[pos]];
+      stepv[pos] = (pos > 0 && n.group >= 0 && n.group != order[pos]) ? stepv[pos - 1] : int(pos);
+    }
     for (LG& n : lgs) n.last_use = -1;
     for (size_t pos = 0; pos < order.size(); ++pos)
-      for (int q : lgs[order[pos]].in) lgs[q].last_use = int(pos);
+      for (int q : lgs[order[pos]].in) lgs[q].last_use = stepv[pos];
     struct Blk {
       size_t off, size;
     };
@@ -811,8 +871,11 @@ struct slcs_program {
       freel.swap(merged);
     };
     size_t scratch_need = 0;
-    for (size_t pos = 0; pos < order.size(); ++pos) {
-      LG& n = lgs[order[pos]];
+    for (size_t pos = 0; pos < order.size();) {
+      size_t end = pos + 1;
+      while (end < order.size() && stepv[end] == stepv[pos]) ++end;
+      for (size_t p = pos; p < end; ++p) {
+      LG& n = lgs[order[p]];
       if (n.type == VT_AUX) {
         // labelling + the reach flag stamps (one uint32 per 2x2 block)
         n.bytes = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256) +
@@ -834,17 +897,24 @@ struct slcs_program {
       } else if (n.kind == LG_NEAR && n.k > 8) {
         scratch_need = std::max(scratch_need, n.bytes);
       }
+      }
       // inputs whose last use is this step can be recycled now
-      std::vector<int> uniq = n.in;
+      std::vector<int> uniq;
+      for (size_t p = pos; p < end; ++p)
+        uniq.insert(uniq.end(), lgs[order[p]].in.begin(), lgs[order[p]].in.end());
       std::sort(uniq.begin(), uniq.end());
       uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
       for (int q : uniq) {
         LG& m = lgs[q];
-        if (m.kind != LG_INPUT && m.last_use == int(pos) && !m.output && m.type != VT_NUM)
+        if (m.kind != LG_INPUT && m.last_use == stepv[pos] && !m.output && m.type != VT_NUM)
           release(m.offset, m.bytes);
       }
       // a result nobody consumes (and not an output) is dead after its step
-      if (n.type != VT_NUM && n.last_use < 0 && !n.output) release(n.offset, n.bytes);
+      for (size_t p = pos; p < end; ++p) {
+        LG& n = lgs[order[p]];
+        if (n.type != VT_NUM && n.last_use < 0 && !n.output) release(n.offset, n.bytes);
+      }
+      pos = end;
     }
     arena_bytes = top;
     scratch_bytes = scratch_need;
@@ -877,6 +947,8 @@ struct slcs_program {
       os << "  step " << q << ": " << kn[n.kind];
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
+      if (n.kind == LG_EW && n.group >= 0)
+        os << (n.group == q ? " [sibling group lead]" : " [with step " + std::to_string(n.group) + "]");
       if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
       if (n.kind == LG_REACH && n.tk > 0) os << " target near^" << n.tk;
       if (n.kind == LG_REACH && n.k == 0) os << " emits selection";
@@ -892,6 +964,7 @@ struct slcs_program {
   }
 
   // ------------------------------------------------------------------ emit
+  std::map<int, int> fwd_;  // sibling LG -> register holding its value
   int compile_expr(int e, FusedProgram& fp, std::vector<const uint32_t*>& bin,
                    std::vector<const uint16_t*>& uin, int reg_base) {
     const Expr& x = exprs[e];
@@ -907,6 +980,11 @@ struct slcs_program {
     };
     switch (x.k) {
       case E_LEAF: {
+        auto f = fwd_.find(x.lg);
+        if (f != fwd_.end()) {  // a sibling computed earlier in this listing
+          add(FOP_OR, reg_base, f->second, f->second);
+          return reg_base;
+        }
         const uint32_t* p = static_cast<const uint32_t*>(lgs[x.lg].ptr);
         int idx = int(std::find(bin.begin(), bin.end(), p) - bin.begin());
         if (idx == int(bin.size())) bin.push_back(p);
@@ -951,21 +1029,49 @@ struct slcs_program {
       Geo gb = bool_geo(n.w, n.h, n.batch);
       switch (n.kind) {
         case LG_EW: {
+          if (n.group >= 0 && n.group != int(q)) break;  // emitted with its group lead
+          std::vector<int> members{int(q)};
+          if (n.group >= 0)
+            for (size_t z = q + 1; z < lgs.size(); ++z)
+              if (lgs[z].group == int(q)) {
+                for (int i : lgs[z].in)
+                  if (!lgs[i].ptr) bad = true;
+                members.push_back(int(z));
+              }
+          if (bad) break;
           FusedProgram fp;
           std::vector<const uint32_t*> bin;
           std::vector<const uint16_t*> uin;
-          int r = compile_expr(n.expr, fp, bin, uin, 0);
-          FusedOp st_op;
-          st_op.op = FOP_STORE;
-          st_op.dst = uint8_t(r);
-          st_op.a = 0;
-          st_op.b = 0;
-          st_op.lo = st_op.hi = 0;
-          fp.ops[fp.n_ops++] = st_op;
+          fwd_.clear();
+          int saved_reg = kFusedRegs;
+          for (size_t i = 0; i < members.size(); ++i) {
+            const LG& m = lgs[members[i]];
+            const int r = compile_expr(m.expr, fp, bin, uin, 0);
+            FusedOp st_op;
+            st_op.op = FOP_STORE;
+            st_op.dst = uint8_t(r);
+            st_op.a = uint8_t(i);
+            st_op.b = 0;
+            st_op.lo = st_op.hi = 0;
+            fp.ops[fp.n_ops++] = st_op;
+            fp.out[i] = static_cast<uint32_t*>(m.ptr);
+            for (size_t k = i + 1; k < members.size(); ++k)
+              if (std::find(lgs[members[k]].in.begin(), lgs[members[k]].in.end(), members[i]) !=
+                  lgs[members[k]].in.end()) {
+                FusedOp cp;
+                cp.op = FOP_OR;
+                cp.dst = uint8_t(--saved_reg);
+                cp.a = cp.b = uint8_t(r);
+                cp.lo = cp.hi = 0;
+                fp.ops[fp.n_ops++] = cp;
+                fwd_[members[i]] = saved_reg;
+                break;
+              }
+          }
+          fwd_.clear();
           for (size_t z = 0; z < bin.size(); ++z) fp.bin[z] = bin[z];
           fp.n_bin = int(bin.size());
           for (size_t z = 0; z < uin.size(); ++z) fp.uin[z] = uin[z];
-          fp.out[0] = static_cast<uint32_t*>(n.ptr);
           launches += launch_fused(fp, gb, u16_geo(n.w, n.h, n.batch), st);
           break;
         }
