@@ -1022,12 +1022,24 @@ constexpr int SSLOTS = 128 * 128;
 
 size_t small_smem_bytes() { return size_t(SSLOTS) * 4 + 2 * ST_THREADS * 4 + 256 * STWW * 4 + 64; }
 
+// up to kSmallJobs independent same-shape problems in one launch (the program
+// batches independent reaches): CTA x = job * batch + slice
+constexpr int kSmallJobs = 4;
+struct SmallJobs {
+  const uint32_t* u[kSmallJobs];
+  const uint32_t* t[kSmallJobs];
+  uint32_t* out[kSmallJobs];
+  int batch;
+};
+
 // mode 0 = labels, 1 = reach, 2 = maxvol
 template <int MODE>
-__global__ void __launch_bounds__(ST_THREADS, 2) k_small(const uint32_t* __restrict__ ubits,
-                                                      const uint32_t* __restrict__ tbits,
-                                                      uint32_t* __restrict__ out, G g) {
+__global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G g) {
   slcs_pdl_wait();
+  const int job = int(blockIdx.x) / jobs.batch;
+  const uint32_t* __restrict__ ubits = jobs.u[job];
+  const uint32_t* __restrict__ tbits = jobs.t[job];
+  uint32_t* __restrict__ out = jobs.out[job];
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* par = reinterpret_cast<uint32_t*>(smem);  // SSLOTS
   uint32_t* sT = par + SSLOTS;                         // 1024
@@ -1035,7 +1047,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const uint32_t* __restr
   uint32_t* rows = sB + ST_THREADS;                    // 256 rows x 8 words
   __shared__ unsigned int s_max;
   using T = RunTile<SKW>;
-  const int slice = blockIdx.x;
+  const int slice = int(blockIdx.x) - job * jobs.batch;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const int u0 = threadIdx.x;
   const int band = u0 / STWW, w = u0 % STWW;
@@ -1186,16 +1198,26 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const uint32_t* __restr
 }
 
 template <int MODE>
-int small_launch(const uint32_t* u, const uint32_t* t, uint32_t* out, const G& g, int batch,
-                 cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+int small_launch_jobs(const SmallJobs& jobs, int n, const G& g, cudaStream_t st) {
+  static const bool attr_set = [] {
     cudaFuncSetAttribute(k_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(small_smem_bytes()));
-    attr_set = true;
-  }
-  pdl(k_small<MODE>, batch, ST_THREADS, small_smem_bytes(), st, u, t, out, g);
+    return true;
+  }();
+  (void)attr_set;
+  pdl(k_small<MODE>, n * jobs.batch, ST_THREADS, small_smem_bytes(), st, jobs, g);
   return 1;
+}
+
+template <int MODE>
+int small_launch(const uint32_t* u, const uint32_t* t, uint32_t* out, const G& g, int batch,
+                 cudaStream_t st) {
+  SmallJobs jobs{};
+  jobs.u[0] = u;
+  jobs.t[0] = t;
+  jobs.out[0] = out;
+  jobs.batch = batch;
+  return small_launch_jobs<MODE>(jobs, 1, g, st);
 }
 
 // ===========================================================================
@@ -1931,6 +1953,22 @@ bool fused_reach_enabled() {
     return !(e && *e && *e != '0');
   }();
   return on;
+}
+
+// n (<= 4) independent small-image reaches of one shape in one k_small launch
+int launch_reach_small_multi(const uint32_t* const* target, const uint32_t* const* through,
+                             uint32_t* const* out, int n, const Geo& gb, cudaStream_t st) {
+  if (!ccl_small_path(gb.w, gb.h) || n < 1 || n > kSmallJobs)
+    fail(SLCS_ERR_ARG, "reach: batched launch needs 1-4 small images");
+  G g = make_g(gb);
+  SmallJobs jobs{};
+  for (int i = 0; i < n; ++i) {
+    jobs.u[i] = through[i];
+    jobs.t[i] = target[i];
+    jobs.out[i] = out[i];
+  }
+  jobs.batch = gb.batch;
+  return small_launch_jobs<1>(jobs, n, g, st);
 }
 
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,

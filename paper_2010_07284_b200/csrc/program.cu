@@ -225,6 +225,7 @@ struct slcs_program {
   cudaGraphExec_t exec = nullptr;
   int launches_per_run = 0;
   std::string plan_text;
+  std::vector<int> exec_order;  // live steps in launch order (after reordering)
 
   ~slcs_program() { release_plan(); }
 
@@ -282,6 +283,20 @@ struct slcs_program {
     leaves(e, b, u);
     return exprs[e].ops + 2 <= kFusedMaxOps && exprs[e].need <= kFusedRegs &&
            int(b.size()) <= kFusedMaxIn && int(u.size()) <= kFusedMaxIn;
+  }
+
+  // the steps of the launch group led by `lead`, in launch order; `bad` when an
+  // input of any member has no storage
+  std::vector<int> group_members(int lead, bool& bad) const {
+    std::vector<int> m;
+    for (int q : exec_order)
+      if (q == lead || lgs[q].group == lead) {
+        if (q != lead && lgs[q].group != lead) continue;
+        for (int i : lgs[q].in)
+          if (!lgs[i].ptr) bad = true;
+        m.push_back(q);
+      }
+    return m;
   }
 
   // can these LG_EW steps (in order) run as one multi-output listing?
@@ -794,6 +809,59 @@ struct slcs_program {
     for (size_t q = 0; q < lgs.size(); ++q)
       if (!lgs[q].dead && lgs[q].kind != LG_INPUT) order.push_back(int(q));
 
+    // ---- reorder (list scheduling): among the ready steps, prefer one that can
+    // share a launch with the step just scheduled (an elementwise sibling, or an
+    // independent small reach of the same shape), else the earliest.  The
+    // reference runs independent nodes concurrently (executor.cpp:220, 259); here
+    // they share launches instead.
+    auto small_reach = [&](const LG& n) {
+      return n.kind == LG_REACH && n.gen_idx < 0 && n.k == 1 && n.tk == 0 &&
+             ccl_small_path(n.w, n.h);
+    };
+    auto joinable = [&](const LG& a, const LG& b) {
+      if (a.w != b.w || a.h != b.h || a.batch != b.batch) return false;
+      return (a.kind == LG_EW && b.kind == LG_EW) || (small_reach(a) && small_reach(b));
+    };
+    if (fuse && order.size() > 2) {
+      std::vector<char> done(lgs.size(), 0);
+      for (size_t q = 0; q < lgs.size(); ++q)
+        if (lgs[q].dead || lgs[q].kind == LG_INPUT) done[q] = 1;
+      // device numbers are dependencies too (volume -> arith / threshold(dev))
+      std::map<int, int> num_producer;
+      for (size_t q = 0; q < lgs.size(); ++q)
+        if (!lgs[q].dead && lgs[q].num_out >= 0) {
+          const int nslots = lgs[q].kind == LG_VOLUME ? lgs[q].batch : 1;
+          for (int z = 0; z < nslots; ++z) num_producer[lgs[q].num_out + z] = int(q);
+        }
+      auto num_ready = [&](int slot) {
+        if (slot < 0) return true;
+        auto it = num_producer.find(slot);
+        return it == num_producer.end() || done[it->second];
+      };
+      std::vector<int> sched;
+      std::vector<char> taken(order.size(), 0);
+      while (sched.size() < order.size()) {
+        int pick = -1;
+        for (size_t i = 0; i < order.size(); ++i) {
+          if (taken[i]) continue;
+          const LG& c = lgs[order[i]];
+          bool ready = num_ready(c.num_a) && num_ready(c.num_b);
+          for (int in : c.in) ready = ready && done[in];
+          if (!ready) continue;
+          if (pick < 0) pick = int(i);
+          if (!sched.empty() && joinable(lgs[sched.back()], lgs[order[i]])) {
+            pick = int(i);
+            break;
+          }
+        }
+        if (pick < 0) break;  // (cannot happen for a DAG) keep the original order
+        taken[pick] = 1;
+        done[order[pick]] = 1;
+        sched.push_back(order[pick]);
+      }
+      if (sched.size() == order.size()) order.swap(sched);
+    }
+
     // ---- sibling merge: adjacent elementwise steps of one shape run as one
     // multi-output listing (a u16 image thresholded twice is read once, and a
     // member that a later member reads is forwarded in a register)
@@ -813,6 +881,20 @@ struct slcs_program {
               grp.pop_back();
               break;
             }
+            ++j;
+          }
+          if (grp.size() > 1)
+            for (int q : grp) lgs[q].group = order[i];
+        } else if (small_reach(lead)) {
+          // independent small reaches of one shape: one k_small launch
+          std::vector<int> grp{order[i]};
+          while (j < order.size() && int(grp.size()) < 4 && small_reach(lgs[order[j]]) &&
+                 joinable(lead, lgs[order[j]])) {
+            bool dep = false;
+            for (int q : grp)
+              for (int in : lgs[order[j]].in) dep = dep || in == q;
+            if (dep) break;
+            grp.push_back(order[j]);
             ++j;
           }
           if (grp.size() > 1)
@@ -918,6 +1000,7 @@ struct slcs_program {
     }
     arena_bytes = top;
     scratch_bytes = scratch_need;
+    exec_order = order;
 
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (arena_bytes) cuda_check(cudaMalloc(&arena, arena_bytes), "program arena");
@@ -947,8 +1030,8 @@ struct slcs_program {
       os << "  step " << q << ": " << kn[n.kind];
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
-      if (n.kind == LG_EW && n.group >= 0)
-        os << (n.group == q ? " [sibling group lead]" : " [with step " + std::to_string(n.group) + "]");
+      if (n.group >= 0)
+        os << (n.group == q ? " [launch group lead]" : " [with step " + std::to_string(n.group) + "]");
       if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
       if (n.kind == LG_REACH && n.tk > 0) os << " target near^" << n.tk;
       if (n.kind == LG_REACH && n.k == 0) os << " emits selection";
@@ -1019,7 +1102,8 @@ struct slcs_program {
     int launches = 0;
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
     if (label_cse_used) launches += launch_epoch_bump(d_epoch, st);
-    for (size_t q = 0; q < lgs.size(); ++q) {
+    for (int qi : exec_order) {
+      const size_t q = size_t(qi);
       LG& n = lgs[q];
       if (n.dead || n.kind == LG_INPUT) continue;
       bool bad = false;
@@ -1030,14 +1114,7 @@ struct slcs_program {
       switch (n.kind) {
         case LG_EW: {
           if (n.group >= 0 && n.group != int(q)) break;  // emitted with its group lead
-          std::vector<int> members{int(q)};
-          if (n.group >= 0)
-            for (size_t z = q + 1; z < lgs.size(); ++z)
-              if (lgs[z].group == int(q)) {
-                for (int i : lgs[z].in)
-                  if (!lgs[i].ptr) bad = true;
-                members.push_back(int(z));
-              }
+          std::vector<int> members = group_members(int(q), bad);
           if (bad) break;
           FusedProgram fp;
           std::vector<const uint32_t*> bin;
@@ -1092,6 +1169,22 @@ struct slcs_program {
           break;
         }
         case LG_REACH: {
+          if (n.group >= 0) {  // a batch of independent small reaches
+            if (n.group != int(q)) break;
+            std::vector<int> members = group_members(int(q), bad);
+            if (bad) break;
+            const uint32_t* tg[4];
+            const uint32_t* th[4];
+            uint32_t* ou[4];
+            for (size_t i = 0; i < members.size(); ++i) {
+              const LG& m = lgs[members[i]];
+              tg[i] = static_cast<const uint32_t*>(lgs[m.in[0]].ptr);
+              th[i] = static_cast<const uint32_t*>(lgs[m.in[1]].ptr);
+              ou[i] = static_cast<uint32_t*>(m.ptr);
+            }
+            launches += launch_reach_small_multi(tg, th, ou, int(members.size()), gb, st);
+            break;
+          }
           if (n.gen_idx >= 0) {
             const LG& lab = lgs[n.in[2]];
             size_t lb = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256);

@@ -175,6 +175,9 @@ size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes);
 void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool sizes,
                        CclScratch* s);
 bool ccl_small_path(int w, int h);
+// n <= 4 independent reaches of one small shape (k_out 1, tk 0) in one launch
+int launch_reach_small_multi(const uint32_t* const* target, const uint32_t* const* through,
+                             uint32_t* const* out, int n, const Geo& gb, cudaStream_t st);
 // the tiled path's scratch regardless of size (row bands always use it)
 size_t ccl_scratch_bytes_large(int w, int h, int batch, bool flags, bool sizes);
 void ccl_scratch_carve_large(void* base, int w, int h, int batch, bool flags, bool sizes,
