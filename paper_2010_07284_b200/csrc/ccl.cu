@@ -1032,14 +1032,49 @@ struct SmallJobs {
   int batch;
 };
 
+// optional bool-only listings around a small-image kernel: the operand words
+// computed by `pro`, the result words passed through `epi` (FOP_PRESET = result)
+struct SmallListings {
+  FusedProgram pro, epi;
+  int has_pro = 0, has_epi = 0;
+};
+
+__device__ uint32_t eval_listing(const FusedProgram& p, size_t q, uint32_t vm, uint32_t preset) {
+  uint32_t R[kFusedRegs];
+  uint32_t res = 0;
+  for (int i = 0; i < p.n_ops; ++i) {
+    const FusedOp op = p.ops[i];
+    switch (op.op) {
+      case FOP_LOADB: R[op.dst] = __ldg(p.bin[op.a] + q); break;
+      case FOP_PRESET: R[op.dst] = preset; break;
+      case FOP_NOT: R[op.dst] = ~R[op.a] & vm; break;
+      case FOP_AND: R[op.dst] = R[op.a] & R[op.b]; break;
+      case FOP_OR: R[op.dst] = R[op.a] | R[op.b]; break;
+      case FOP_ANDNOT: R[op.dst] = R[op.a] & ~R[op.b]; break;
+      case FOP_STORE: res = R[op.dst]; break;
+      default: break;
+    }
+  }
+  return res;
+}
+
 // mode 0 = labels, 1 = reach, 2 = maxvol
 template <int MODE>
-__global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G g) {
+__global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G g,
+                                                      const SmallListings lst) {
   slcs_pdl_wait();
   const int job = int(blockIdx.x) / jobs.batch;
-  const uint32_t* __restrict__ ubits = jobs.u[job];
-  const uint32_t* __restrict__ tbits = jobs.t[job];
-  uint32_t* __restrict__ out = jobs.out[job];
+  // constant indices keep the job table in parameter space (no local copy)
+  const uint32_t* __restrict__ ubits = jobs.u[0];
+  const uint32_t* __restrict__ tbits = jobs.t[0];
+  uint32_t* __restrict__ out = jobs.out[0];
+#pragma unroll
+  for (int i = 1; i < kSmallJobs; ++i)
+    if (job == i) {
+      ubits = jobs.u[i];
+      tbits = jobs.t[i];
+      out = jobs.out[i];
+    }
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* par = reinterpret_cast<uint32_t*>(smem);  // SSLOTS
   uint32_t* sT = par + SSLOTS;                         // 1024
@@ -1053,8 +1088,22 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G
   const int band = u0 / STWW, w = u0 % STWW;
   const int r = 2 * band;
   const bool in = band < g.BH && w < g.wpr;
-  const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + w) : 0u;
-  const uint32_t Bw = (in && r + 1 < g.H) ? __ldg(u + size_t(r + 1) * g.pitch + w) : 0u;
+  const uint32_t vm = w + 1 < g.wpr ? FULL : (w + 1 == g.wpr && (g.W & 31)) ? (1u << (g.W & 31)) - 1u
+                                                                           : (w < g.wpr ? FULL : 0u);
+  const size_t q0 = size_t(slice) * g.slice + size_t(r) * g.pitch + w;
+  uint32_t Tw = 0, Bw = 0;
+  bool loaded = false;
+  if constexpr (MODE == 2) {
+    if (lst.has_pro) {
+      Tw = in ? eval_listing(lst.pro, q0, vm, 0u) : 0u;
+      Bw = (in && r + 1 < g.H) ? eval_listing(lst.pro, q0 + g.pitch, vm, 0u) : 0u;
+      loaded = true;
+    }
+  }
+  if (!loaded) {
+    Tw = in ? __ldg(u + size_t(r) * g.pitch + w) : 0u;
+    Bw = (in && r + 1 < g.H) ? __ldg(u + size_t(r + 1) * g.pitch + w) : 0u;
+  }
   sT[u0] = Tw;
   sB[u0] = Bw;
   if (threadIdx.x == 0) s_max = 0;
@@ -1190,6 +1239,10 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G
     uint32_t* o = out + size_t(slice) * g.slice;
     if (band < g.BH && w < int(g.pitch)) {
       // unit (band, w) owns both words; words >= wpr (padding) are zero
+      if (lst.has_epi) {
+        ST = eval_listing(lst.epi, q0, vm, ST);
+        if (r + 1 < g.H) SB = eval_listing(lst.epi, q0 + g.pitch, vm, SB);
+      }
       o[size_t(r) * g.pitch + w] = ST;
       if (r + 1 < g.H) o[size_t(r + 1) * g.pitch + w] = SB;
     }
@@ -1198,14 +1251,15 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G
 }
 
 template <int MODE>
-int small_launch_jobs(const SmallJobs& jobs, int n, const G& g, cudaStream_t st) {
+int small_launch_jobs(const SmallJobs& jobs, int n, const G& g, cudaStream_t st,
+                      const SmallListings& lst = SmallListings{}) {
   static const bool attr_set = [] {
     cudaFuncSetAttribute(k_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(small_smem_bytes()));
     return true;
   }();
   (void)attr_set;
-  pdl(k_small<MODE>, n * jobs.batch, ST_THREADS, small_smem_bytes(), st, jobs, g);
+  pdl(k_small<MODE>, n * jobs.batch, ST_THREADS, small_smem_bytes(), st, jobs, g, lst);
   return 1;
 }
 
@@ -1953,6 +2007,26 @@ bool fused_reach_enabled() {
     return !(e && *e && *e != '0');
   }();
   return on;
+}
+
+int launch_maxvol_small_listing(const FusedProgram* pro, const FusedProgram* epi,
+                                const uint32_t* bits, uint32_t* out, const Geo& gb,
+                                cudaStream_t st) {
+  if (!ccl_small_path(gb.w, gb.h)) fail(SLCS_ERR_ARG, "maxvol listings need a small image");
+  SmallListings lst;
+  if (pro) {
+    lst.pro = *pro;
+    lst.has_pro = 1;
+  }
+  if (epi) {
+    lst.epi = *epi;
+    lst.has_epi = 1;
+  }
+  SmallJobs jobs{};
+  jobs.u[0] = bits;
+  jobs.out[0] = out;
+  jobs.batch = gb.batch;
+  return small_launch_jobs<2>(jobs, 1, make_g(gb), st, lst);
 }
 
 // n (<= 4) independent small-image reaches of one shape in one k_small launch

@@ -100,7 +100,8 @@ struct LG {
   int gen_idx = -1;  // LG_REACH against an LG_LABELS input (label CSE)
   std::string name;  // LG_INPUT
   bool dead = false, output = false;
-  int group = -1;  // LG_EW: leader of its multi-output launch (sibling merge)
+  int group = -1;  // leader of its shared launch (EW siblings, batched small reaches)
+  int pro_expr = -1, epi_expr = -1, epi_src = -1;  // small maxvol: folded listings
   int consumers = 0, last_use = -1;
   size_t bytes = 0, offset = 0;
   void* ptr = nullptr;
@@ -297,6 +298,34 @@ struct slcs_program {
         m.push_back(q);
       }
     return m;
+  }
+
+  bool bool_only(int e) const {
+    const Expr& x = exprs[e];
+    if (x.k == E_THRESH) return false;
+    if (x.k == E_LEAF) return true;
+    return bool_only(x.a) && (x.b < 0 || bool_only(x.b));
+  }
+
+  // a one-output listing for a folded prologue/epilogue (preset_lg's value is
+  // the host kernel's own result word)
+  FusedProgram listing(int e, int preset_lg) {
+    FusedProgram fp;
+    std::vector<const uint32_t*> bin;
+    std::vector<const uint16_t*> uin;
+    fwd_.clear();
+    if (preset_lg >= 0) fwd_[preset_lg] = -1;
+    const int r = compile_expr(e, fp, bin, uin, 0);
+    fwd_.clear();
+    FusedOp st_op;
+    st_op.op = FOP_STORE;
+    st_op.dst = uint8_t(r);
+    st_op.a = st_op.b = 0;
+    st_op.lo = st_op.hi = 0;
+    fp.ops[fp.n_ops++] = st_op;
+    for (size_t z = 0; z < bin.size(); ++z) fp.bin[z] = bin[z];
+    fp.n_bin = int(bin.size());
+    return fp;
   }
 
   // can these LG_EW steps (in order) run as one multi-output listing?
@@ -805,6 +834,56 @@ struct slcs_program {
       }
     }
 
+    // ---- small-image maxvol absorbs a bool-only elementwise operand (prologue)
+    // and a bool-only elementwise consumer (epilogue): k_small evaluates them
+    // per word, so grow -> maxvol -> "| surrounded" (C3) is one launch
+    if (fuse) {
+      auto recount = [&] {
+        for (LG& n : lgs) n.consumers = 0;
+        for (const LG& n : lgs)
+          if (!n.dead)
+            for (int q : n.in) lgs[q].consumers++;
+      };
+      auto same_shape = [](const LG& a, const LG& b) {
+        return a.w == b.w && a.h == b.h && a.batch == b.batch;
+      };
+      recount();
+      for (LG& n : lgs) {
+        if (n.dead || n.kind != LG_MAXVOL || !ccl_small_path(n.w, n.h)) continue;
+        LG& m = lgs[n.in[0]];
+        if (m.kind == LG_EW && !m.dead && m.consumers == 1 && !m.output && bool_only(m.expr) &&
+            same_shape(m, n)) {
+          n.pro_expr = m.expr;
+          n.in = m.in;
+          m.dead = true;
+        }
+      }
+      recount();
+      for (size_t q = 0; q < lgs.size(); ++q) {
+        LG& e = lgs[q];
+        if (e.dead || e.kind != LG_EW || !bool_only(e.expr)) continue;
+        const std::vector<int> ins = e.in;  // e is overwritten below
+        for (int i : ins) {
+          LG& m = lgs[i];
+          if (m.kind != LG_MAXVOL || m.dead || m.consumers != 1 || m.output || m.epi_expr >= 0 ||
+              !ccl_small_path(m.w, m.h) || !same_shape(m, e))
+            continue;
+          // e becomes the maxvol step, its own expression the epilogue (values
+          // refer to e's index, so e keeps it)
+          LG nm = m;
+          nm.epi_expr = e.expr;
+          nm.epi_src = i;
+          nm.output = e.output;
+          for (int z : e.in)
+            if (z != i && std::find(nm.in.begin(), nm.in.end(), z) == nm.in.end())
+              nm.in.push_back(z);
+          m.dead = true;
+          e = nm;
+          break;
+        }
+      }
+    }
+
     std::vector<int> order;
     for (size_t q = 0; q < lgs.size(); ++q)
       if (!lgs[q].dead && lgs[q].kind != LG_INPUT) order.push_back(int(q));
@@ -1030,6 +1109,8 @@ struct slcs_program {
       os << "  step " << q << ": " << kn[n.kind];
       if (n.kind == LG_NEAR) os << (n.erode ? " interior" : " near") << "^" << n.k;
       if (n.kind == LG_EW) os << " (" << exprs[n.expr].ops << " ops)";
+      if (n.pro_expr >= 0) os << " +prologue(" << exprs[n.pro_expr].ops << " ops)";
+      if (n.epi_expr >= 0) os << " +epilogue(" << exprs[n.epi_expr].ops << " ops)";
       if (n.group >= 0)
         os << (n.group == q ? " [launch group lead]" : " [with step " + std::to_string(n.group) + "]");
       if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
@@ -1064,6 +1145,10 @@ struct slcs_program {
     switch (x.k) {
       case E_LEAF: {
         auto f = fwd_.find(x.lg);
+        if (f != fwd_.end() && f->second < 0) {  // the host kernel's result (epilogue)
+          add(FOP_PRESET, reg_base, 0, 0);
+          return reg_base;
+        }
         if (f != fwd_.end()) {  // a sibling computed earlier in this listing
           add(FOP_OR, reg_base, f->second, f->second);
           return reg_base;
@@ -1215,6 +1300,16 @@ struct slcs_program {
           break;
         }
         case LG_MAXVOL: {
+          if (n.pro_expr >= 0 || n.epi_expr >= 0) {
+            FusedProgram pro, epi;
+            if (n.pro_expr >= 0) pro = listing(n.pro_expr, -1);
+            if (n.epi_expr >= 0) epi = listing(n.epi_expr, n.epi_src);
+            launches += launch_maxvol_small_listing(
+                n.pro_expr >= 0 ? &pro : nullptr, n.epi_expr >= 0 ? &epi : nullptr,
+                n.pro_expr >= 0 ? nullptr : static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
+                static_cast<uint32_t*>(n.ptr), gb, st);
+            break;
+          }
           CclScratch cs;
           ccl_scratch_carve(scratch, n.w, n.h, n.batch, false, true, &cs);
           launches += launch_maxvol(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),

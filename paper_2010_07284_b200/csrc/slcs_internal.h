@@ -148,6 +148,7 @@ enum : uint8_t {
   FOP_OR = 4,
   FOP_ANDNOT = 5,  // r[a] & ~r[b]
   FOP_STORE = 6,   // output a = r[dst]
+  FOP_PRESET = 7,  // r[dst] = the host kernel's own result word (epilogues inside k_small)
 };
 constexpr int kFusedMaxOps = 24;
 constexpr int kFusedMaxIn = 8;
@@ -175,6 +176,12 @@ size_t ccl_scratch_bytes(int w, int h, int batch, bool flags, bool sizes);
 void ccl_scratch_carve(void* base, int w, int h, int batch, bool flags, bool sizes,
                        CclScratch* s);
 bool ccl_small_path(int w, int h);
+// small-image maxvol with an elementwise prologue (its operand computed from a
+// bool-only listing, `bits` unused) and/or epilogue (a listing over the maxvol
+// result, read as FOP_PRESET); either may be null
+int launch_maxvol_small_listing(const FusedProgram* pro, const FusedProgram* epi,
+                                const uint32_t* bits, uint32_t* out, const Geo& gb,
+                                cudaStream_t st);
 // n <= 4 independent reaches of one small shape (k_out 1, tk 0) in one launch
 int launch_reach_small_multi(const uint32_t* const* target, const uint32_t* const* through,
                              uint32_t* const* out, int n, const Geo& gb, cudaStream_t st);

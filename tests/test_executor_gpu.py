@@ -345,3 +345,30 @@ def test_components_saved_as_label_colours(dev, tmp_path):
     lab = O.flood_fill_label(O.threshold(0, img, 45000))
     want = np.array([[O.label_color(int(x)) for x in row] for row in lab], np.uint8)
     assert np.array_equal(np.array(Image.open(tmp_path / "lab.png").convert("RGB")), want)
+
+
+@pytest.mark.parametrize("fusion", [True, False])
+def test_small_maxvol_prologue_epilogue_folds(dev, fusion):
+    # the planner folds a bool-only operand listing (prologue) and a bool-only
+    # consumer listing (epilogue) into the small-image maxvol launch, and batches
+    # independent small reaches; results must not depend on it
+    rng = O.Rng(77)
+    n_sl, h, w = 5, 61, 97
+    a = np.stack([O.random_mask(w, h, 0.45, rng) for _ in range(n_sl)])
+    b = np.stack([O.random_mask(w, h, 0.3, rng) for _ in range(n_sl)])
+    cases = [
+        ("maxvol(a & !b) | b", lambda x, y: O.logical_or(O.maxvol(O.logical_and(x, O.logical_not(y))), y)),
+        ("!maxvol(a | b) & a", lambda x, y: O.logical_and(O.logical_not(O.maxvol(O.logical_or(x, y))), x)),
+        ("maxvol(maxvol(a) | b)", lambda x, y: O.maxvol(O.logical_or(O.maxvol(x), y))),
+        ("maxvol(a) | maxvol(b)", lambda x, y: O.logical_or(O.maxvol(x), O.maxvol(y))),
+        ("reach(a, b) | reach(b, a)", lambda x, y: O.logical_or(O.reach(x, y), O.reach(y, x))),
+    ]
+    for expr, ref in cases:
+        prog = Program(compile_text(f'load a = "a.png"\nload b = "b.png"\nsave "o.png" {expr}\n'))
+        prog.bind("a.png", a, PixelKind.Bool)
+        prog.bind("b.png", b, PixelKind.Bool)
+        prog.run(fusion=fusion)
+        got = np.zeros((n_sl, h, w), np.uint8)
+        prog.download(prog.graph.outputs[0], got)
+        for s in range(n_sl):
+            assert np.array_equal(got[s], ref(a[s], b[s])), (expr, s, prog.plan)
