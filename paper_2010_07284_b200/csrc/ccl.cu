@@ -1807,12 +1807,12 @@ size_t tile_smem() {
 template <int MODE>
 void tile_launch(dim3 grid, const uint32_t* u, const uint32_t* t, CclScratch& s, const G& g,
                  cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {  // thread-safe one-time initialisation
     cudaFuncSetAttribute(k_tile_local<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(tile_smem<MODE>()));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   pdl(k_tile_local<MODE>, grid, LT_THREADS, tile_smem<MODE>(), st, u, t, s.parent, s.flag, s.size,
                                                                  s.lists, g);
 }
