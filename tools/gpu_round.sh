@@ -21,4 +21,9 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --log-file $O/traffic_4096.csv timeout 600 python tools/prof_primitives.py --reps 2 --ops reach,near,threshold > /dev/null 2>&1
 echo "ncu traffic rc=$?"
 python tools/launches.py $O/launches_bench.csv $O/traffic_4096.csv
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $O/kernels_c4_16384.csv timeout 600 python tools/prof_primitives.py --size 16384 --random 0.5 \
+    --ops ccl,reach,maxvol --reps 2 > /dev/null 2>&1
+echo "ncu c4 rc=$?"
+python tools/launches.py $O/kernels_c4_16384.csv
 fi
