@@ -643,32 +643,47 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
 
 // After the merge: every listed local root points straight at its global
 // root and hands over its seed flag (reach) or pixel count (maxvol).  Then a
-// run's global root is exactly P[P[key block]].
-__global__ void k_root_flatten(uint32_t* P, uint8_t* F, uint32_t* SZ,
-                               const uint32_t* __restrict__ lists, G g, int ntiles, int mode) {
+// run's global root is exactly P[P[key block]].  One thread per list entry
+// (two 256-entry chunks per tile), so each SM keeps hundreds of independent
+// find chains in flight; the flag / size / max-key updates are aggregated per
+// warp over the lanes that found the same global root (inside a dense tile
+// most ring roots belong to one giant component, and one L2 atomic per warp
+// replaces up to 32 on the same address).
+__global__ void __launch_bounds__(256) k_root_flatten(uint32_t* P, uint8_t* F, uint32_t* SZ,
+                                                      const uint32_t* __restrict__ lists, G g,
+                                                      int ntiles, int mode) {
   slcs_pdl_wait();
   const int slice = blockIdx.y;
-  const int tile = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
+  const int tile = int(blockIdx.x >> 1);
   if (tile >= ntiles) return;
+  const int i = int((blockIdx.x & 1u) * 256u + threadIdx.x);
   uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t* L = lists + (size_t(slice) * ntiles + tile) * LT_LIST;
-  const int n = int(L[0]);
-  for (int i = lane; i < n; i += 32) {
-    const uint32_t rv = L[1 + i];
-    const uint32_t R = gfind_ro(Ps, g, rv);
-    if (R != rv) {
-      Ps[gblk(g, rv)] = R;
-      if (mode == MODE_REACH) {
-        uint8_t* Fs = F + size_t(slice) * g.sb;
-        if (Fs[gblk(g, rv)]) Fs[gblk(g, R)] = 1;
-      } else if (mode == MODE_SIZE) {
-        uint32_t* Ss = SZ + size_t(slice) * g.sb;
-        atomicAdd(Ss + gblk(g, R), Ss[gblk(g, rv)]);
-      } else if (SZ) {  // MODE_CCL: SZ holds the max key of each root (MK)
-        uint32_t* Ss = SZ + size_t(slice) * g.sb;
-        atomicMax(Ss + gblk(g, R), Ss[gblk(g, rv)]);
-      }
+  const int n = int(__ldg(L));
+  if ((blockIdx.x & 1u) * 256u >= uint32_t(n)) return;  // whole-CTA exit
+  const bool act = i < n;
+  const uint32_t rv = act ? __ldg(L + 1 + i) : 0u;
+  const uint32_t R = act ? gfind_ro(Ps, g, rv) : 0u;
+  const bool moved = act && R != rv;
+  if (moved) Ps[gblk(g, rv)] = R;
+  if (mode == MODE_CCL && !SZ) return;
+  const unsigned part = __ballot_sync(FULL, moved);
+  if (!moved) return;
+  const unsigned grp = __match_any_sync(part, R);
+  const bool leader = (threadIdx.x & 31) == __ffs(grp) - 1;
+  if (mode == MODE_REACH) {
+    uint8_t* Fs = F + size_t(slice) * g.sb;
+    const unsigned any = __ballot_sync(part, Fs[gblk(g, rv)] != 0) & grp;
+    if (leader && any) Fs[gblk(g, R)] = 1;
+  } else {
+    uint32_t* Ss = SZ + size_t(slice) * g.sb;
+    const uint32_t v = Ss[gblk(g, rv)];
+    if (mode == MODE_SIZE) {
+      const uint32_t sum = __reduce_add_sync(grp, v);
+      if (leader) atomicAdd(Ss + gblk(g, R), sum);
+    } else {  // MODE_CCL: SZ holds the max key of each root (MK)
+      const uint32_t mx = __reduce_max_sync(grp, v);
+      if (leader) atomicMax(Ss + gblk(g, R), mx);
     }
   }
 }
@@ -1835,7 +1850,7 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
     pdl(k_tile_merge, mg, 256, 0, st, u, s.parent, g, nhb, nvb);
     ++launches;
     const int ntiles = int(grid.x * grid.y);
-    dim3 fg(unsigned((ntiles * 32 + 255) / 256), unsigned(batch));
+    dim3 fg(unsigned(ntiles) * 2u, unsigned(batch));
     pdl(k_root_flatten, fg, 256, 0, st, s.parent, s.flag, s.size, s.lists, g, ntiles, mode);
     launches += 1;
   }
