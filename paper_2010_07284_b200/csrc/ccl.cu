@@ -307,14 +307,21 @@ struct RunTile {
       if (r[i] == node(key(band, w, T, B, m))) par[nslot(r[i])] = 0;
     }
     __syncthreads();
+    // consecutive runs of a word mostly share a root: one atomic per stretch
+    // of equal roots (inside a dense tile every run hits the same slot)
     x = T | B;
+    uint32_t cr = 0, ck = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (!x) break;
       const uint32_t m = first_run(x);
       x &= ~m;
-      atomicMax(par + nslot(r[i]), key(band, w, T, B, m));
+      const uint32_t k = key(band, w, T, B, m);
+      if (i > 0 && r[i] != cr) atomicMax(par + nslot(cr), ck);
+      ck = (i > 0 && r[i] == cr) ? max(ck, k) : k;
+      cr = r[i];
     }
+    if (T | B) atomicMax(par + nslot(cr), ck);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 16; ++i) mk[i] = par[nslot(r[i])];
@@ -455,8 +462,10 @@ __global__ void __launch_bounds__(LT_THREADS, 2048 / LT_THREADS) k_tile_local(co
   uint32_t* par = reinterpret_cast<uint32_t*>(lsm);           // LSLOTS
   uint32_t* sT = par + LSLOTS;                                 // LUNITS
   uint32_t* sB = sT + LUNITS;                                  // LUNITS
-  uint32_t* lsz = sB + LUNITS;                                 // LSLOTS (MODE_SIZE)
-  uint8_t* touch = reinterpret_cast<uint8_t*>(lsz + (MODE == MODE_SIZE ? LSLOTS : 0));
+  // MODE_SIZE: per-root pixel counts reuse the union-find slots once every
+  // run's root is in registers (keeps the tile at four CTAs per SM)
+  uint32_t* lsz = par;
+  uint8_t* touch = reinterpret_cast<uint8_t*>(sB + LUNITS);
   uint8_t* fl = touch + LSLOTS;                                // LSLOTS (MODE_REACH)
   __shared__ int s_cnt;
   using T = RunTile<LKW>;
@@ -482,8 +491,6 @@ __global__ void __launch_bounds__(LT_THREADS, 2048 / LT_THREADS) k_tile_local(co
     reinterpret_cast<uint32_t*>(touch)[q] = 0;
     if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
   }
-  if (MODE == MODE_SIZE)
-    for (int q = threadIdx.x; q < LSLOTS; q += blockDim.x) lsz[q] = 0;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   T tile{par, sT, sB};
@@ -491,12 +498,19 @@ __global__ void __launch_bounds__(LT_THREADS, 2048 / LT_THREADS) k_tile_local(co
   uint32_t rt[16];
   tile.roots(u0, Tw, Bw, rt);
   __syncthreads();
+  if (MODE == MODE_SIZE) {
+    for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x)
+      reinterpret_cast<uint4*>(lsz)[q] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+  }
 
   const int R0 = blockIdx.y * LTNB * 2, C0 = blockIdx.x * LTWW * 32;
   const uint32_t lmask = (1u << LKW) - 1u;
   uint32_t* Ps = P + size_t(slice) * g.sb;
   {
     uint32_t x = Tw | Bw;
+    int cs = -1;       // MODE_SIZE: the stretch of runs sharing root slot cs
+    uint32_t cn = 0;   // and its pixel count (one shared atomic per stretch)
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (!x) break;
@@ -511,9 +525,15 @@ __global__ void __launch_bounds__(LT_THREADS, 2048 / LT_THREADS) k_tile_local(co
         if (band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31)))
           touch[rs] = 1;
         if (MODE == MODE_REACH && (((Tw & ntT) | (Bw & ntB)) & m)) fl[rs] = 1;
-        if (MODE == MODE_SIZE) atomicAdd(lsz + rs, uint32_t(__popc(Tw & m) + __popc(Bw & m)));
+        if (MODE == MODE_SIZE) {
+          const uint32_t n = uint32_t(__popc(Tw & m) + __popc(Bw & m));
+          if (rs != cs && cs >= 0) atomicAdd(lsz + cs, cn);
+          cn = rs == cs ? cn + n : n;
+          cs = rs;
+        }
       }
     }
+    if (MODE == MODE_SIZE && cs >= 0) atomicAdd(lsz + cs, cn);
   }
   __syncthreads();
   uint32_t mk[16];  // MODE_CCL: component max keys (roots are hash-ordered)
@@ -1222,13 +1242,18 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G
   if (MODE == 2) {
     {
       uint32_t x = Tw | Bw;
+      uint32_t cr = 0, cn = 0;  // one shared atomic per stretch of runs sharing a root
 #pragma unroll
       for (int q = 0; q < 16; ++q)
         if (x) {
           const uint32_t m = first_run(x);
           x &= ~m;
-          atomicAdd(par + T::nslot(rt[q]), uint32_t(__popc(Tw & m) + __popc(Bw & m)));
+          const uint32_t n = uint32_t(__popc(Tw & m) + __popc(Bw & m));
+          if (q > 0 && rt[q] != cr) atomicAdd(par + T::nslot(cr), cn);
+          cn = (q > 0 && rt[q] == cr) ? cn + n : n;
+          cr = rt[q];
         }
+      if (Tw | Bw) atomicAdd(par + T::nslot(cr), cn);
     }
     __syncthreads();
     uint32_t best = 0;
@@ -1815,8 +1840,7 @@ void ccl_scratch_carve_large(void* base, int w, int h, int batch, bool flags, bo
 
 template <int MODE>
 size_t tile_smem() {
-  return size_t(LSLOTS) * 4 + 2 * size_t(LUNITS) * 4 + (MODE == MODE_SIZE ? size_t(LSLOTS) * 4 : 0) +
-         2 * size_t(LSLOTS) + 16;
+  return size_t(LSLOTS) * 4 + 2 * size_t(LUNITS) * 4 + 2 * size_t(LSLOTS) + 16;
 }
 
 template <int MODE>
