@@ -191,6 +191,19 @@ __device__ __forceinline__ void gunite_dedup(uint32_t* P, const G& g, uint32_t a
   if (la != lb) gunite(P, g, la, lb);
 }
 
+// gunite_dedup for a pair of already-looked-up ancestors (la, lb)
+__device__ __forceinline__ void unite_dedup_pair(uint32_t* P, const G& g, uint32_t la, uint32_t lb,
+                                                 bool active) {
+  const uint32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31;
+  const uint32_t plo = __shfl_up_sync(mask, lo, 1), phi = __shfl_up_sync(mask, hi, 1);
+  const bool prev_active = lane > 0 && ((mask >> (lane - 1)) & 1u);
+  if (!active) return;
+  if (prev_active && plo == lo && phi == hi) return;
+  if (la != lb) gunite(P, g, la, lb);
+}
+
 // read-only find (concurrent writers only ever store final roots)
 __device__ __forceinline__ uint32_t gfind_ro(const uint32_t* P, const G& g, uint32_t v) {
   uint32_t q = __ldcg(P + gblk(g, v));
@@ -604,35 +617,42 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
       if ((T & 1u) && !(Bu & 1u)) load_unit(u, g, k - 1, j - 1, Tl, Bl);
       if ((T >> 31) && !(Bu >> 31)) load_unit(u, g, k - 1, j + 1, Tr, Br);
       const uint32_t cu = Tu | Bu;
-      // the first link of every word goes through the warp dedupe (along a
-      // solid stretch of border all words link the same two local roots);
-      // any further links are united directly
+      // Links are made between the endpoints' current ancestors (their local
+      // roots after tile_local, or anything above them): along a tile border
+      // most links join the same two pieces (the giant component of the tiles
+      // above and below), so a lane skips a pair equal to the pair it linked
+      // last, and the first pair of every word goes through the warp dedupe.
       bool first = true;
-      uint32_t fa = 0, fb = 0;
+      uint32_t fa = 0, fb = 0, clo = 0, chi = 0;
       for (uint32_t x = T | B; x;) {
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t td = T & m;
         if (!td) continue;
-        const uint32_t v = grun(g, k, j, T, B, m);
+        const uint32_t la = __ldcg(Ps + gblk(g, grun(g, k, j, T, B, m)));
+        auto link = [&](uint32_t wnode) {
+          const uint32_t lb = __ldcg(Ps + gblk(g, wnode));
+          const uint32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
+          if (lo == hi || (lo == clo && hi == chi)) return;
+          clo = lo;
+          chi = hi;
+          if (first) {
+            fa = la;
+            fb = lb;
+            first = false;
+          } else {
+            gunite(Ps, g, la, lb);
+          }
+        };
         for (uint32_t a = dil1(td) & Bu; a;) {
           const uint32_t mu = run_at(cu, __ffs(a) - 1);
           a &= ~mu;
-          const uint32_t w = grun(g, k - 1, j, Tu, Bu, mu);
-          if (first) {
-            fa = v;
-            fb = w;
-            first = false;
-          } else {
-            gunite(Ps, g, v, w);
-          }
+          link(grun(g, k - 1, j, Tu, Bu, mu));
         }
-        if ((td & 1u) && (Bl >> 31))
-          gunite(Ps, g, v, grun(g, k - 1, j - 1, Tl, Bl, run_at(Tl | Bl, 31)));
-        if ((td >> 31) && (Br & 1u))
-          gunite(Ps, g, v, grun(g, k - 1, j + 1, Tr, Br, run_at(Tr | Br, 0)));
+        if ((td & 1u) && (Bl >> 31)) link(grun(g, k - 1, j - 1, Tl, Bl, run_at(Tl | Bl, 31)));
+        if ((td >> 31) && (Br & 1u)) link(grun(g, k - 1, j + 1, Tr, Br, run_at(Tr | Br, 0)));
       }
-      gunite_dedup(Ps, g, fa, fb, !first);
+      unite_dedup_pair(Ps, g, fa, fb, !first);
     } else {
       const uint32_t i2 = i - nA;
       const int t = int(i2 / uint32_t(g.BH)), k = int(i2 - uint32_t(t) * uint32_t(g.BH));
@@ -1867,7 +1887,12 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
   else
     tile_launch<MODE_CCL>(grid, u, t, s, g, st);
   ++launches;
-  const int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
+  int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
+  {  // diagnostics only (wrong labels): SLCS_MERGE_PART=H|V times one border kind
+    static const char* part = getenv("SLCS_MERGE_PART");
+    if (part && part[0] == 'H') nvb = 0;
+    if (part && part[0] == 'V') nhb = 0;
+  }
   const size_t links = size_t(nhb) * g.wpr + size_t(nvb) * g.BH;
   if (links) {
     dim3 mg(unsigned(grid_blocks(links, 256)), unsigned(batch));
