@@ -393,7 +393,7 @@ struct RunTile {
             have = true;
             fa = a;
             fb = b;
-          } else {
+          } else if (par[nslot(b)] != a) {  // b hangs under a already: same set
             a = unite(a, b);
           }
         };
