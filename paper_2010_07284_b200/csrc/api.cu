@@ -367,15 +367,16 @@ slcs_image* upload(slcs_ctx* ctx, int kind, int w, int h, int batch, const void*
       void* staging = ctx->alloc(npx * 2);
       cuda_check(cudaMemcpyAsync(staging, src, npx * 2, cudaMemcpyHostToDevice, ctx->stream),
                  "upload u16");
-      cuda_check(cudaMemcpy2DAsync(img.p->data, img.p->geo.pitch * 2, staging, size_t(w) * 2,
-                                   size_t(w) * 2, size_t(h) * size_t(batch),
-                                   cudaMemcpyDeviceToDevice, ctx->stream),
-                 "repitch u16");
+      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(staging), size_t(w),
+                                          static_cast<uint16_t*>(img.p->data), img.p->geo.pitch,
+                                          w, size_t(h) * size_t(batch), ctx->stream);
       ctx->release(staging);
+    } else if (img.p->geo.pitch != size_t(w)) {  // device source: repitch in place
+      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(src), size_t(w),
+                                          static_cast<uint16_t*>(img.p->data), img.p->geo.pitch,
+                                          w, size_t(h) * size_t(batch), ctx->stream);
     } else {
-      cuda_check(cudaMemcpy2DAsync(img.p->data, img.p->geo.pitch * 2, src, size_t(w) * 2,
-                                   size_t(w) * 2, size_t(h) * size_t(batch), dir, ctx->stream),
-                 "upload u16");
+      cuda_check(cudaMemcpyAsync(img.p->data, src, npx * 2, dir, ctx->stream), "upload u16");
     }
   } else {
     const void* dev = src;
@@ -405,9 +406,20 @@ void download(slcs_ctx* ctx, const slcs_image* img, void* dst, size_t bytes, boo
   if (img->kind == SLCS_LABEL) {
     cuda_check(cudaMemcpyAsync(dst, img->data, need, dir, ctx->stream), "download labels");
   } else if (img->kind == SLCS_U16) {
-    cuda_check(cudaMemcpy2DAsync(dst, size_t(g.w) * 2, img->data, g.pitch * 2, size_t(g.w) * 2,
-                                 size_t(g.h) * size_t(g.batch), dir, ctx->stream),
-               "download u16");
+    if (g.pitch == size_t(g.w)) {
+      cuda_check(cudaMemcpyAsync(dst, img->data, need, dir, ctx->stream), "download u16");
+    } else if (to_device) {
+      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(img->data), g.pitch,
+                                          static_cast<uint16_t*>(dst), size_t(g.w), g.w,
+                                          size_t(g.h) * size_t(g.batch), ctx->stream);
+    } else {  // dense on the device, then one D2H copy
+      void* staging = ctx->alloc(need);
+      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(img->data), g.pitch,
+                                          static_cast<uint16_t*>(staging), size_t(g.w), g.w,
+                                          size_t(g.h) * size_t(g.batch), ctx->stream);
+      cuda_check(cudaMemcpyAsync(dst, staging, need, dir, ctx->stream), "download u16");
+      ctx->release(staging);
+    }
   } else {
     if (to_device) {
       ctx->launches += launch_unpack(words(img), static_cast<uint8_t*>(dst), g, ctx->stream);

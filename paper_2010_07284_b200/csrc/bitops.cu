@@ -108,6 +108,21 @@ __global__ void k_unpack(const uint32_t* __restrict__ bits, uint8_t* __restrict_
   }
 }
 
+// u16 rows between two pitches (dense host layout <-> the padded device
+// layout), padding columns zeroed.  Replaces cudaMemcpy2D for short rows
+// (C3's 240-px slices: 37,200 rows of 480 B), which the copy engine moves
+// row by row.
+__global__ void k_repitch_u16(const uint16_t* __restrict__ src, size_t spitch,
+                              uint16_t* __restrict__ dst, size_t dpitch, int w, size_t total) {
+  slcs_pdl_wait();
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const size_t row = i / dpitch;
+    const int c = int(i - row * dpitch);
+    dst[i] = c < w ? __ldg(src + row * spitch + c) : uint16_t(0);
+  }
+}
+
 // threshold: one thread per output word; 4 x 16 B loads of u16 pixels.
 __global__ void k_threshold(const uint16_t* __restrict__ px, uint32_t* __restrict__ bits,
                             int wpr, uint32_t lastmask, size_t bpitch, size_t upitch,
@@ -732,6 +747,14 @@ int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool, cud
 int launch_pack_u16_mask(const uint16_t* dense, uint32_t* bits, const Geo& g, cudaStream_t st) {
   size_t n = g.slice * size_t(g.batch);
   pdl(k_pack_u16, grid_for(n, kThreads), kThreads, 0, st, dense, bits, g.w, g.wpr, g.pitch, n);
+  return 1;
+}
+
+int launch_repitch_u16(const uint16_t* src, size_t spitch, uint16_t* dst, size_t dpitch, int w,
+                       size_t rows, cudaStream_t st) {
+  const size_t total = dpitch * rows;
+  pdl(k_repitch_u16, grid_for(total, kThreads, 148 * 32), kThreads, 0, st, src, spitch, dst,
+      dpitch, w, total);
   return 1;
 }
 

@@ -1543,10 +1543,9 @@ int slcs_program_set_input_host(slcs_program* prog, const char* name, slcs_kind 
         prog->ensure_staging(dense);
         cuda_check(cudaMemcpyAsync(prog->staging, host, dense, cudaMemcpyHostToDevice, st),
                    "input upload");
-        cuda_check(cudaMemcpy2DAsync(s.data, s.geo.pitch * 2, prog->staging, size_t(w) * 2,
-                                     size_t(w) * 2, size_t(h) * size_t(batch),
-                                     cudaMemcpyDeviceToDevice, st),
-                   "input repitch");
+        prog->ctx->launches += launch_repitch_u16(
+            static_cast<const uint16_t*>(prog->staging), size_t(w), static_cast<uint16_t*>(s.data),
+            s.geo.pitch, w, size_t(h) * size_t(batch), st);
       }
     } else if (kind == SLCS_LABEL) {
       cuda_check(cudaMemcpyAsync(s.data, host, size_t(w) * h * batch * 4, cudaMemcpyHostToDevice,
@@ -1596,9 +1595,15 @@ int slcs_program_download(slcs_program* prog, int task, void* host, size_t bytes
     } else if (v.type == VT_U16) {
       if (bytes < npx * 2) fail(SLCS_ERR_ARG, "buffer too small");
       Geo g = u16_geo(n.w, n.h, n.batch);
-      cuda_check(cudaMemcpy2DAsync(host, size_t(n.w) * 2, n.ptr, g.pitch * 2, size_t(n.w) * 2,
-                                   size_t(n.h) * n.batch, cudaMemcpyDeviceToHost, st),
-                 "d2h");
+      const void* src = n.ptr;
+      if (g.pitch != size_t(n.w)) {  // dense on the device first: one D2H copy
+        prog->ensure_staging(npx * 2);
+        prog->ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(n.ptr), g.pitch,
+                                                  static_cast<uint16_t*>(prog->staging),
+                                                  size_t(n.w), n.w, size_t(n.h) * n.batch, st);
+        src = prog->staging;
+      }
+      cuda_check(cudaMemcpyAsync(host, src, npx * 2, cudaMemcpyDeviceToHost, st), "d2h");
     } else {
       if (bytes < npx * 4) fail(SLCS_ERR_ARG, "buffer too small");
       cuda_check(cudaMemcpyAsync(host, n.ptr, npx * 4, cudaMemcpyDeviceToHost, st), "d2h");

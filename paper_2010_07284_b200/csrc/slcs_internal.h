@@ -111,6 +111,9 @@ KeyGeo key_geo(int w, int h);
 int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool nonzero_is_true,
                    cudaStream_t st);
 int launch_unpack(const uint32_t* bits, uint8_t* dense, const Geo& g, cudaStream_t st);
+// u16 rows from pitch spitch to pitch dpitch (pixels), columns >= w of dst zeroed
+int launch_repitch_u16(const uint16_t* src, size_t spitch, uint16_t* dst, size_t dpitch, int w,
+                       size_t rows, cudaStream_t st);
 // interval threshold: bit = lo <= p <= hi (empty interval when lo > hi)
 int launch_threshold(const uint16_t* px, uint32_t* bits, const Geo& gu, const Geo& gb, int lo,
                      int hi, cudaStream_t st);
