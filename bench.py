@@ -519,6 +519,41 @@ def c4_config(args, ws, rank, local):
             trs.append(ev[2].elapsed_time(ev[3]))
         sweep[str(dens)] = {"ccl_ms": sum(tcs) / len(tcs), "reach_ms": sum(trs) / len(trs)}
         del m2
+    # e2e through the reference-facing host wrappers (kernels/ccl/reach signatures,
+    # slcs_h_*): pinned 1 B/px masks in, u32 labels and 1 B/px reach result out
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+
+        from paper_2010_07284_b200 import _lib
+        from paper_2010_07284_b200.pixlog import _check as _check_rc
+        L = _lib.load()
+        pin_m = torch.empty((n, n), dtype=torch.uint8).pin_memory()
+        pin_t = torch.empty((n, n), dtype=torch.uint8).pin_memory()
+        pin_lab = torch.empty((n, n), dtype=torch.int32).pin_memory()
+        pin_r = torch.empty((n, n), dtype=torch.uint8).pin_memory()
+        pin_m.copy_(torch.from_numpy(mask.numpy()))
+        pin_t.copy_(torch.from_numpy(target.numpy()))
+
+        def e2e_step():
+            _check_rc(L.slcs_h_ccl_label(dev.handle, C.c_void_p(pin_m.data_ptr()), n, n,
+                                         C.c_void_p(pin_lab.data_ptr())))
+            _check_rc(L.slcs_h_reach(dev.handle, C.c_void_p(pin_t.data_ptr()),
+                                     C.c_void_p(pin_m.data_ptr()), n, n,
+                                     C.c_void_p(pin_r.data_ptr())))
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": 2 * px / e2e_s / 1e9, "unit": "Gpixel-ops/s",
+               "h2d_bytes_per_step": 3 * px, "d2h_bytes_per_step": 5 * px,
+               "ms_per_step": e2e_s * 1e3,
+               "timing": "host wall clock, synced (slcs_h_ccl_label + slcs_h_reach)"}
+        del pin_m, pin_t, pin_lab, pin_r
     peak, pk = measured_peak_gbs()
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -558,7 +593,7 @@ def c4_config(args, ws, rank, local):
                          "achieved": 4.125 * px / tc / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": 4.125 * px / tc / 1e9 / peak, "traffic": ccl_traffic,
                          "traffic_source": ccl_src, "peak_source": pk},
-            "cpu_baseline": cpu}), flush=True)
+            "e2e": e2e, "cpu_baseline": cpu}), flush=True)
 
 
 def c5_config(args, ws, rank, local):
