@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libslcs.so")
+# SLCS_LIB_PATH: an alternative build of the same sources (A/B measurements only)
+LIB_PATH = os.environ.get("SLCS_LIB_PATH") or os.path.join(HERE, "libslcs.so")
 HEADER = os.path.join(HERE, "..", "include", "slcs.h")
 
 _lib = None

@@ -463,8 +463,11 @@ enum { MODE_CCL = 0, MODE_REACH = 1, MODE_SIZE = 2 };
 // F = "holds a seed" (reach) or SZ = local pixel count (maxvol).  Per tile:
 // the local roots touching the tile ring -- the only ones a border union can
 // link, hence the only ones root_flatten visits.
+#ifndef SLCS_TL_MINB
+#define SLCS_TL_MINB (2048 / LT_THREADS)
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(LT_THREADS, 2048 / LT_THREADS) k_tile_local(const uint32_t* __restrict__ ubits,
+__global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const uint32_t* __restrict__ ubits,
                                                            const uint32_t* __restrict__ tbits,
                                                            uint32_t* __restrict__ P,
                                                            uint8_t* __restrict__ F,
