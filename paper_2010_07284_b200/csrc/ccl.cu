@@ -34,6 +34,10 @@
 #include <vector>
 namespace cg = cooperative_groups;
 
+#ifndef SLCS_TL_HINTS
+#define SLCS_TL_HINTS 1
+#endif
+
 namespace slcs {
 
 KeyGeo key_geo(int w, int h) {
@@ -424,7 +428,11 @@ struct RunTile {
       const uint32_t plo = __shfl_up_sync(0xffffffffu, lo, 1);
       const uint32_t phi = __shfl_up_sync(0xffffffffu, hi, 1);
       const bool phave = __shfl_up_sync(0xffffffffu, have ? 1u : 0u, 1) != 0u;
+#if SLCS_TL_HINTS
+      if (have && lo != hi && !(lane > 0 && phave && plo == lo && phi == hi)) unite(fa, fb);
+#else
       if (have && !(lane > 0 && phave && plo == lo && phi == hi)) unite(fa, fb);
+#endif
     }
     __syncwarp();
     __syncthreads();
@@ -437,6 +445,21 @@ struct RunTile {
     uint32_t x = T | B;
 #pragma unroll
     for (int i = 0; i < 16; ++i) r[i] = 0;
+#if SLCS_TL_HINTS
+    // no unions are in flight: a run whose parent is the previous run's root
+    // (or itself) needs no find
+    uint32_t last = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (!x) break;
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      const uint32_t v = rnode(band, w, T, B, m);
+      const uint32_t p = static_cast<volatile uint32_t*>(par)[nslot(v)];
+      last = (p == v || p == last) ? p : find(p);
+      r[i] = last;
+    }
+#else
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (!x) break;
@@ -444,6 +467,7 @@ struct RunTile {
       x &= ~m;
       r[i] = find(rnode(band, w, T, B, m));
     }
+#endif
   }
 };
 
