@@ -34,6 +34,9 @@
 #include <vector>
 namespace cg = cooperative_groups;
 
+#ifndef SLCS_COOP_PDL
+#define SLCS_COOP_PDL 2
+#endif
 #ifndef SLCS_TL_HINTS
 #define SLCS_TL_HINTS 1
 #endif
@@ -1472,7 +1475,7 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
                                                                uint32_t* P, uint32_t* GP,
                                                                uint32_t* sel,
                                                                uint32_t* __restrict__ out, G g,
-                                                               long long* tstamp) {
+                                                               long long* tstamp, int early) {
   cg::grid_group grid = cg::this_grid();
   // diagnostics (SLCS_PHASE_TIMING=1): per-CTA %globaltimer (ns) at phase boundaries
   int tsn = 0;
@@ -1520,19 +1523,71 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   const bool two = r + 1 < g.H;
   const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
   const uint32_t Bw = (in && two) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
-  // target window: rows R0-TH .. R0+2NB+TH-1, columns j0-1 .. j0+8 (halo words by
-  // threads < 20TH + 4NB).  With TK > 0 the window holds the operand before its
-  // folded nears and tbits may be written by the previous kernel of a chain.
-  tw[(r - R0 + TH) * 10 + w + 1] = word_or0(t, g, r, j, false);
-  tw[(r - R0 + TH + 1) * 10 + w + 1] = word_or0(t, g, r + 1, j, false);
-  if (u0 < 20 * TH) {
-    const int q = u0 % (10 * TH);
-    const int hr = u0 < 10 * TH ? R0 - TH + q / 10 : R0 + 2 * NB + q / 10;
-    tw[(hr - R0 + TH) * 10 + q % 10] = word_or0(t, g, hr, j0 - 1 + q % 10, false);
-  } else if (u0 < 20 * TH + 4 * NB) {
-    const int q = u0 - 20 * TH, side = q / (2 * NB), hr = R0 + q % (2 * NB);
-    tw[(hr - R0 + TH) * 10 + (side ? 9 : 0)] = word_or0(t, g, hr, side ? j0 + 8 : j0 - 1, false);
-  }
+#if !SLCS_COOP_PDL
+  (void)early;
+#else
+  // Programmatic dependent launch: when `through` was not written by the
+  // previous launch (early), everything up to the flattened tile union-find
+  // reads only `through` and shared memory, so it runs while the previous
+  // kernel drains; the target window and all scratch writes wait for it.
+  if (!early) slcs_pdl_wait();
+#endif
+  uint32_t tT, tB, seedT, seedB;
+  auto stage_target = [&]() {
+    // target window: rows R0-TH .. R0+2NB+TH-1, columns j0-1 .. j0+8 (halo words by
+    // threads < 20TH + 4NB).  With TK > 0 the window holds the operand before its
+    // folded nears and tbits may be written by the previous kernel of a chain.
+    tw[(r - R0 + TH) * 10 + w + 1] = word_or0(t, g, r, j, false);
+    tw[(r - R0 + TH + 1) * 10 + w + 1] = word_or0(t, g, r + 1, j, false);
+    if (u0 < 20 * TH) {
+      const int q = u0 % (10 * TH);
+      const int hr = u0 < 10 * TH ? R0 - TH + q / 10 : R0 + 2 * NB + q / 10;
+      tw[(hr - R0 + TH) * 10 + q % 10] = word_or0(t, g, hr, j0 - 1 + q % 10, false);
+    } else if (u0 < 20 * TH + 4 * NB) {
+      const int q = u0 - 20 * TH, side = q / (2 * NB), hr = R0 + q % (2 * NB);
+      tw[(hr - R0 + TH) * 10 + (side ? 9 : 0)] = word_or0(t, g, hr, side ? j0 + 8 : j0 - 1, false);
+    }
+  };
+  auto seeds = [&]() {
+    // the target operand t = near^TK(window) at this unit's two words, and the
+    // seeds through & near(t) = through & near^(TK+1)(window).  The box stencil is
+    // separable: vertical ORs of the (L, C, R) column words first (shared by the
+    // two rows and by both radii), then one horizontal pass per result.
+    {
+      const int base = r - R0;  // window row of r - TH
+      uint3 rows[2 * TH + 2];
+#pragma unroll
+      for (int i = 0; i < 2 * TH + 2; ++i) {
+        const uint32_t* wr = tw + (base + i) * 10 + w;
+        rows[i] = make_uint3(wr[0], wr[1], wr[2]);
+      }
+      auto orv = [](uint3 a, uint3 b) { return make_uint3(a.x | b.x, a.y | b.y, a.z | b.z); };
+      auto hdil = [](uint3 v, int k) {
+        uint32_t acc = v.y;
+#pragma unroll
+        for (int e = 1; e <= TH; ++e)
+          if (e <= k) acc |= __funnelshift_l(v.x, v.y, e) | __funnelshift_r(v.y, v.z, e);
+        return acc;
+      };
+      // rows[TH] is row r, rows[TH + 1] is row r + 1
+      uint3 inner = rows[TH];  // rows r - TK + 1 .. r + TK (shared core of both rows)
+#pragma unroll
+      for (int d = 1; d < TK; ++d) inner = orv(inner, orv(rows[TH - d], rows[TH + d]));
+      if (TK > 0) inner = orv(inner, rows[TH + TK]);
+      // row r: rows r-TK .. r+TK; row r+1: rows r-TK+1 .. r+TK+1
+      const uint3 vT = TK > 0 ? orv(inner, rows[TH - TK]) : rows[TH];
+      const uint3 vB = TK > 0 ? orv(inner, rows[TH + TK + 1]) : rows[TH + 1];
+      tT = TK > 0 ? hdil(vT, TK) : rows[TH].y;
+      tB = TK > 0 ? hdil(vB, TK) : rows[TH + 1].y;
+      const uint3 sTv = orv(orv(vT, rows[TH - TK - 1]), rows[TH + TK + 1]);
+      const uint3 sBv = orv(orv(vB, rows[TH - TK]), rows[2 * TH + 1]);  // rows r-TK .. r+TK+2
+      seedT = Tw & hdil(sTv, TK + 1);
+      seedB = Bw & hdil(sBv, TK + 1);
+    }
+  };
+#if !SLCS_COOP_PDL
+  stage_target();
+#endif
   if (u0 < NB) {  // inputs only: safe to read before any barrier
     uint32_t a = 0, b = 0;
     if (blockIdx.x > 0) load_unit(u, g, blockIdx.y * NB + u0, j0 - 1, a, b);
@@ -1548,42 +1603,9 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   sB[u0] = Bw;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
-  // the target operand t = near^TK(window) at this unit's two words, and the
-  // seeds through & near(t) = through & near^(TK+1)(window).  The box stencil is
-  // separable: vertical ORs of the (L, C, R) column words first (shared by the
-  // two rows and by both radii), then one horizontal pass per result.
-  uint32_t tT, tB, seedT, seedB;
-  {
-    const int base = r - R0;  // window row of r - TH
-    uint3 rows[2 * TH + 2];
-#pragma unroll
-    for (int i = 0; i < 2 * TH + 2; ++i) {
-      const uint32_t* wr = tw + (base + i) * 10 + w;
-      rows[i] = make_uint3(wr[0], wr[1], wr[2]);
-    }
-    auto orv = [](uint3 a, uint3 b) { return make_uint3(a.x | b.x, a.y | b.y, a.z | b.z); };
-    auto hdil = [](uint3 v, int k) {
-      uint32_t acc = v.y;
-#pragma unroll
-      for (int e = 1; e <= TH; ++e)
-        if (e <= k) acc |= __funnelshift_l(v.x, v.y, e) | __funnelshift_r(v.y, v.z, e);
-      return acc;
-    };
-    // rows[TH] is row r, rows[TH + 1] is row r + 1
-    uint3 inner = rows[TH];  // rows r - TK + 1 .. r + TK (shared core of both rows)
-#pragma unroll
-    for (int d = 1; d < TK; ++d) inner = orv(inner, orv(rows[TH - d], rows[TH + d]));
-    if (TK > 0) inner = orv(inner, rows[TH + TK]);
-    // row r: rows r-TK .. r+TK; row r+1: rows r-TK+1 .. r+TK+1
-    const uint3 vT = TK > 0 ? orv(inner, rows[TH - TK]) : rows[TH];
-    const uint3 vB = TK > 0 ? orv(inner, rows[TH + TK + 1]) : rows[TH + 1];
-    tT = TK > 0 ? hdil(vT, TK) : rows[TH].y;
-    tB = TK > 0 ? hdil(vB, TK) : rows[TH + 1].y;
-    const uint3 sTv = orv(orv(vT, rows[TH - TK - 1]), rows[TH + TK + 1]);
-    const uint3 sBv = orv(orv(vB, rows[TH - TK]), rows[2 * TH + 1]);  // rows r-TK .. r+TK+2
-    seedT = Tw & hdil(sTv, TK + 1);
-    seedB = Bw & hdil(sBv, TK + 1);
-  }
+#if !SLCS_COOP_PDL
+  seeds();
+#endif
   stamp();  // 1: loads
   T tile{par, sT, sB};
   tile.link(u0, Tw, Bw);
@@ -1604,6 +1626,12 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
       par[T::slot(k)] = rt[i] == T::node(k) ? REC_ROOT : uint32_t(T::nslot(rt[i]));
     }
   }
+#if SLCS_COOP_PDL
+  if (early) slcs_pdl_wait();
+  stage_target();
+  __syncthreads();
+  seeds();
+#endif
   __syncthreads();
   stamp();  // 3: roots
   auto root_of = [&](uint32_t k) {  // the root's slot
@@ -1720,6 +1748,13 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();  // 6: merge
   grid.sync();
   stamp();  // 7: barrier
+#if SLCS_COOP_PDL == 2
+  // the next launch may start its through-only prologue on free SM slots.  Only
+  // after this grid's last grid.sync: a cooperative launch re-arms the grid
+  // barrier, so an earlier trigger breaks this grid's remaining barriers
+  // (measured: triggering after the first barrier corrupts chained reaches)
+  if (KOUT == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 
   // ---- C: resolve this tile's ring roots (read-only finds), then select
   if (u0 < s_cnt) {
@@ -1765,6 +1800,9 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();  // 9: select
   grid.sync();
   stamp();  // 10: barrier
+#if SLCS_COOP_PDL == 2
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the last grid.sync
+#endif
 
   // ---- D: closing near^KOUT; halo from the neighbours' selections
   constexpr int KO = KOUT > 0 ? KOUT : 1;  // (KOUT == 0 returned above)
@@ -2017,7 +2055,8 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
 
 template <int KOUT, int NB, int TK>
 bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* out,
-                     uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st) {
+                     uint32_t* tmp_bits, const G& g, int batch, CclScratch& s, cudaStream_t st,
+                     bool early) {
   constexpr int THREADS = NB * LTWW;
   constexpr size_t smem = size_t(NB) * (1 << (LKW - 1)) * 4 + 2 * size_t(THREADS) * 4 +
                           size_t(2 * NB + 2 * (TK + 1)) * 40 +
@@ -2046,11 +2085,13 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (SLCS_COOP_PDL && pdl_enabled()) ? 2 : 1;
   static const bool timing = [] {
     const char* e = std::getenv("SLCS_PHASE_TIMING");
     return e && *e == '1';
@@ -2058,7 +2099,7 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
   long long* ts = nullptr;
   if (timing) cuda_check(cudaMalloc(&ts, tiles * 16 * sizeof(long long)), "timing buffer");
   cuda_check(cudaLaunchKernelEx(&cfg, k_reach_fused<KOUT, NB, TK>, through, target, s.parent, GP,
-                                tmp_bits, out, g, ts),
+                                tmp_bits, out, g, ts, early ? 1 : 0),
              "fused reach launch");
   if (timing) {  // diagnostics only: timeline of phase ends, min/max over CTAs (us)
     std::vector<long long> h(tiles * 16);
@@ -2138,7 +2179,7 @@ int launch_reach_small_multi(const uint32_t* const* target, const uint32_t* cons
 
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
                  uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st, int k_out,
-                 int tk) {
+                 int tk, bool early_through) {
   G g = make_g(gb);
   if (ccl_small_path(gb.w, gb.h)) {
     if (k_out != 1 || tk != 0)
@@ -2156,7 +2197,8 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
     bool done = false;
 #define SLCS_FUSED(KO, NBV, TKV)                                                                \
   case (KO) * 10000 + (NBV) * 10 + (TKV):                                                      \
-    done = reach_fused_try<KO, NBV, TKV>(target, through, out, tmp_bits, g, gb.batch, s, st); \
+    done = reach_fused_try<KO, NBV, TKV>(target, through, out, tmp_bits, g, gb.batch, s, st,  \
+                                         early_through);                                       \
     break;
     switch (k_out * 10000 + nb * 10 + tk) {
       SLCS_FUSED(0, 64, 0) SLCS_FUSED(0, 64, 1) SLCS_FUSED(0, 64, 2)

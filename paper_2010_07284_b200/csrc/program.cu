@@ -1187,10 +1187,16 @@ struct slcs_program {
     int launches = 0;
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
     if (label_cse_used) launches += launch_epoch_bump(d_epoch, st);
+    // `through` of the reach launched just before (null after any other step):
+    // a reach on the same `through` may read it before its launch dependency
+    const void* prev_through = nullptr;
     for (int qi : exec_order) {
       const size_t q = size_t(qi);
       LG& n = lgs[q];
       if (n.dead || n.kind == LG_INPUT) continue;
+      const void* cur_through = n.kind == LG_REACH && n.in.size() > 1 ? lgs[n.in[1]].ptr : nullptr;
+      const bool early_through = cur_through && cur_through == prev_through;
+      prev_through = cur_through;
       bool bad = false;
       for (int i : n.in)
         if (!lgs[i].ptr) bad = true;
@@ -1289,7 +1295,8 @@ struct slcs_program {
                               : reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + sb);
           launches += launch_reach(static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
                                    static_cast<const uint32_t*>(lgs[n.in[1]].ptr),
-                                   static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st, n.k, n.tk);
+                                   static_cast<uint32_t*>(n.ptr), tmp, gb, cs, st, n.k, n.tk,
+                                   early_through);
           break;
         }
         case LG_CCL: {

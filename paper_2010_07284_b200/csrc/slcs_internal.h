@@ -199,7 +199,9 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
 // tk: the target operand is near^tk(target) (nears folded into the reach).
 int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
                  uint32_t* tmp_bits, const Geo& gb, CclScratch& s, cudaStream_t st,
-                 int k_out = 1, int tk = 0);
+                 int k_out = 1, int tk = 0, bool early_through = false);
+// early_through: `through` was not written by the launch just before this one
+// (the fused kernel may then read it before its programmatic-launch wait)
 int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
                   cudaStream_t st);
 // row bands: reach in phases (large path always)

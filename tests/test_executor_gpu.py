@@ -282,6 +282,11 @@ CHAIN_SHAPES = [
     "reach(near(near(near(a))), b)",                      # tk 3: beyond the fused window
     "reach(reach(a, b), reach(a, b))",                    # shared reach: no selection emit
     "near(reach(a, b)) | reach(near(a), b)",              # two consumers of near(a)
+    # a reach with a closing near (k_out >= 1, three grid barriers) launched right
+    # before another reach on the same `through` (early launch of the second)
+    "reach(reach(a, b), b) | reach(a, b)",
+    "near(reach(reach(a, b), b)) & near(reach(a, b))",
+    "reach(reach(reach(a, b), b) | a, b)",
 ]
 
 
