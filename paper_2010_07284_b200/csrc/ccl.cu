@@ -955,7 +955,10 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
 // output row cooperatively -- lane l stores pixels 4l..4l+3 of every 128-px
 // stretch, so each warp store is 512 contiguous bytes (the label image is the
 // 4 B/px bulk of the CCL traffic).
-constexpr int TL_WARPS = 8;
+#ifndef SLCS_TL_WARPS
+#define SLCS_TL_WARPS 8
+#endif
+constexpr int TL_WARPS = SLCS_TL_WARPS;
 __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* __restrict__ ubits,
                                                              const uint32_t* __restrict__ P,
                                                              const uint32_t* __restrict__ MKall,
