@@ -624,9 +624,15 @@ void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st
         nstrips);
   } else {
     // long strips amortise the 2K halo rows; short images keep >= ~2 waves
-    constexpr int P = 4;
+#ifndef SLCS_NS_P
+#define SLCS_NS_P 4
+#endif
+    constexpr int P = SLCS_NS_P;
     int S = 32;
     if (size_t(pitch4) * size_t((g.h + S - 1) / S) * g.batch < 148u * 512u) S = 16;
+#ifdef SLCS_NS_S
+    S = SLCS_NS_S;
+#endif
     const int nstrips = (g.h + S - 1) / S;
     const size_t threads = size_t(pitch4) * size_t(nstrips);
     dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
