@@ -1016,10 +1016,14 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
           const size_t p = size_t(it) * 128 + size_t(lane) * 4;
           if (c0 + p < size_t(g.W)) {
             uint32_t v[4];
+            // run index of pixel x0 (runs starting at or before it, minus one), then
+            // advanced by the run starts at x0+1 .. x0+3
+            const uint32_t sb = ws >> x0, pb = wb >> x0;
+            const uint32_t* trow = tb + wi * 17 + __popc(ws & ((2u << x0) - 1u)) - 1;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const int x = x0 + e;
-              v[e] = ((wb >> x) & 1u) ? tb[wi * 17 + __popc(ws & ((2u << x) - 1u)) - 1] : 0u;
+              if (e > 0) trow += (sb >> e) & 1u;
+              v[e] = ((pb >> e) & 1u) ? *trow : 0u;
             }
             *reinterpret_cast<uint4*>(dst + p) = make_uint4(v[0], v[1], v[2], v[3]);
           }
