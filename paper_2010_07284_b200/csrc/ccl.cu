@@ -1959,12 +1959,7 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
   else
     tile_launch<MODE_CCL>(grid, u, t, s, g, st);
   ++launches;
-  int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
-  {  // diagnostics only (wrong labels): SLCS_MERGE_PART=H|V times one border kind
-    static const char* part = getenv("SLCS_MERGE_PART");
-    if (part && part[0] == 'H') nvb = 0;
-    if (part && part[0] == 'V') nhb = 0;
-  }
+  const int nhb = int(grid.y) - 1, nvb = int(grid.x) - 1;
   const size_t links = size_t(nhb) * g.wpr + size_t(nvb) * g.BH;
   if (links) {
     dim3 mg(unsigned(grid_blocks(links, 256)), unsigned(batch));
