@@ -37,6 +37,12 @@ namespace cg = cooperative_groups;
 #ifndef SLCS_COOP_PDL
 #define SLCS_COOP_PDL 2
 #endif
+#ifndef SLCS_FUSED_QUEUE
+#define SLCS_FUSED_QUEUE 0
+#endif
+#ifndef SLCS_TL_QUEUE
+#define SLCS_TL_QUEUE 1
+#endif
 #ifndef SLCS_TL_HINTS
 #define SLCS_TL_HINTS 1
 #endif
@@ -350,7 +356,11 @@ struct RunTile {
   // between B of band-1 and T of this band, incl. the diagonals into the
   // neighbouring words) and with the next word of the same band.  Links
   // leaving the tile are left to the global merge.
-  __device__ void link(int u, uint32_t T, uint32_t B) const {
+  // q (optional): a per-warp queue in shared memory (256 node-slot pairs per warp,
+  // counters qn[warp]); the band-above pairs are queued and then united 32 per warp
+  // step instead of inside each lane's divergent run/overlap loops
+  __device__ void link(int u, uint32_t T, uint32_t B, uint32_t* q = nullptr,
+                       int* qn = nullptr, int qcap = 256) const {
     const int band = u / TWW, w = u % TWW;
     for (uint32_t x = T | B; x;) {
       const uint32_t m = first_run(x);
@@ -401,6 +411,14 @@ struct RunTile {
             fa = a;
             fb = b;
           } else if (par[nslot(b)] != a) {  // b hangs under a already: same set
+            if (q) {
+              const int wq = threadIdx.x >> 5;
+              const int at = atomicAdd(qn + wq, 1);
+              if (at < qcap) {
+                q[wq * qcap + at] = (uint32_t(nslot(a)) << 16) | uint32_t(nslot(b));
+                return;
+              }
+            }
             a = unite(a, b);
           }
         };
@@ -433,6 +451,16 @@ struct RunTile {
       const bool phave = __shfl_up_sync(0xffffffffu, have ? 1u : 0u, 1) != 0u;
 #if SLCS_TL_HINTS
       if (have && lo != hi && !(lane > 0 && phave && plo == lo && phi == hi)) unite(fa, fb);
+      if (q) {
+        __syncwarp();
+        const int wq = threadIdx.x >> 5;
+        const int n = min(qn[wq], qcap);
+        for (int i = lane; i < n; i += 32) {
+          const uint32_t e = q[wq * qcap + i];
+          const uint32_t a = snode(e >> 16), b = snode(e & 0xffffu);
+          if (par[nslot(b)] != a) unite(a, b);
+        }
+      }
 #else
       if (have && !(lane > 0 && phave && plo == lo && phi == hi)) unite(fa, fb);
 #endif
@@ -530,6 +558,22 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   }
   sT[u0] = Tw;
   sB[u0] = Bw;
+#if SLCS_TL_QUEUE
+  // touch + fl (16 KB) are free until the roots are known: the link queue
+  __shared__ int s_qn[LT_THREADS / 32];
+  if (threadIdx.x < LT_THREADS / 32) s_qn[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  T tile{par, sT, sB};
+  tile.link(u0, Tw, Bw, reinterpret_cast<uint32_t*>(touch), s_qn);
+  uint32_t rt[16];
+  tile.roots(u0, Tw, Bw, rt);
+  for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x) {
+    reinterpret_cast<uint32_t*>(touch)[q] = 0;
+    if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
+  }
+  __syncthreads();
+#else
   for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x) {
     reinterpret_cast<uint32_t*>(touch)[q] = 0;
     if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
@@ -541,6 +585,7 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   uint32_t rt[16];
   tile.roots(u0, Tw, Bw, rt);
   __syncthreads();
+#endif
   if (MODE == MODE_SIZE) {
     for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x)
       reinterpret_cast<uint4*>(lsz)[q] = make_uint4(0u, 0u, 0u, 0u);
@@ -1615,7 +1660,19 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
 #endif
   stamp();  // 1: loads
   T tile{par, sT, sB};
+#if SLCS_COOP_PDL && SLCS_FUSED_QUEUE
+  {
+    // the target/selection windows and the ring list are staged after the
+    // union-find: their shared memory holds the link queue meanwhile
+    constexpr int QWORDS = (TROWS * 10 + SROWS * 10 + FT_LIST / 2) / (UNITS / 32);
+    __shared__ int s_qn[UNITS / 32];
+    if (threadIdx.x < UNITS / 32) s_qn[threadIdx.x] = 0;
+    __syncthreads();
+    tile.link(u0, Tw, Bw, tw, s_qn, QWORDS);
+  }
+#else
   tile.link(u0, Tw, Bw);
+#endif
   stamp();  // 2: link
   // flatten in place: a run's slot holds its root's slot, a root's slot holds
   // its record (REC_ROOT set) -- no per-run root registers stay live afterwards
