@@ -410,7 +410,8 @@ struct RunTile {
             have = true;
             fa = a;
             fb = b;
-          } else if (par[nslot(b)] != a) {  // b hangs under a already: same set
+          } else {
+            // queued pairs are filtered when the warp unites them
             if (q) {
               const int wq = threadIdx.x >> 5;
               const int at = atomicAdd(qn + wq, 1);
@@ -419,6 +420,7 @@ struct RunTile {
                 return;
               }
             }
+            if (par[nslot(b)] == a) return;  // b hangs under a already: same set
             a = unite(a, b);
           }
         };
