@@ -37,6 +37,9 @@ namespace cg = cooperative_groups;
 #ifndef SLCS_COOP_PDL
 #define SLCS_COOP_PDL 2
 #endif
+#ifndef SLCS_MERGE_QUEUE
+#define SLCS_MERGE_QUEUE 1
+#endif
 #ifndef SLCS_FUSED_QUEUE
 #define SLCS_FUSED_QUEUE 0
 #endif
@@ -680,6 +683,17 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t nA = uint32_t(nhb) * uint32_t(g.wpr), nB = uint32_t(nvb) * uint32_t(g.BH);
+#if SLCS_MERGE_QUEUE
+  // a horizontal-border word's further pairs are queued per warp and united by
+  // all lanes together at the end: divergent lanes would run their L2 find
+  // chains one after another, the compacted warp runs 32 of them in parallel
+  constexpr int MQ = 64;
+  __shared__ uint32_t s_qa[8][MQ], s_qb[8][MQ];
+  __shared__ int s_qn[8];
+  const int mw = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_qn[mw] = 0;
+  __syncwarp();
+#endif
   // units [0, nA): horizontal tile borders; [nA, nA + nB): vertical ones
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nA + nB;
        i += gridDim.x * blockDim.x) {
@@ -718,6 +732,14 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
             fb = lb;
             first = false;
           } else {
+#if SLCS_MERGE_QUEUE
+            const int at = atomicAdd(&s_qn[mw], 1);
+            if (at < MQ) {
+              s_qa[mw][at] = la;
+              s_qb[mw][at] = lb;
+              return;
+            }
+#endif
             gunite(Ps, g, la, lb);
           }
         };
@@ -756,6 +778,11 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
       }
     }
   }
+#if SLCS_MERGE_QUEUE
+  __syncwarp();
+  const int n = min(s_qn[mw], MQ);
+  for (int q = threadIdx.x & 31; q < n; q += 32) gunite(Ps, g, s_qa[mw][q], s_qb[mw][q]);
+#endif
 }
 
 // After the merge: every listed local root points straight at its global
