@@ -78,6 +78,25 @@ __global__ void k_pack_u8(const uint8_t* __restrict__ dense, uint32_t* __restric
   }
 }
 
+// 1 B/px -> bits for rows of a multiple of 128 px (no padding words): a thread
+// packs 16 bytes from one coalesced 16 B load (4 bytes -> 4 bits by one
+// multiply), and an even lane joins its odd neighbour's half into a word.
+__device__ __forceinline__ uint32_t nz4(uint32_t v) {
+  const uint32_t x = __vcmpne4(v, 0u) & 0x01010101u;
+  return (x * 0x01020408u) >> 24;
+}
+__global__ void k_pack_u8_vec(const uint4* __restrict__ dense, uint32_t* __restrict__ bits,
+                              size_t halves) {
+  slcs_pdl_wait();
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < halves;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const uint4 v = __ldg(dense + i);
+    const uint32_t h = nz4(v.x) | (nz4(v.y) << 4) | (nz4(v.z) << 8) | (nz4(v.w) << 12);
+    const uint32_t hi = __shfl_down_sync(__activemask(), h, 1);
+    if (!(i & 1)) bits[i >> 1] = h | (hi << 16);
+  }
+}
+
 __global__ void k_pack_u16(const uint16_t* __restrict__ dense, uint32_t* __restrict__ bits, int w,
                            int wpr, size_t pitch, size_t nwords_total) {
   slcs_pdl_wait();
@@ -744,6 +763,12 @@ __global__ void k_random_mask(uint32_t* __restrict__ bits, int w, int h, long lo
 }  // namespace
 
 int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool, cudaStream_t st) {
+  if (g.w % 128 == 0 && g.pitch == size_t(g.wpr) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0) {
+    const size_t halves = size_t(g.w) / 16 * size_t(g.h) * size_t(g.batch);
+    pdl(k_pack_u8_vec, grid_for(halves, kThreads, 148 * 16), kThreads, 0, st,
+        reinterpret_cast<const uint4*>(dense), bits, halves);
+    return 1;
+  }
   size_t n = g.slice * size_t(g.batch);
   pdl(k_pack_u8, grid_for(n, kThreads), kThreads, 0, st, dense, bits, g.w, g.h, g.wpr, g.pitch,
                                                         n);

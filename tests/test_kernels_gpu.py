@@ -273,3 +273,20 @@ def test_wide_images_bulk_slab_near(dev, w, h, batch, k):
             ed, ee = O.dilate(ed), O.erode(ee)
         assert np.array_equal(got_d[i], ed)
         assert np.array_equal(got_e[i], ee)
+
+
+@pytest.mark.parametrize("shape", [(1, 128, 1), (3, 17, 256), (2, 5, 1024), (1, 9, 4096),
+                                   (1, 8, 160), (2, 3, 100)])
+def test_bool_upload_pack_round_trip(dev, shape):
+    # 1 B/px -> bit-packed upload: the vectorised 16-byte path (rows of a multiple of
+    # 128 px) and the generic path must agree with the bytes (any nonzero is true)
+    b, h, w = shape
+    rng = np.random.default_rng(b * 1000 + h * 10 + w)
+    a = rng.integers(0, 4, size=(b, h, w), dtype=np.uint8) * rng.integers(0, 2, size=(b, h, w),
+                                                                          dtype=np.uint8)
+    arr = a[0] if b == 1 else a
+    img = DeviceImage.upload(arr, PixelKind.Bool)
+    got = img.numpy()
+    assert np.array_equal(got, (arr != 0).astype(np.uint8))
+    want = [int((s_ != 0).sum()) for s_ in a]
+    assert kernels.countTrue(img) == (want[0] if b == 1 else want)
