@@ -96,6 +96,12 @@ int slcs_image_to_device(slcs_ctx* ctx, const slcs_image* img, void* dev, size_t
  * draw i.  Lets each rank of a banded run generate its own band. */
 int slcs_random_mask(slcs_ctx* ctx, int w, int h, long long row0, uint64_t seed, double density,
                      slcs_image** out);
+/* Rows [row0, row0 + h) of a uniform U16 fixture, pixel i of the w-wide image
+ * = (draw i of splitmix64(seed)) % 65536 -- the reference's Rng::below(65536)
+ * per pixel (proj/include/pixlog/rng.hpp:21-23), as make_golden uses it.
+ * Fixture for the 65536^2 threshold parity/bench (no reference function). */
+int slcs_random_u16(slcs_ctx* ctx, int w, int h, long long row0, uint64_t seed,
+                    slcs_image** out);
 int slcs_image_retain(slcs_image* img);
 int slcs_image_release(slcs_image* img);
 int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch);
@@ -225,6 +231,11 @@ int slcs_program_download(slcs_program* prog, int task, void* host, size_t bytes
  * (synchronises).  kind_out: 0 image, 1 number. */
 int slcs_program_result(slcs_program* prog, int task, int* kind_out, slcs_image** img_out,
                         double* num_out);
+/* Outcome of task `task` in the last run: *state 0 = evaluated, 1 = failed
+ * (*message = the RunError text, e.g. "division by zero"), 2 = aborted because a
+ * dependency failed (executor.cpp:204-218).  *message stays valid until the
+ * next run. */
+int slcs_program_task_state(slcs_program* prog, int task, int* state, const char** message);
 /* Kernel launches issued by one run (after fusion). */
 int slcs_program_launches(slcs_program* prog, int* out);
 /* Human-readable execution plan (fused groups, buffer slots). */

@@ -1,0 +1,208 @@
+// pixlog_slcs_run.cpp -- executor::run on the device ("Level 2").
+//
+// Replaces run() (proj/include/pixlog/executor.hpp:50, proj/src/executor.cpp:231-282)
+// for callers that link it: instead of scheduling one primitive per DAG node on
+// the WorkerPool, the whole TaskGraph becomes one slcs_program (include/slcs.h)
+// -- fused elementwise/near chains, fused reaches, liveness-planned device
+// memory, replayed as a CUDA graph -- and only `load` (PNG decode + upload),
+// `save` (download + PNG encode) and `print` touch the host.
+//
+// The RunReport contract is kept: the log lines "starting computation",
+// "saving file <p>", "<label>=<value>" and "task <id> <opcode> <ms>ms"; one
+// TaskEvent per node with evaluations = 1 for nodes that ran and 0 for nodes
+// aborted because a dependency failed; printLines/savedFiles in program order;
+// the first failure rethrown as RunError(message, id, opcode)
+// (executor.cpp:277-280), after independent branches completed.
+//
+// Timing: a device program has no per-node host timeline.  `load`/`save`
+// events carry their own host intervals; every device-evaluated node gets the
+// program's completion time as both start and end (so dependency order holds),
+// and its log line reports 0.000ms.
+#include <chrono>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "pixlog/executor.hpp"
+#include "pixlog/png_io.hpp"
+#include "slcs.h"
+
+namespace pixlog {
+namespace slcs_bridge {
+slcs_ctx* ctx();
+void check(int rc);
+}  // namespace slcs_bridge
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double msSince(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+std::string resolvePath(const RunOptions& options, const std::string& path) {
+  std::filesystem::path p(path);  // executor.cpp:24-27
+  return (p.is_absolute() ? p : options.baseDir / p).string();
+}
+
+const char* kindName(int k) {
+  return k == SLCS_BOOL ? "bool" : (k == SLCS_U16 ? "u16" : "label");
+}
+
+struct DeviceProgram {
+  slcs_program* p = nullptr;
+  ~DeviceProgram() {
+    if (p) slcs_program_destroy(p);
+  }
+};
+struct Img {
+  slcs_image* p = nullptr;
+  ~Img() {
+    if (p) slcs_image_release(p);
+  }
+};
+
+}  // namespace
+
+RunReport run(const TaskGraph& graph, const RunOptions& options) {
+  using slcs_bridge::check;
+  const size_t n = graph.nodeCount();
+  RunReport report;
+  report.taskCount = n;
+  report.events.resize(n);
+  for (NodeId i = 0; i < n; ++i) {
+    report.events[i].id = i;
+    report.events[i].opcode = graph.node(i).opcode;
+  }
+  report.workers = options.workers > 0 ? options.workers : WorkerPool::defaultWorkers();
+  auto log = [&](const std::string& line) {
+    if (options.log) {
+      options.log(line);
+    } else {
+      std::fprintf(stdout, "%s\n", line.c_str());
+      std::fflush(stdout);
+    }
+  };
+
+  // the TaskGraph as the C ABI's task list (task_graph.hpp:20-24); load paths
+  // are resolved against baseDir so a missing file fails with its full path
+  std::vector<std::string> ops(n), strs(n);
+  std::vector<const char*> op_p(n), str_p(n);
+  std::vector<double> nums(n, 0.0);
+  std::vector<int> dep_off(n + 1, 0), deps;
+  for (NodeId i = 0; i < n; ++i) {
+    const Task& t = graph.node(i);
+    ops[i] = t.opcode;
+    if (const double* d = std::get_if<double>(&t.payload)) nums[i] = *d;
+    if (const std::string* s = std::get_if<std::string>(&t.payload))
+      strs[i] = t.opcode == "load" ? resolvePath(options, *s) : *s;
+    op_p[i] = ops[i].c_str();
+    str_p[i] = std::get_if<std::string>(&t.payload) ? strs[i].c_str() : nullptr;
+    for (NodeId d : t.deps) deps.push_back(int(d));
+    dep_off[i + 1] = int(deps.size());
+  }
+
+  const Clock::time_point t0 = Clock::now();
+  log("starting computation");
+  if (n == 0) {
+    report.computationMs = msSince(t0);
+    return report;
+  }
+  DeviceProgram prog;
+  check(slcs_program_create(slcs_bridge::ctx(), int(n), op_p.data(), nums.data(), str_p.data(),
+                            dep_off.data(), deps.empty() ? nullptr : deps.data(), &prog.p));
+
+  // loads: PNG decode on the host, conversion on the device, bound by path
+  std::map<NodeId, std::string> loadError;
+  for (NodeId i = 0; i < n; ++i) {
+    if (ops[i] != "load") continue;
+    TaskEvent& ev = report.events[i];
+    ev.startMs = msSince(t0);
+    Img img;
+    if (slcs_png_load(slcs_bridge::ctx(), strs[i].c_str(), &img.p) == SLCS_OK)
+      check(slcs_program_bind(prog.p, strs[i].c_str(), img.p));
+    else
+      loadError[i] = slcs_last_error();
+    ev.endMs = msSince(t0);
+  }
+
+  // the whole DAG on the device (graph capture on first run, replay after);
+  // a failing task does not stop independent branches
+  const int rc = slcs_program_run(prog.p, 1);
+  if (rc != SLCS_OK && rc != 8 /* SLCS_ERR_RUN: a task failed */) check(rc);
+  const double doneMs = msSince(t0);
+
+  // per-task outcome; a dependent of a failed or aborted task is aborted
+  std::vector<int> state(n, 0);
+  std::vector<std::string> message(n);
+  for (NodeId i = 0; i < n; ++i) {
+    int st = 0;
+    const char* msg = nullptr;
+    check(slcs_program_task_state(prog.p, int(i), &st, &msg));
+    if (loadError.count(i)) {
+      st = 1;
+      message[i] = loadError[i];
+    } else if (st == 1) {
+      message[i] = msg ? msg : "";
+    }
+    for (NodeId d : graph.node(i).deps)
+      if (state[d] != 0) st = 2;
+    state[i] = st;
+  }
+
+  std::optional<NodeId> firstFailure;
+  for (NodeId i = 0; i < n; ++i) {
+    const Task& t = graph.node(i);
+    TaskEvent& ev = report.events[i];
+    if (state[i] == 2) continue;  // aborted: never ran
+    ev.ran = true;
+    ev.evaluations = 1;
+    if (t.opcode != "load") ev.startMs = ev.endMs = doneMs;
+    if (state[i] == 1) {
+      if (!firstFailure) firstFailure = i;
+    } else if (t.opcode == "save") {
+      log("saving file " + strs[i]);
+      ev.startMs = msSince(t0);
+      int kind = 0;
+      Img img;
+      check(slcs_program_result(prog.p, int(i), &kind, &img.p, nullptr));
+      check(slcs_png_save(slcs_bridge::ctx(), img.p, resolvePath(options, strs[i]).c_str()));
+      ev.endMs = msSince(t0);
+    } else if (t.opcode == "print") {
+      int kind = 0;
+      double num = 0;
+      Img img;
+      check(slcs_program_result(prog.p, int(i), &kind, &img.p, &num));
+      std::string desc;
+      if (kind == 1) {
+        desc = formatNumber(num);
+      } else {
+        int k = 0, w = 0, h = 0, b = 0;
+        check(slcs_image_info(img.p, &k, &w, &h, &b));
+        desc = "image(" + std::to_string(w) + "x" + std::to_string(h) + "," + kindName(k) + ")";
+      }
+      message[i] = desc;
+      log(strs[i] + "=" + desc);
+    }
+    char line[160];
+    std::snprintf(line, sizeof(line), "task %u %s %.3fms", i, t.opcode.c_str(),
+                  ev.endMs - ev.startMs);
+    log(line);
+  }
+  report.computationMs = msSince(t0);
+
+  for (NodeId out : graph.outputs()) {  // executor.cpp:267-275
+    const Task& t = graph.node(out);
+    if (state[out] != 0) continue;
+    if (t.opcode == "save") report.savedFiles.push_back(std::get<std::string>(t.payload));
+    else if (t.opcode == "print")
+      report.printLines.push_back(std::get<std::string>(t.payload) + "=" + message[out]);
+  }
+  if (firstFailure) throw RunError(message[*firstFailure], *firstFailure,
+                                   graph.node(*firstFailure).opcode);
+  return report;
+}
+
+}  // namespace pixlog

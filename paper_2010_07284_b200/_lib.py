@@ -38,6 +38,7 @@ _SIGS = {
     "slcs_image_download": (i32, [vp, vp, vp, sz]),
     "slcs_image_to_device": (i32, [vp, vp, vp, sz]),
     "slcs_random_mask": (i32, [vp, i32, i32, C.c_longlong, C.c_uint64, dbl, pvp]),
+    "slcs_random_u16": (i32, [vp, i32, i32, C.c_longlong, C.c_uint64, pvp]),
     "slcs_image_retain": (i32, [vp]),
     "slcs_image_release": (i32, [vp]),
     "slcs_image_info": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
@@ -84,6 +85,7 @@ _SIGS = {
     "slcs_program_set_input_host": (i32, [vp, cstr, i32, i32, i32, i32, vp]),
     "slcs_program_download": (i32, [vp, i32, vp, sz]),
     "slcs_program_result": (i32, [vp, i32, C.POINTER(i32), pvp, C.POINTER(dbl)]),
+    "slcs_program_task_state": (i32, [vp, i32, C.POINTER(i32), C.POINTER(cstr)]),
     "slcs_program_launches": (i32, [vp, C.POINTER(i32)]),
     "slcs_program_plan": (cstr, [vp]),
 }

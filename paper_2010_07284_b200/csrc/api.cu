@@ -19,13 +19,23 @@ namespace {
 
 thread_local std::string g_err;
 
+// Every entry point runs under guard: exceptions become status codes plus the
+// thread-local message, and a launch error left by the call (CUDA error state
+// is per host thread) fails the call instead of returning SLCS_OK with an
+// unwritten output.
 template <class F>
 int guard(F&& f) {
   try {
     f();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      g_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+      return e == cudaErrorMemoryAllocation ? SLCS_ERR_OOM : SLCS_ERR_CUDA;
+    }
     return SLCS_OK;
   } catch (const Error& e) {
     g_err = e.what();
+    cudaGetLastError();  // reported: do not blame the next call
     return e.code;
   } catch (const std::bad_alloc&) {
     g_err = "host allocation failed";
@@ -35,6 +45,105 @@ int guard(F&& f) {
     return SLCS_ERR_RUN;
   }
 }
+
+// ---- per-thread pinned staging ------------------------------------------------
+// Host<->device copies go through pinned per-thread buffers, so the context
+// lock covers only ENQUEUEING: the host memcpy into staging happens before the
+// lock is taken and the wait for a result after it is released.  Concurrent
+// callers (the reference evaluates independent nodes on WorkerPool threads,
+// executor.cpp:220,259) therefore never block each other on a stream
+// synchronisation.  Slots: 0/1 inputs, 2/3 outputs.  A slot is reused only
+// after the copy that last used it has completed (its event).  Buffers larger
+// than kStageMax fall back to pageable copies under the lock.
+constexpr size_t kStageMax = size_t(256) << 20;
+struct StageSlot {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  int ev_dev = -1;
+  bool pending = false;
+};
+struct ThreadStage {
+  StageSlot s[4];
+  ~ThreadStage() {
+    for (auto& x : s) {
+      if (x.p) cudaFreeHost(x.p);
+      if (x.ev) cudaEventDestroy(x.ev);
+    }
+  }
+};
+thread_local ThreadStage t_stage;
+
+void stage_wait(int i) {
+  StageSlot& x = t_stage.s[i];
+  if (x.pending) {
+    x.pending = false;
+    cuda_check(cudaEventSynchronize(x.ev), "staging wait");
+  }
+}
+// the slot, grown to n bytes, once its previous copy is done (nullptr: too big)
+void* stage_slot(int i, size_t n) {
+  if (n > kStageMax) return nullptr;
+  StageSlot& x = t_stage.s[i];
+  stage_wait(i);
+  if (x.cap < n) {
+    if (x.p) cudaFreeHost(x.p);
+    x.p = nullptr;
+    x.cap = 0;
+    cuda_check(cudaMallocHost(&x.p, n), "cudaMallocHost");
+    x.cap = n;
+  }
+  return x.p;
+}
+// the slot stays busy until the work enqueued so far on `st` has completed
+void stage_fence(int i, int dev, cudaStream_t st) {
+  StageSlot& x = t_stage.s[i];
+  if (x.ev && x.ev_dev != dev) {
+    cudaEventDestroy(x.ev);
+    x.ev = nullptr;
+  }
+  if (!x.ev) {
+    cuda_check(cudaEventCreateWithFlags(&x.ev, cudaEventDisableTiming), "event");
+    x.ev_dev = dev;
+  }
+  cuda_check(cudaEventRecord(x.ev, st), "event");
+  x.pending = true;
+}
+// host source -> pinned staging copy (or the source itself when too big)
+const void* stage_in(int i, const void* src, size_t n) {
+  void* p = stage_slot(i, n);
+  if (!p) return src;
+  std::memcpy(p, src, n);
+  return p;
+}
+
+// a device->host copy enqueued under the lock, completed after it
+struct HostOut {
+  int slot = -1;
+  bool staged = false;  // bytes land in the slot's pinned buffer (else in place)
+  void* dst = nullptr;
+  size_t n = 0;
+  // enqueue the D2H of `bytes` at dev_src for host memory `host` on st
+  void enqueue(int i, void* host, const void* dev_src, size_t bytes, int dev, cudaStream_t st,
+               const char* what) {
+    stage_wait(i);
+    slot = i;
+    dst = host;
+    n = bytes;
+    void* p = stage_slot(i, bytes);
+    staged = p != nullptr;
+    cuda_check(cudaMemcpyAsync(staged ? p : host, dev_src, bytes, cudaMemcpyDeviceToHost, st),
+               what);
+    stage_fence(i, dev, st);
+  }
+  // wait (no lock held) and deliver
+  void finish() {
+    if (slot < 0) return;
+    stage_wait(slot);
+    if (staged) std::memcpy(dst, t_stage.s[slot].p, n);
+    slot = -1;
+  }
+};
 
 const char* kind_name(int k) {
   switch (k) {
@@ -46,6 +155,11 @@ const char* kind_name(int k) {
 }
 
 size_t unit_bytes(int kind) { return kind == SLCS_U16 ? 2 : 4; }
+// bytes of a host image in the reference layout (Bool 1 B/px)
+size_t host_bytes(int kind, int w, int h, int batch) {
+  const size_t px = size_t(w) * size_t(h) * size_t(batch);
+  return px * (kind == SLCS_BOOL ? 1 : (kind == SLCS_U16 ? 2 : 4));
+}
 
 Geo geo_for(int kind, int w, int h, int batch) {
   switch (kind) {
@@ -78,6 +192,16 @@ bool slcs::pdl_enabled() {
     return !(e && e[0] && e[0] != '0');
   }();
   return on;
+}
+
+bool slcs::fault_launch() {
+  static const long long at = [] {
+    const char* e = std::getenv("SLCS_FAULT_LAUNCH");
+    return e ? std::atoll(e) : 0ll;
+  }();
+  if (at <= 0) return false;
+  static std::atomic<long long> n{0};
+  return ++n == at;
 }
 
 void* slcs_ctx::alloc(size_t bytes) {
@@ -149,10 +273,10 @@ slcs_image* bool_arg(slcs_ctx* ctx, const slcs_image* v, const char* op) {
     return const_cast<slcs_image*>(v);
   }
   if (v->kind == SLCS_U16) {
-    slcs_image* out = new_image(ctx, SLCS_BOOL, v->geo.w, v->geo.h, v->geo.batch);
-    ctx->launches += launch_threshold(static_cast<const uint16_t*>(v->data), words(out), v->geo,
-                                      out->geo, 1, 65535, ctx->stream);
-    return out;
+    Ref out(new_image(ctx, SLCS_BOOL, v->geo.w, v->geo.h, v->geo.batch));
+    ctx->launches += launch_threshold(static_cast<const uint16_t*>(v->data), words(out.p),
+                                      v->geo, out.p->geo, 1, 65535, ctx->stream);
+    return out.release();
   }
   fail(SLCS_ERR_KIND, std::string("'") + op + "' expects a boolean image, got " +
                           kind_name(v->kind));
@@ -208,17 +332,17 @@ slcs_image* op_threshold(slcs_ctx* ctx, int op, const slcs_image* img, double n)
                             kind_name(img->kind));
   int lo, hi;
   threshold_interval(op, n, lo, hi);
-  slcs_image* out = new_image(ctx, SLCS_BOOL, img->geo.w, img->geo.h, img->geo.batch);
-  ctx->launches += launch_threshold(static_cast<const uint16_t*>(img->data), words(out), img->geo,
-                                    out->geo, lo, hi, ctx->stream);
-  return out;
+  Ref out(new_image(ctx, SLCS_BOOL, img->geo.w, img->geo.h, img->geo.batch));
+  ctx->launches += launch_threshold(static_cast<const uint16_t*>(img->data), words(out.p),
+                                    img->geo, out.p->geo, lo, hi, ctx->stream);
+  return out.release();
 }
 
 slcs_image* op_not(slcs_ctx* ctx, const slcs_image* a0) {
   Ref a(bool_arg(ctx, a0, "!"));
-  slcs_image* out = new_image(ctx, SLCS_BOOL, a.p->geo.w, a.p->geo.h, a.p->geo.batch);
-  ctx->launches += launch_not(words(a.p), words(out), a.p->geo, ctx->stream);
-  return out;
+  Ref out(new_image(ctx, SLCS_BOOL, a.p->geo.w, a.p->geo.h, a.p->geo.batch));
+  ctx->launches += launch_not(words(a.p), words(out.p), a.p->geo, ctx->stream);
+  return out.release();
 }
 
 slcs_image* op_binary(slcs_ctx* ctx, const slcs_image* a0, const slcs_image* b0, bool is_and) {
@@ -226,12 +350,12 @@ slcs_image* op_binary(slcs_ctx* ctx, const slcs_image* a0, const slcs_image* b0,
   Ref a(bool_arg(ctx, a0, name));
   Ref b(bool_arg(ctx, b0, name));
   same_shape(a.p, b.p, name);
-  slcs_image* out = new_image(ctx, SLCS_BOOL, a.p->geo.w, a.p->geo.h, a.p->geo.batch);
+  Ref out(new_image(ctx, SLCS_BOOL, a.p->geo.w, a.p->geo.h, a.p->geo.batch));
   if (is_and)
-    ctx->launches += launch_and(words(a.p), words(b.p), words(out), a.p->geo, ctx->stream);
+    ctx->launches += launch_and(words(a.p), words(b.p), words(out.p), a.p->geo, ctx->stream);
   else
-    ctx->launches += launch_or(words(a.p), words(b.p), words(out), a.p->geo, ctx->stream);
-  return out;
+    ctx->launches += launch_or(words(a.p), words(b.p), words(out.p), a.p->geo, ctx->stream);
+  return out.release();
 }
 
 slcs_image* op_near(slcs_ctx* ctx, const slcs_image* a0, int k, bool erode) {
@@ -242,12 +366,12 @@ slcs_image* op_near(slcs_ctx* ctx, const slcs_image* a0, int k, bool erode) {
   const slcs_image* src = a.p;
   while (k > 0) {
     int step = k > 8 ? 8 : k;
-    slcs_image* out = new_image(ctx, SLCS_BOOL, g.w, g.h, g.batch);
-    ctx->launches += launch_near(words(src), words(out), g, step, erode, ctx->stream);
+    Ref out(new_image(ctx, SLCS_BOOL, g.w, g.h, g.batch));
+    ctx->launches += launch_near(words(src), words(out.p), g, step, erode, ctx->stream);
     k -= step;
     drop_image(cur.p);
-    cur.p = out;
-    src = out;
+    cur.p = out.release();
+    src = cur.p;
   }
   return cur.release();
 }
@@ -255,31 +379,26 @@ slcs_image* op_near(slcs_ctx* ctx, const slcs_image* a0, int k, bool erode) {
 void ensure_counts(slcs_ctx* ctx, int b) {
   if (ctx->counts_cap >= b) return;
   if (ctx->d_counts) cudaFree(ctx->d_counts);
-  if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
   if (ctx->d_vscratch) cudaFree(ctx->d_vscratch);
   ctx->d_counts = nullptr;
-  ctx->h_counts = nullptr;
   ctx->d_vscratch = nullptr;
   ctx->counts_cap = 0;
   cuda_check(cudaMalloc(&ctx->d_counts, sizeof(unsigned long long) * b), "cudaMalloc");
-  cuda_check(cudaMallocHost(&ctx->h_counts, sizeof(unsigned long long) * b), "cudaMallocHost");
   cuda_check(cudaMalloc(&ctx->d_vscratch, sizeof(unsigned long long) * 2 * b), "cudaMalloc");
   cuda_check(cudaMemsetAsync(ctx->d_vscratch, 0, sizeof(unsigned long long) * 2 * b, ctx->stream),
              "cudaMemsetAsync");
   ctx->counts_cap = b;
 }
 
-void op_volume(slcs_ctx* ctx, const slcs_image* a0, int64_t* out) {
+// counts (u64, identical bits to int64 below 2^63) land in `out` at ho->finish()
+void op_volume(slcs_ctx* ctx, const slcs_image* a0, int64_t* out, HostOut* ho) {
   Ref a(bool_arg(ctx, a0, "volume"));
   int b = a.p->geo.batch;
   ensure_counts(ctx, b);
   ctx->launches += launch_volume(words(a.p), ctx->d_counts, nullptr, ctx->d_vscratch, a.p->geo,
                                  ctx->stream);
-  cuda_check(cudaMemcpyAsync(ctx->h_counts, ctx->d_counts, sizeof(unsigned long long) * b,
-                             cudaMemcpyDeviceToHost, ctx->stream),
-             "volume readback");
-  cuda_check(cudaStreamSynchronize(ctx->stream), "volume sync");
-  for (int i = 0; i < b; ++i) out[i] = int64_t(ctx->h_counts[i]);
+  ho->enqueue(3, out, ctx->d_counts, sizeof(unsigned long long) * b, ctx->device, ctx->stream,
+              "volume readback");
 }
 
 // device-side volume: counts land in device memory, no synchronisation
@@ -394,44 +513,41 @@ slcs_image* upload(slcs_ctx* ctx, int kind, int w, int h, int batch, const void*
   return img.release();
 }
 
-void download(slcs_ctx* ctx, const slcs_image* img, void* dst, size_t bytes, bool to_device) {
+// to_device: dense copy into device memory `dst`.  Otherwise the D2H copy into
+// host memory `dst` is enqueued on `ho` and completes in ho->finish() (call it
+// after releasing the context lock).
+void download(slcs_ctx* ctx, const slcs_image* img, void* dst, size_t bytes, bool to_device,
+              HostOut* ho = nullptr) {
   need_ctx(ctx);
   need_img(img);
   if (!dst) fail(SLCS_ERR_ARG, "null destination buffer");
+  if (!to_device && !ho) fail(SLCS_ERR_ARG, "host download without a completion");
   const Geo& g = img->geo;
   size_t npx = size_t(g.w) * size_t(g.h) * size_t(g.batch);
   size_t need = npx * (img->kind == SLCS_BOOL ? 1 : unit_bytes(img->kind));
   if (bytes < need) fail(SLCS_ERR_ARG, "destination buffer too small");
-  cudaMemcpyKind dir = to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  if (img->kind == SLCS_LABEL) {
-    cuda_check(cudaMemcpyAsync(dst, img->data, need, dir, ctx->stream), "download labels");
-  } else if (img->kind == SLCS_U16) {
-    if (g.pitch == size_t(g.w)) {
-      cuda_check(cudaMemcpyAsync(dst, img->data, need, dir, ctx->stream), "download u16");
-    } else if (to_device) {
-      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(img->data), g.pitch,
-                                          static_cast<uint16_t*>(dst), size_t(g.w), g.w,
-                                          size_t(g.h) * size_t(g.batch), ctx->stream);
-    } else {  // dense on the device, then one D2H copy
-      void* staging = ctx->alloc(need);
-      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(img->data), g.pitch,
-                                          static_cast<uint16_t*>(staging), size_t(g.w), g.w,
-                                          size_t(g.h) * size_t(g.batch), ctx->stream);
-      cuda_check(cudaMemcpyAsync(dst, staging, need, dir, ctx->stream), "download u16");
-      ctx->release(staging);
-    }
+  // the dense reference layout on the device: in place, or a staging buffer
+  const void* dense = img->data;
+  void* staging = nullptr;
+  void* target = to_device ? dst : nullptr;
+  const bool dense_already =
+      img->kind == SLCS_LABEL || (img->kind == SLCS_U16 && g.pitch == size_t(g.w));
+  if (dense_already) {
+    if (to_device)
+      cuda_check(cudaMemcpyAsync(dst, img->data, need, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "download");
   } else {
-    if (to_device) {
-      ctx->launches += launch_unpack(words(img), static_cast<uint8_t*>(dst), g, ctx->stream);
-    } else {
-      void* staging = ctx->alloc(npx);
-      ctx->launches += launch_unpack(words(img), static_cast<uint8_t*>(staging), g, ctx->stream);
-      cuda_check(cudaMemcpyAsync(dst, staging, npx, cudaMemcpyDeviceToHost, ctx->stream),
-                 "download bool");
-      ctx->release(staging);
-    }
+    if (!to_device) target = staging = ctx->alloc(need);
+    if (img->kind == SLCS_U16)
+      ctx->launches += launch_repitch_u16(static_cast<const uint16_t*>(img->data), g.pitch,
+                                          static_cast<uint16_t*>(target), size_t(g.w), g.w,
+                                          size_t(g.h) * size_t(g.batch), ctx->stream);
+    else
+      ctx->launches += launch_unpack(words(img), static_cast<uint8_t*>(target), g, ctx->stream);
+    dense = target;
   }
-  if (!to_device) cuda_check(cudaStreamSynchronize(ctx->stream), "download sync");
+  if (!to_device) ho->enqueue(2, dst, dense, need, ctx->device, ctx->stream, "download");
+  ctx->release(staging);  // stream-ordered: after the copy
 }
 
 }  // namespace slcs
@@ -475,8 +591,7 @@ int slcs_ctx_destroy(slcs_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->d_counts) cudaFree(ctx->d_counts);
-    if (ctx->h_counts) cudaFreeHost(ctx->h_counts);
-    if (ctx->d_vscratch) cudaFree(ctx->d_vscratch);
+      if (ctx->d_vscratch) cudaFree(ctx->d_vscratch);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -503,9 +618,14 @@ int64_t slcs_ctx_launch_count(slcs_ctx* ctx) { return ctx ? ctx->launches.load()
 int slcs_image_upload(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batch, const void* host,
                       slcs_image** out) {
   return guard([&] {
-    LOCKED(ctx);
+    need_ctx(ctx);
     if (!out) fail(SLCS_ERR_ARG, "null output pointer");
-    *out = upload(ctx, kind, w, h, batch, host, false);
+    if (!host) fail(SLCS_ERR_ARG, "null source buffer");
+    check_dims(w, h, batch);
+    const void* src = stage_in(0, host, host_bytes(kind, w, h, batch));
+    LOCKED(ctx);
+    *out = upload(ctx, kind, w, h, batch, src, false);
+    if (src != host) stage_fence(0, ctx->device, ctx->stream);
   });
 }
 
@@ -520,8 +640,12 @@ int slcs_image_from_device(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batc
 
 int slcs_image_download(slcs_ctx* ctx, const slcs_image* img, void* host, size_t bytes) {
   return guard([&] {
-    LOCKED(ctx);
-    download(ctx, img, host, bytes, false);
+    HostOut ho;
+    {
+      LOCKED(ctx);
+      download(ctx, img, host, bytes, false, &ho);
+    }
+    ho.finish();
   });
 }
 
@@ -540,6 +664,19 @@ int slcs_random_mask(slcs_ctx* ctx, int w, int h, long long row0, uint64_t seed,
     if (row0 < 0) fail(SLCS_ERR_ARG, "row0 must be >= 0");
     Ref img(new_image(ctx, SLCS_BOOL, w, h, 1));
     ctx->launches += launch_random_mask(words(img.p), img.p->geo, row0, seed, density, ctx->stream);
+    *out = img.release();
+  });
+}
+
+int slcs_random_u16(slcs_ctx* ctx, int w, int h, long long row0, uint64_t seed,
+                    slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    if (row0 < 0) fail(SLCS_ERR_ARG, "row0 must be >= 0");
+    Ref img(new_image(ctx, SLCS_U16, w, h, 1));
+    ctx->launches += launch_random_u16(static_cast<uint16_t*>(img.p->data), img.p->geo, row0, seed,
+                                       ctx->stream);
     *out = img.release();
   });
 }
@@ -611,7 +748,15 @@ int slcs_interior_k(slcs_ctx* ctx, const slcs_image* a, int k, slcs_image** out)
   PRIM(*out = op_near(ctx, a, k, true));
 }
 int slcs_volume(slcs_ctx* ctx, const slcs_image* a, int64_t* out) {
-  PRIM(op_volume(ctx, a, out));
+  return guard([&] {
+    HostOut ho;
+    {
+      LOCKED(ctx);
+      if (!out) fail(SLCS_ERR_ARG, "null output");
+      op_volume(ctx, a, out, &ho);
+    }
+    ho.finish();
+  });
 }
 int slcs_volume_async(slcs_ctx* ctx, const slcs_image* a, int64_t* dev_counts) {
   return guard([&] {
@@ -715,6 +860,8 @@ int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls)
   return guard([&] {
     if (!st || !roots || !cls) fail(SLCS_ERR_ARG, "null argument");
     slcs_ctx* ctx = st->ctx;
+    HostOut o1, o2;
+    {
     LOCKED(ctx);
     const Geo& g = st->u->geo;
     if (row < 0 || row >= g.h) fail(SLCS_ERR_SHAPE, "row out of image");
@@ -727,11 +874,11 @@ int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls)
     }
     ctx->launches += launch_reach_row(words(st->u), st->cs, g, row, st->d_roots, st->d_cls,
                                       ctx->stream);
-    cuda_check(cudaMemcpyAsync(roots, st->d_roots, size_t(g.w) * 4, cudaMemcpyDeviceToHost,
-                               ctx->stream), "row roots");
-    cuda_check(cudaMemcpyAsync(cls, st->d_cls, size_t(g.w), cudaMemcpyDeviceToHost, ctx->stream),
-               "row classes");
-    cuda_check(cudaStreamSynchronize(ctx->stream), "row sync");
+    o1.enqueue(2, roots, st->d_roots, size_t(g.w) * 4, ctx->device, ctx->stream, "row roots");
+    o2.enqueue(3, cls, st->d_cls, size_t(g.w), ctx->device, ctx->stream, "row classes");
+    }
+    o1.finish();
+    o2.finish();
   });
 }
 
@@ -783,26 +930,47 @@ int slcs_reach_state_destroy(slcs_reach_state* st) {
 }  // extern "C"
 
 namespace {
+// host-in/host-out: stage the inputs (no lock), enqueue upload + op + download
+// under the lock, wait for the result after it
 template <class F>
 int host_unary(slcs_ctx* ctx, int kind, const void* a, int w, int h, void* out, size_t out_bytes,
                F&& op) {
   return guard([&] {
-    LOCKED(ctx);
-    if (!out) fail(SLCS_ERR_ARG, "null output");
-    Ref ia(upload(ctx, kind, w, h, 1, a, false));
-    Ref r(op(ia.p));
-    download(ctx, r.p, out, out_bytes, false);
+    need_ctx(ctx);
+    if (!out || !a) fail(SLCS_ERR_ARG, "null argument");
+    check_dims(w, h, 1);
+    const void* sa = stage_in(0, a, host_bytes(kind, w, h, 1));
+    HostOut ho;
+    {
+      LOCKED(ctx);
+      Ref ia(upload(ctx, kind, w, h, 1, sa, false));
+      if (sa != a) stage_fence(0, ctx->device, ctx->stream);
+      Ref r(op(ia.p));
+      download(ctx, r.p, out, out_bytes, false, &ho);
+    }
+    ho.finish();
   });
 }
 template <class F>
 int host_binary(slcs_ctx* ctx, const void* a, const void* b, int w, int h, void* out, F&& op) {
   return guard([&] {
-    LOCKED(ctx);
-    if (!out) fail(SLCS_ERR_ARG, "null output");
-    Ref ia(upload(ctx, SLCS_BOOL, w, h, 1, a, false));
-    Ref ib(upload(ctx, SLCS_BOOL, w, h, 1, b, false));
-    Ref r(op(ia.p, ib.p));
-    download(ctx, r.p, out, size_t(w) * size_t(h), false);
+    need_ctx(ctx);
+    if (!out || !a || !b) fail(SLCS_ERR_ARG, "null argument");
+    check_dims(w, h, 1);
+    const size_t n = host_bytes(SLCS_BOOL, w, h, 1);
+    const void* sa = stage_in(0, a, n);
+    const void* sb = stage_in(1, b, n);
+    HostOut ho;
+    {
+      LOCKED(ctx);
+      Ref ia(upload(ctx, SLCS_BOOL, w, h, 1, sa, false));
+      Ref ib(upload(ctx, SLCS_BOOL, w, h, 1, sb, false));
+      if (sa != a) stage_fence(0, ctx->device, ctx->stream);
+      if (sb != b) stage_fence(1, ctx->device, ctx->stream);
+      Ref r(op(ia.p, ib.p));
+      download(ctx, r.p, out, n, false, &ho);
+    }
+    ho.finish();
   });
 }
 }  // namespace
@@ -832,10 +1000,18 @@ int slcs_h_dilate(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint8_t* out) {
 }
 int slcs_h_count_true(slcs_ctx* ctx, const uint8_t* a, int w, int h, int64_t* out) {
   return guard([&] {
-    LOCKED(ctx);
-    if (!out) fail(SLCS_ERR_ARG, "null output");
-    Ref ia(upload(ctx, SLCS_BOOL, w, h, 1, a, false));
-    op_volume(ctx, ia.p, out);
+    need_ctx(ctx);
+    if (!out || !a) fail(SLCS_ERR_ARG, "null argument");
+    check_dims(w, h, 1);
+    const void* sa = stage_in(0, a, host_bytes(SLCS_BOOL, w, h, 1));
+    HostOut ho;
+    {
+      LOCKED(ctx);
+      Ref ia(upload(ctx, SLCS_BOOL, w, h, 1, sa, false));
+      if (sa != a) stage_fence(0, ctx->device, ctx->stream);
+      op_volume(ctx, ia.p, out, &ho);
+    }
+    ho.finish();
   });
 }
 int slcs_h_ccl_label(slcs_ctx* ctx, const uint8_t* a, int w, int h, uint32_t* out) {
@@ -853,18 +1029,23 @@ int slcs_h_reach(slcs_ctx* ctx, const uint8_t* target, const uint8_t* through, i
 // ---- png_io (proj/src/png_io.cpp:30-144) ---------------------------------------
 namespace {
 
+// decode on the host (no lock), then upload + per-pixel conversion on the device
 slcs_image* png_to_image(slcs_ctx* ctx, const uint8_t* bytes, size_t n) {
+  need_ctx(ctx);
   PngInfo info;
   const std::vector<uint8_t> raw = png_decode(bytes, n, info);
+  // pageable H2D copies return once the source is consumed, so `raw` may be
+  // freed right after the enqueue either way
+  const void* src = stage_in(0, raw.data(), raw.size());
+  LOCKED(ctx);
   Ref img(new_image(ctx, SLCS_U16, info.w, info.h, 1));
   void* staging = ctx->alloc(raw.size());
-  cuda_check(cudaMemcpyAsync(staging, raw.data(), raw.size(), cudaMemcpyHostToDevice, ctx->stream),
+  cuda_check(cudaMemcpyAsync(staging, src, raw.size(), cudaMemcpyHostToDevice, ctx->stream),
              "png upload");
+  if (src != raw.data()) stage_fence(0, ctx->device, ctx->stream);
   ctx->launches += launch_png_to_u16(static_cast<const uint8_t*>(staging), info,
                                      static_cast<uint16_t*>(img.p->data), img.p->geo, ctx->stream);
   ctx->release(staging);
-  // `raw` is pageable host memory: the copy must finish before it is freed
-  cuda_check(cudaStreamSynchronize(ctx->stream), "png upload");
   return img.release();
 }
 
@@ -872,7 +1053,6 @@ slcs_image* png_to_image(slcs_ctx* ctx, const uint8_t* bytes, size_t n) {
 
 int slcs_png_decode(slcs_ctx* ctx, const void* bytes, size_t n, slcs_image** out) {
   return guard([&] {
-    LOCKED(ctx);
     if (!out || !bytes) fail(SLCS_ERR_ARG, "null argument");
     *out = png_to_image(ctx, static_cast<const uint8_t*>(bytes), n);
   });
@@ -880,7 +1060,7 @@ int slcs_png_decode(slcs_ctx* ctx, const void* bytes, size_t n, slcs_image** out
 
 int slcs_png_load(slcs_ctx* ctx, const char* path, slcs_image** out) {
   return guard([&] {
-    LOCKED(ctx);
+    need_ctx(ctx);
     if (!out || !path) fail(SLCS_ERR_ARG, "null argument");
     FILE* f = std::fopen(path, "rb");
     if (!f) fail(SLCS_ERR_RUN, std::string("cannot open file for reading: ") + path);
@@ -900,21 +1080,24 @@ int slcs_png_load(slcs_ctx* ctx, const char* path, slcs_image** out) {
 
 int slcs_png_save(slcs_ctx* ctx, const slcs_image* img, const char* path) {
   return guard([&] {
-    LOCKED(ctx);
+    need_ctx(ctx);
     need_img(img);
     if (!path) fail(SLCS_ERR_ARG, "null path");
     if (img->geo.batch != 1) fail(SLCS_ERR_SHAPE, "savePng: one image per file (batch must be 1)");
     const Geo& g = img->geo;
     const int bytes_px = img->kind == SLCS_LABEL ? 3 : 2;
     const size_t n = size_t(g.h) * (size_t(g.w) * bytes_px + 1);
-    void* rows = ctx->alloc(n);
-    ctx->launches += launch_png_rows(img->data, img->kind, g, static_cast<uint8_t*>(rows),
-                                     ctx->stream);
     std::vector<uint8_t> host(n);
-    cuda_check(cudaMemcpyAsync(host.data(), rows, n, cudaMemcpyDeviceToHost, ctx->stream),
-               "png rows");
-    ctx->release(rows);
-    cuda_check(cudaStreamSynchronize(ctx->stream), "png rows");
+    HostOut ho;
+    {
+      LOCKED(ctx);
+      void* rows = ctx->alloc(n);
+      ctx->launches += launch_png_rows(img->data, img->kind, g, static_cast<uint8_t*>(rows),
+                                       ctx->stream);
+      ho.enqueue(2, host.data(), rows, n, ctx->device, ctx->stream, "png rows");
+      ctx->release(rows);
+    }
+    ho.finish();  // filtering + zlib below run without the context lock
     const std::vector<uint8_t> file =
         png_encode(host.data(), g.w, g.h, img->kind == SLCS_LABEL ? 8 : 16,
                    img->kind == SLCS_LABEL ? 2 : 0);

@@ -88,12 +88,17 @@ __device__ __forceinline__ uint32_t nz4(uint32_t v) {
 __global__ void k_pack_u8_vec(const uint4* __restrict__ dense, uint32_t* __restrict__ bits,
                               size_t halves) {
   slcs_pdl_wait();
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < halves;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const uint4 v = __ldg(dense + i);
+  // warp-uniform trip count (blockDim is a multiple of 32), so the whole warp
+  // takes part in every shuffle; lanes past the end load nothing
+  const unsigned lane = threadIdx.x & 31u;
+  for (size_t base = size_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); base < halves;
+       base += size_t(gridDim.x) * blockDim.x) {
+    const size_t i = base + lane;
+    const bool ok = i < halves;
+    const uint4 v = ok ? __ldg(dense + i) : make_uint4(0u, 0u, 0u, 0u);
     const uint32_t h = nz4(v.x) | (nz4(v.y) << 4) | (nz4(v.z) << 8) | (nz4(v.w) << 12);
-    const uint32_t hi = __shfl_down_sync(__activemask(), h, 1);
-    if (!(i & 1)) bits[i >> 1] = h | (hi << 16);
+    const uint32_t hi = __shfl_down_sync(0xffffffffu, h, 1);
+    if (ok && !(i & 1)) bits[i >> 1] = h | (hi << 16);
   }
 }
 
@@ -629,15 +634,11 @@ bool near_bulk_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream
   const int R = bulk_slab_rows(g, K);
   if (off || R == 0) return false;
   const size_t smem = 2 * size_t(R + 2 * K) * g.pitch * 4 + 16;
-  static const bool attr = [] {
-    cudaFuncSetAttribute(k_near_bulk<K, ERODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         112 * 1024);
-    return true;
-  }();
-  (void)attr;
+  static PerDevice<int> attr;
+  smem_opt_in(attr, k_near_bulk<K, ERODE>, 112 * 1024);
   const int per_slice = (g.h + R - 1) / R;
   const int total = per_slice * g.batch;
-  const int ctas = std::min(total, 148 * 2);
+  const int ctas = std::min(total, device_sm_count() * 2);
   pdl(k_near_bulk<K, ERODE>, ctas, 256, smem, st, a, out, g.h, g.wpr, g.lastmask,
       int(g.pitch / 4), g.slice, R, per_slice, total);
   return true;
@@ -773,8 +774,40 @@ __global__ void k_random_mask(uint32_t* __restrict__ bits, int w, int h, long lo
   }
 }
 
+// uniform u16 fixture: pixel i = (draw i of splitmix64(seed)) % 65536, the
+// reference's Rng::below(65536) per pixel (rng.hpp:21-23) -- the C5 threshold
+// input.  Rows [row0, row0 + h) of a w-wide image; u16 rows use pitch `pitch`.
+__global__ void k_random_u16(uint16_t* __restrict__ px, int w, int h, long long row0,
+                             size_t pitch, unsigned long long seed) {
+  slcs_pdl_wait();
+  const size_t n = pitch * size_t(h);
+  for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = q / pitch;
+    const int c = int(q - r * pitch);
+    uint16_t v = 0;
+    if (c < w) {
+      const unsigned long long i =
+          (unsigned long long)(row0 + (long long)r) * (unsigned long long)w + (unsigned long long)c;
+      unsigned long long z = seed + (i + 1ull) * 0x9e3779b97f4a7c15ull;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      z ^= z >> 31;
+      v = uint16_t(z & 0xffffu);
+    }
+    px[q] = v;
+  }
+}
 
 }  // namespace
+
+int launch_random_u16(uint16_t* px, const Geo& g, long long row0, unsigned long long seed,
+                      cudaStream_t st) {
+  size_t n = g.slice;
+  pdl(k_random_u16, grid_for(n, kThreads, 148 * 32), kThreads, 0, st, px, g.w, g.h, row0,
+      g.pitch, seed);
+  return 1;
+}
 
 int launch_pack_u8(const uint8_t* dense, uint32_t* bits, const Geo& g, bool, cudaStream_t st) {
   if (g.w % 128 == 0 && g.pitch == size_t(g.wpr) && (reinterpret_cast<uintptr_t>(dense) & 15) == 0) {

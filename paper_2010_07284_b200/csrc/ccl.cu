@@ -903,21 +903,20 @@ __global__ void k_reach_select(const uint32_t* __restrict__ ubits,
 }
 
 // ---- reach against a precomputed labelling (label CSE) ------------------------
-// Flags are generation stamps so the per-block flag array never needs
-// clearing: gen = *epoch * 4096 + idx, with *epoch bumped once per program run.
-__global__ void k_epoch_bump(uint32_t* epoch) {
-  slcs_pdl_wait(); *epoch += 1u; }
+// Flags are stamps: the labelling step zeroes the per-block flag array once per
+// program run, and the reaches sharing that labelling stamp gen = idx + 1
+// (idx < 4096 distinct per labelling), so a stamp is never 0 and never reused
+// within a run.
 
 __global__ void k_reach_seed(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ tbits,
                              const uint32_t* __restrict__ P, uint32_t* __restrict__ F32,
-                             const uint32_t* __restrict__ epoch, uint32_t idx, G g) {
+                             uint32_t gen, G g) {
   slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* t = tbits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
   uint32_t* Fs = F32 + size_t(slice) * g.sb;
-  const uint32_t gen = *epoch * 4096u + idx;
   const uint32_t n = uint32_t(g.BH) * uint32_t(g.wpr);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int k = int(i / uint32_t(g.wpr)), j = int(i - uint32_t(k) * uint32_t(g.wpr));
@@ -938,8 +937,7 @@ __global__ void k_reach_select_gen(const uint32_t* __restrict__ ubits,
                                    const uint32_t* __restrict__ tbits,
                                    const uint32_t* __restrict__ P,
                                    const uint32_t* __restrict__ F32,
-                                   const uint32_t* __restrict__ epoch, uint32_t idx,
-                                   uint32_t* __restrict__ out, G g) {
+                                   uint32_t gen, uint32_t* __restrict__ out, G g) {
   slcs_pdl_wait();
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
@@ -947,7 +945,6 @@ __global__ void k_reach_select_gen(const uint32_t* __restrict__ ubits,
   const uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t* Fs = F32 + size_t(slice) * g.sb;
   uint32_t* o = out + size_t(slice) * g.slice;
-  const uint32_t gen = *epoch * 4096u + idx;
   const uint32_t n = uint32_t(g.BH) * g.pitch;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int k = int(i / g.pitch), j = int(i - uint32_t(k) * g.pitch);
@@ -1424,12 +1421,8 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_small(const SmallJobs jobs, G
 template <int MODE>
 int small_launch_jobs(const SmallJobs& jobs, int n, const G& g, cudaStream_t st,
                       const SmallListings& lst = SmallListings{}) {
-  static const bool attr_set = [] {
-    cudaFuncSetAttribute(k_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(small_smem_bytes()));
-    return true;
-  }();
-  (void)attr_set;
+  static PerDevice<int> attr;
+  smem_opt_in(attr, k_small<MODE>, small_smem_bytes());
   pdl(k_small<MODE>, n * jobs.batch, ST_THREADS, small_smem_bytes(), st, jobs, g, lst);
   return 1;
 }
@@ -2024,12 +2017,8 @@ size_t tile_smem() {
 template <int MODE>
 void tile_launch(dim3 grid, const uint32_t* u, const uint32_t* t, CclScratch& s, const G& g,
                  cudaStream_t st) {
-  static const bool attr = [] {  // thread-safe one-time initialisation
-    cudaFuncSetAttribute(k_tile_local<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(tile_smem<MODE>()));
-    return true;
-  }();
-  (void)attr;
+  static PerDevice<int> attr;
+  smem_opt_in(attr, k_tile_local<MODE>, tile_smem<MODE>());
   pdl(k_tile_local<MODE>, grid, LT_THREADS, tile_smem<MODE>(), st, u, t, s.parent, s.flag, s.size,
                                                                  s.lists, g);
 }
@@ -2072,20 +2061,17 @@ int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStre
   return launches;
 }
 
-int launch_epoch_bump(uint32_t* epoch, cudaStream_t st) {
-  pdl(k_epoch_bump, 1, 1, 0, st, epoch);
-  return 1;
-}
-
 int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,
-                         uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
+                         uint32_t* flags32, uint32_t idx, uint32_t* out,
                          uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out) {
+  if (idx >= 4096u) fail(SLCS_ERR_ARG, "too many reaches share one labelling");
+  const uint32_t gen = idx + 1u;
   G g = make_g(gb);
   const uint32_t* P = static_cast<const uint32_t*>(labels);
   dim3 ug(unsigned(grid_blocks(size_t(g.BH) * g.wpr, 256)), unsigned(gb.batch));
-  pdl(k_reach_seed, ug, 256, 0, st, through, target, P, flags32, epoch, idx, g);
+  pdl(k_reach_seed, ug, 256, 0, st, through, target, P, flags32, gen, g);
   dim3 sg(unsigned(grid_blocks(size_t(g.BH) * g.pitch, 256)), unsigned(gb.batch));
-  pdl(k_reach_select_gen, sg, 256, 0, st, through, target, P, flags32, epoch, idx, tmp_bits, g);
+  pdl(k_reach_select_gen, sg, 256, 0, st, through, target, P, flags32, gen, tmp_bits, g);
   return 2 + launch_near(tmp_bits, out, gb, k_out, false, st);
 }
 
@@ -2151,18 +2137,18 @@ bool reach_fused_try(const uint32_t* target, const uint32_t* through, uint32_t* 
                           size_t(KOUT > 0 ? 2 * NB + 2 * KOUT : 1) * 40 + FT_LIST * 2 +
                           size_t(2 * NB + 20) * 4;
   // co-resident CTAs on this device (thread-safe one-time initialisation)
-  static const int capacity = [] {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+  static PerDevice<int> cap;
+  const int capacity = cap.get([](int dev) {
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaFuncSetAttribute(k_reach_fused<KOUT, NB, TK>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_fused<KOUT, NB, TK>, THREADS,
                                                       smem) != cudaSuccess)
       per = 0;
-    cudaGetLastError();
+    cudaGetLastError();  // a failed opt-in only disables the fused path
     return per * sms;
-  }();
+  });
   dim3 grid(unsigned((g.wpr + LTWW - 1) / LTWW), unsigned((g.BH + NB - 1) / NB),
             unsigned(batch));
   const size_t tiles = size_t(grid.x) * grid.y * grid.z;

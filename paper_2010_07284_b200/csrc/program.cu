@@ -36,9 +36,15 @@ template <class F>
 int pguard(F&& f) {
   try {
     f();
+    const cudaError_t e = cudaGetLastError();  // launch errors of this call (per thread)
+    if (e != cudaSuccess) {
+      set_last_error(std::string("CUDA error: ") + cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? SLCS_ERR_OOM : SLCS_ERR_CUDA;
+    }
     return SLCS_OK;
   } catch (const Error& e) {
     set_last_error(e.what());
+    cudaGetLastError();
     return e.code;
   } catch (const std::exception& e) {
     set_last_error(e.what());
@@ -188,6 +194,16 @@ __global__ void k_arith(const double* nums, int a, int b, double ca, double cb, 
         r = x / y;
       }
   }
+  // x86-64 SSE NaN rules, so prints match the reference bit for bit ("-nan" vs
+  // "nan" under %.6g): an invalid operation (inf - inf, 0 * inf) yields the
+  // default NaN, which has the sign bit set; a NaN operand propagates (the
+  // first one when both are NaN).  The GPU's own default NaN is positive.
+  if (r != r) {
+    const unsigned long long q = 0x0008000000000000ull;
+    if (x != x) r = __longlong_as_double(__double_as_longlong(x) | q);
+    else if (y != y) r = __longlong_as_double(__double_as_longlong(y) | q);
+    else r = __longlong_as_double(0xfff8000000000000ull);
+  }
   const_cast<double*>(nums)[out] = r;
 }
 
@@ -195,6 +211,11 @@ __global__ void k_arith(const double* nums, int a, int b, double ca, double cb, 
 
 struct slcs_program {
   slcs_ctx* ctx = nullptr;
+  // Guards this program's state.  A program runs on its own stream and touches
+  // the context only through thread-safe calls (stream-ordered allocation,
+  // event record/wait, the atomic launch counter), so its synchronisations
+  // (division-by-zero check, downloads) never hold the context lock.
+  std::mutex mu;
   std::vector<PTask> tasks;
   std::map<std::string, InputSlot> inputs;
 
@@ -214,7 +235,6 @@ struct slcs_program {
   double* d_nums = nullptr;
   unsigned long long* d_counts = nullptr;
   int* d_err = nullptr;
-  uint32_t* d_epoch = nullptr;
   bool label_cse_used = false;
   void* staging = nullptr;
   size_t staging_bytes = 0;
@@ -240,8 +260,6 @@ struct slcs_program {
     if (d_nums) cudaFree(d_nums);
     if (d_counts) cudaFree(d_counts);
     if (d_err) cudaFree(d_err);
-    if (d_epoch) cudaFree(d_epoch);
-    d_epoch = nullptr;
     arena = scratch = nullptr;
     d_nums = nullptr;
     d_counts = nullptr;
@@ -1090,8 +1108,6 @@ struct slcs_program {
     cuda_check(cudaMemset(d_counts, 0, 2 * sizeof(unsigned long long) * std::max(1, n_nums)),
                "program counts");
     cuda_check(cudaMalloc(&d_err, sizeof(int)), "program error flag");
-    cuda_check(cudaMalloc(&d_epoch, sizeof(uint32_t)), "program epoch");
-    cuda_check(cudaMemset(d_epoch, 0, sizeof(uint32_t)), "program epoch");
     for (LG& n : lgs) {
       if (n.kind == LG_INPUT) n.ptr = inputs[n.name].data;
       else if (!n.dead && n.type != VT_NUM) n.ptr = static_cast<char*>(arena) + n.offset;
@@ -1186,7 +1202,6 @@ struct slcs_program {
   int enqueue(cudaStream_t st) {
     int launches = 0;
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
-    if (label_cse_used) launches += launch_epoch_bump(d_epoch, st);
     // `through` of the reach launched just before (null after any other step):
     // a reach on the same `through` may read it before its launch dependency
     const void* prev_through = nullptr;
@@ -1282,7 +1297,7 @@ struct slcs_program {
             launches += launch_reach_labeled(
                 static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
                 static_cast<const uint32_t*>(lgs[n.in[1]].ptr), lab.ptr,
-                reinterpret_cast<uint32_t*>(static_cast<char*>(lab.ptr) + lb), d_epoch,
+                reinterpret_cast<uint32_t*>(static_cast<char*>(lab.ptr) + lb),
                 uint32_t(n.gen_idx), static_cast<uint32_t*>(n.ptr),
                 static_cast<uint32_t*>(scratch), gb, st, n.k);
             break;
@@ -1400,9 +1415,11 @@ struct slcs_program {
       int err = 0;
       cuda_check(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, pstream), "err");
       cuda_check(cudaStreamSynchronize(pstream), "sync");
-      if (err)
+      if (err) {
+        vals[err - 1].err = "division by zero";
         fail(SLCS_ERR_RUN, "task " + std::to_string(err - 1) + " (" + tasks[err - 1].opcode +
                                ") failed: division by zero");
+      }
     }
     if (first_fail >= 0) fail(SLCS_ERR_RUN, fail_msg);
   }
@@ -1516,7 +1533,7 @@ static InputSlot& input_slot(slcs_program* prog, const char* name, int kind, int
 int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* img) {
   return pguard([&] {
     if (!prog || !img) fail(SLCS_ERR_ARG, "null argument");
-    std::lock_guard<std::mutex> lock(prog->ctx->mu);
+    std::lock_guard<std::mutex> lock(prog->mu);
     cuda_check(cudaSetDevice(prog->ctx->device), "cudaSetDevice");
     InputSlot& s = input_slot(prog, name, img->kind, img->geo.w, img->geo.h, img->geo.batch);
     const_cast<slcs_image*>(img)->refs.fetch_add(1);
@@ -1530,7 +1547,7 @@ int slcs_program_set_input_host(slcs_program* prog, const char* name, slcs_kind 
                                 int h, int batch, const void* host) {
   return pguard([&] {
     if (!prog || !host) fail(SLCS_ERR_ARG, "null argument");
-    std::lock_guard<std::mutex> lock(prog->ctx->mu);
+    std::lock_guard<std::mutex> lock(prog->mu);
     cuda_check(cudaSetDevice(prog->ctx->device), "cudaSetDevice");
     InputSlot& s = input_slot(prog, name, kind, w, h, batch);
     if (s.bound) {
@@ -1572,7 +1589,7 @@ int slcs_program_set_input_host(slcs_program* prog, const char* name, slcs_kind 
 int slcs_program_run(slcs_program* prog, int flags) {
   return pguard([&] {
     if (!prog) fail(SLCS_ERR_ARG, "null program");
-    std::lock_guard<std::mutex> lock(prog->ctx->mu);
+    std::lock_guard<std::mutex> lock(prog->mu);
     prog->run(flags);
   });
 }
@@ -1580,7 +1597,7 @@ int slcs_program_run(slcs_program* prog, int flags) {
 int slcs_program_download(slcs_program* prog, int task, void* host, size_t bytes) {
   return pguard([&] {
     if (!prog || !host) fail(SLCS_ERR_ARG, "null argument");
-    std::lock_guard<std::mutex> lock(prog->ctx->mu);
+    std::lock_guard<std::mutex> lock(prog->mu);
     cuda_check(cudaSetDevice(prog->ctx->device), "cudaSetDevice");
     const Val& v = prog->result_val(task);
     if (v.type == VT_NUM) {
@@ -1623,7 +1640,7 @@ int slcs_program_result(slcs_program* prog, int task, int* kind_out, slcs_image*
                         double* num_out) {
   return pguard([&] {
     if (!prog) fail(SLCS_ERR_ARG, "null program");
-    std::lock_guard<std::mutex> lock(prog->ctx->mu);
+    std::lock_guard<std::mutex> lock(prog->mu);
     cuda_check(cudaSetDevice(prog->ctx->device), "cudaSetDevice");
     const Val& v = prog->result_val(task);
     if (v.type == VT_NUM) {
@@ -1644,6 +1661,18 @@ int slcs_program_result(slcs_program* prog, int task, int* kind_out, slcs_image*
                                prog->ctx->stream),
                "result copy");
     *img_out = img;
+  });
+}
+
+int slcs_program_task_state(slcs_program* prog, int task, int* state, const char** message) {
+  return pguard([&] {
+    if (!prog || !state) fail(SLCS_ERR_ARG, "null argument");
+    std::lock_guard<std::mutex> lock(prog->mu);
+    if (!prog->planned) fail(SLCS_ERR_RUN, "program has not run");
+    if (task < 0 || task >= int(prog->tasks.size())) fail(SLCS_ERR_ARG, "task id out of range");
+    const Val& v = prog->vals[task];
+    *state = v.err.empty() ? 0 : (v.aborted ? 2 : 1);
+    if (message) *message = v.err.c_str();
   });
 }
 

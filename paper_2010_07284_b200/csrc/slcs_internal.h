@@ -61,6 +61,10 @@ __device__ __forceinline__ void slcs_pdl_wait() {
 }
 
 bool pdl_enabled();
+// Fault injection for tests: with SLCS_FAULT_LAUNCH=n in the
+// environment, the n-th kernel launch of the process is issued with an
+// impossible shared-memory request, so it fails like a real launch error.
+bool fault_launch();
 
 template <typename... KArgs, typename... Args>
 inline void pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -75,7 +79,46 @@ inline void pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (fault_launch()) cfg.dynamicSmemBytes = size_t(1) << 30;
+  cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), "kernel launch");
+}
+
+// ---- per-device one-time initialisation ----------------------------------------
+// Kernel attributes (the dynamic shared-memory opt-in) and occupancy are per
+// device, and a process may hold contexts on several devices, so one-time
+// set-up is keyed by the calling thread's current device (every entry point
+// selects its context's device first).
+constexpr int kMaxDevices = 64;
+template <typename T>
+struct PerDevice {
+  std::once_flag once[kMaxDevices];
+  T val[kMaxDevices] = {};
+  template <typename F>
+  T get(F&& init) {
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    if (d < 0 || d >= kMaxDevices) fail(SLCS_ERR_ARG, "device index out of range");
+    std::call_once(once[d], [&] { val[d] = init(d); });
+    return val[d];
+  }
+};
+// opt a kernel into `bytes` of dynamic shared memory on the current device
+template <typename K>
+inline void smem_opt_in(PerDevice<int>& pd, K kern, size_t bytes) {
+  int rc = pd.get([&](int) {
+    return int(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  });
+  if (rc != cudaSuccess)
+    fail(SLCS_ERR_CUDA, std::string("cudaFuncSetAttribute(MaxDynamicSharedMemorySize): ") +
+                            cudaGetErrorString(cudaError_t(rc)));
+}
+inline int device_sm_count() {
+  static PerDevice<int> pd;
+  return pd.get([](int d) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n > 0 ? n : 148;
+  });
 }
 
 // Row geometry of one image kind.
@@ -135,6 +178,10 @@ int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
 // rows [row0, row0 + g.h) of randomMask(g.w x H, density, Rng(seed)) as bits
 int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned long long seed,
                        double density, cudaStream_t st);
+
+// rows [row0, row0 + g.h) of the uniform u16 fixture (pixel i = draw i % 65536)
+int launch_random_u16(uint16_t* px, const Geo& g, long long row0, unsigned long long seed,
+                      cudaStream_t st);
 
 // Fused elementwise program over bit-packed words (see fused.cu).
 struct FusedOp {
@@ -217,10 +264,10 @@ int launch_reach_finish(const uint32_t* target, const uint32_t* through, const C
 // label CSE: one labelling of `through` (large path only), reused by many reaches
 size_t ccl_labels_bytes(int w, int h, int batch);
 int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStream_t st);
-int launch_epoch_bump(uint32_t* epoch, cudaStream_t st);
-// flags32: one uint32 per 2x2 block (generation stamps); idx < 4096 per run
+// flags32: one uint32 per 2x2 block, zeroed by the labelling step once per run;
+// reach number idx (< 4096) of that labelling stamps idx + 1
 int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,
-                         uint32_t* flags32, const uint32_t* epoch, uint32_t idx, uint32_t* out,
+                         uint32_t* flags32, uint32_t idx, uint32_t* out,
                          uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out = 1);
 
 // row-band CCL: out[i] = 0 | vals[k] if lab[i] == keys[k] (keys sorted) | offset + lab[i]
@@ -254,7 +301,6 @@ struct slcs_ctx {
   std::atomic<int64_t> launches{0};
   // small pinned/device scratch for reductions
   unsigned long long* d_counts = nullptr;
-  unsigned long long* h_counts = nullptr;
   unsigned long long* d_vscratch = nullptr;  // 2 * counts_cap, zeroed (launch_volume)
   int counts_cap = 0;
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import time
+import math
 from dataclasses import dataclass, field
 from typing import Optional, Union
 
@@ -29,7 +30,11 @@ FLAG_NO_LABEL_CSE = 4
 
 
 def format_number(v: float) -> str:
-    """formatNumber (image.cpp:64-68): %.6g."""
+    """formatNumber (image.cpp:64-68): snprintf "%.6g".  glibc prints a NaN with
+    its sign bit set (e.g. inf - inf on x86) as "-nan"; Python's % prints "nan"
+    for every NaN, so the sign is restored here."""
+    if math.isnan(v):
+        return "-nan" if math.copysign(1.0, v) < 0 else "nan"
     return "%.6g" % v
 
 

@@ -452,6 +452,16 @@ def random_mask_device(w: int, h: int, density: float, seed: int, row0: int = 0,
     return DeviceImage(out, device)
 
 
+def random_u16_device(w: int, h: int, seed: int, row0: int = 0,
+                      device: Optional[Device] = None) -> DeviceImage:
+    """Rows [row0, row0+h) of the uniform u16 fixture (pixel i = draw i of
+    splitmix64(seed) % 65536, Rng::below(65536) per pixel), generated on the GPU."""
+    device = device or Device.default()
+    out = C.c_void_p()
+    _check(_lib.load().slcs_random_u16(device.handle, w, h, row0, seed, C.byref(out)))
+    return DeviceImage(out, device)
+
+
 def loadPng(path: str, device: Optional[Device] = None) -> DeviceImage:
     """png_io loadPng (proj/src/png_io.cpp:30-73): a U16 device image (first channel,
     8-bit samples widened by v*257)."""

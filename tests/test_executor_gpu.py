@@ -377,3 +377,24 @@ def test_small_maxvol_prologue_epilogue_folds(dev, fusion):
         prog.download(prog.graph.outputs[0], got)
         for s in range(n_sl):
             assert np.array_equal(got[s], ref(a[s], b[s])), (expr, s, prog.plan)
+
+
+@needs_ref
+def test_nan_and_inf_prints_match_reference_executor(dev):
+    """print of NaN/inf results reads like the reference's snprintf("%.6g")
+    (image.cpp:64-68): an invalid operation on x86 gives a NaN with the sign bit
+    set ("-nan"), a propagated NaN keeps its operand's sign; the device
+    arithmetic reproduces both (program.cu k_arith)."""
+    R = O.Reference(workers=1)
+    m = mask("x...\n.x..\n..x.\n...x")
+    img = np.asarray(m.data, np.uint8)
+    spec = ('load x = "m.png"\n'
+            'print "a" 1e400 - 1e400\n'
+            'print "b" (volume(x) * 1e400) - 1e400\n'
+            'print "c" 0 * (volume(x) * 1e400)\n'
+            'print "d" ((volume(x) * 1e400) - 1e400) * (0 - 1)\n'
+            'print "e" (0 - 1) * 1e400 + volume(x)\n'
+            'print "f" volume(x) / 3\n')
+    want = R.run(spec, {"m.png": img}, STDLIB)["prints"]
+    rep = run_text(spec, {"m.png": B(img)})
+    assert rep.printLines == want
