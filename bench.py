@@ -605,8 +605,9 @@ def c5_config(args, ws, rank, local):
     import torch
 
     from paper_2010_07284_b200 import Device
-    from paper_2010_07284_b200.bands import (LocalGroup, TorchComm, band_rows, ccl_banded,
-                                             near_banded, reach_banded, volume_banded)
+    from paper_2010_07284_b200.bands import (LocalGroup, SoloComm, TorchComm, band_rows,
+                                             ccl_banded, near_banded, reach_banded,
+                                             volume_banded)
     from paper_2010_07284_b200.pixlog import random_mask_device
 
     stream = torch.cuda.Stream(device=local)
@@ -617,23 +618,11 @@ def c5_config(args, ws, rank, local):
     mask = random_mask_device(n, r1 - r0, args.density, 1, r0, dev)
     target = random_mask_device(n, r1 - r0, 0.05, 2, r0, dev)
 
-    class _Solo:
-        rank, world = 0, 1
-
-        def neighbours(self, first, last):
-            return None, None
-
-        def allgather(self, obj):
-            return [obj]
-
-        def allreduce_sum(self, x):
-            return x
-
-    comm = TorchComm() if ws > 1 else _Solo()
+    comm = TorchComm() if ws > 1 else SoloComm()
 
     if ws == 1 and n * n >= 0xFFFFFFFE:
-        from paper_2010_07284_b200.bands import _rows
-        halves = [_rows(mask, 0, n // 2), _rows(mask, n // 2, n - n // 2)]
+        halves = [random_mask_device(n, b - a, args.density, 1, a, dev)
+                  for a, b in (band_rows(n, 2, 0), band_rows(n, 2, 1))]
 
         def labels():
             return LocalGroup(2).run(ccl_banded, halves)

@@ -109,16 +109,6 @@ int slcs_image_info(const slcs_image* img, int* kind, int* w, int* h, int* batch
 int slcs_image_storage(const slcs_image* img, void** dev, size_t* row_pitch_bytes,
                        size_t* slice_bytes);
 
-/* Row-band CCL: global 64-bit labels of one band from its
- * band-local labels (`labels`: a LABEL image, local max index + 1).  Every
- * non-zero label becomes row0*W + label, except the `nkeys` sorted labels in
- * `keys_dev` (device memory) that take `vals_dev[k]` -- the canonical label of
- * a component merged across band borders.  `out_dev`: W*H uint64 in device
- * memory, written in stream order. */
-int slcs_ccl_band_relabel(slcs_ctx* ctx, const slcs_image* labels, uint64_t row0,
-                          const uint32_t* keys_dev, const uint64_t* vals_dev, int nkeys,
-                          uint64_t* out_dev);
-
 /* ---- image ingest / egress (png_io, proj/src/png_io.cpp:30-144) ----------
  * loadPng: 8/16-bit grey, grey+alpha, RGB or RGBA (Adam7 allowed) -> U16, the
  * first channel, 8-bit samples widened by v*257; palette images and other bit
@@ -168,18 +158,46 @@ int slcs_reach(slcs_ctx* ctx, const slcs_image* target, const slcs_image* throug
 int slcs_maxvol(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
 
 /* ---- row bands (multi-GPU) ------------------------------------
- * A 65536^2 image is split into row bands, one per GPU.  reach is run in
- * phases so bands can be stitched: prepare labels `through` and flags the
- * components holding a seed (through & near(target)); reach_row exports, per
- * pixel of one row, the component's root node and a class byte (0 background,
- * 1 unseeded, 2 seeded); the host resolves cross-band components and hands the
- * roots that became seeded back with reach_set_flags; finish writes
+ * A 65536^2 image is split into row bands, one per GPU (one process per GPU).
+ * Each band runs the single-image kernels on its rows; what crosses a band
+ * border is exchanged on the device:
+ *   near/interior: k halo rows from each neighbour (e.g. NCCL send/recv of the
+ *     neighbours' first/last k packed rows, slcs_image_storage) feed one
+ *     slcs_near_k_halo launch -- no band copies;
+ *   reach: slcs_reach_prepare labels the band; slcs_reach_border_record writes
+ *     the band's BORDER RECORD (roots/classes of its first and last row and its
+ *     first and last target row, slcs_band_record_bytes(0, w) bytes of device
+ *     memory); the caller all-gathers the records of all nb bands (in band
+ *     order, e.g. ncclAllGather); slcs_band_reach_merge resolves the
+ *     components that cross borders with a small device union-find and flags
+ *     this band's newly seeded roots; slcs_reach_finish(k_out = 0) gives
+ *     target | selected, closed by slcs_near_k_halo;
+ *   ccl: band-local labels (slcs_ccl), slcs_ccl_border_record, all-gather,
+ *     slcs_band_ccl_relabel -> global 64-bit labels equal to the whole-image
+ *     ccl::label (component max index + 1), which 65536^2 needs.
+ * Halo buffers are packed rows with the band image's row pitch. */
+int slcs_near_k_halo(slcs_ctx* ctx, const slcs_image* a, int k, int erode, const void* top_dev,
+                     int top_rows, const void* bot_dev, int bot_rows, slcs_image** out);
+/* kind 0 = reach record, 1 = label record, for a band of width w */
+size_t slcs_band_record_bytes(int kind, int w);
+int slcs_ccl_border_record(slcs_ctx* ctx, const slcs_image* labels, void* record_dev);
+/* records_dev: nb records in band order; band_heights: host array of nb heights;
+ * out_dev: W*H uint64 device memory for this band (band `me`). */
+int slcs_band_ccl_relabel(slcs_ctx* ctx, const slcs_image* labels, int nb, int me,
+                          const void* records_dev, const long long* band_heights,
+                          uint64_t* out_dev);
+/* reach in phases: prepare labels `through` and flags the components holding a
+ * seed (through & near(target)); reach_row copies, per pixel of one row, the
+ * component's root node and a class byte (0 background, 1 unseeded, 2 seeded)
+ * to the host; reach_set_flags seeds host-listed roots; finish writes
  * near^k_out(target | selected components) (k_out = 0: no closing near). */
 typedef struct slcs_reach_state slcs_reach_state;
 int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
                        slcs_reach_state** out);
 int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls);
 int slcs_reach_set_flags(slcs_reach_state* st, int n, const uint32_t* roots);
+int slcs_reach_border_record(slcs_reach_state* st, void* record_dev);
+int slcs_band_reach_merge(slcs_reach_state* st, int nb, int me, const void* records_dev);
 int slcs_reach_finish(slcs_reach_state* st, int k_out, slcs_image** out);
 int slcs_reach_state_destroy(slcs_reach_state* st);
 /* Rows [row0, row0 + nrows) of an image / vertical concatenation (same kind

@@ -55,7 +55,12 @@ _SIGS = {
     "slcs_volume": (i32, [vp, vp, C.POINTER(i64)]),
     "slcs_volume_async": (i32, [vp, vp, vp]),
     "slcs_png_load": (i32, [vp, cstr, pvp]),
-    "slcs_ccl_band_relabel": (i32, [vp, vp, C.c_uint64, vp, vp, i32, vp]),
+    "slcs_near_k_halo": (i32, [vp, vp, i32, i32, vp, i32, vp, i32, pvp]),
+    "slcs_band_record_bytes": (sz, [i32, i32]),
+    "slcs_ccl_border_record": (i32, [vp, vp, vp]),
+    "slcs_band_ccl_relabel": (i32, [vp, vp, i32, i32, vp, vp, vp]),
+    "slcs_reach_border_record": (i32, [vp, vp]),
+    "slcs_band_reach_merge": (i32, [vp, i32, i32, vp]),
     "slcs_png_decode": (i32, [vp, vp, sz, pvp]),
     "slcs_png_save": (i32, [vp, vp, cstr]),
     "slcs_label_color": (None, [C.c_uint32, vp]),

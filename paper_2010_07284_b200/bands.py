@@ -1,37 +1,47 @@
 """Row-band decomposition of very large images across GPUs.
 
-A W x H image is split into contiguous row bands, one per rank (one process
-per GPU, ``torch.distributed`` over NCCL; gloo in the CPU tests).  The
-reference cannot process these images at all (its labels throw at
-W*H >= 0xFFFFFFFE, image.cpp:26-28); the banded path computes the same
-results as a single-device run:
+A W x H image is split into contiguous row bands, one per rank (one process per
+GPU, ``torch.distributed`` over NCCL).  The reference cannot process these
+images at all (its labels throw at W*H >= 0xFFFFFFFE, image.cpp:26-28); the
+banded path computes the same results as a single-device run, and every byte it
+exchanges stays in device memory:
 
 * elementwise ops / thresholds: local, no communication;
-* ``near`` / ``interior``: exchange one halo row with each neighbour, run the
-  stencil on [halo; band; halo], crop (out-of-image halo = 0 for dilation, 1
-  for erosion -- the reference's clipping, kernels.cpp:106-121);
-* ``volume``: local popcount + all-reduce SUM;
-* ``reach(t, u)``: each band labels its own ``u`` with the tiled union-find
-  (target halo rows supply near(t) at the band edges), exports the root node
-  and seed class of every pixel of its first and last row, all ranks
-  all-gather those border rows, resolve the components that cross band
-  borders with one small union-find (``resolve_border_flags``, pure numpy),
-  push the newly seeded roots back, select, and close with a halo-exchanged
-  ``near``.
+* ``near^k`` / ``interior^k``: each rank sends its first k packed rows up and its
+  last k rows down (point-to-point NCCL send/recv, neighbours only) into halo
+  buffers, and one ``slcs_near_k_halo`` launch reads them in place -- no band
+  copies (out-of-image rows stay absent: 0 for near, 1 for interior, the
+  reference's clipping, kernels.cpp:106-121);
+* ``volume``: device popcount into an int64 + NCCL all-reduce SUM;
+* ``reach(t, u)``: each band labels its own ``u`` (``slcs_reach_prepare``),
+  writes a small border record (roots / seed classes of its first and last row
+  and its first and last target row), the records are all-gathered (NCCL), and
+  every rank resolves the components that cross band borders with one small
+  device union-find (``slcs_band_reach_merge``, csrc/bands.cu), flags its newly
+  seeded roots, selects ``t | S`` and closes with a halo ``near``;
+* ``ccl::label``: band-local labels, a label border record, all-gather, and a
+  device merge + relabel to global 64-bit labels (``slcs_band_ccl_relabel``).
 
-``Comm`` abstracts the exchange so the same code runs under torch.distributed
-(``TorchComm``) or as N bands on one GPU (``LocalGroup``, used to check the
-banded path bit-exactly against the single-image path on one device).
+Per step and rank the communication is: near^k 2*k packed rows (k * W/8 bytes
+each way), reach 2 * (5 W + W/4) bytes all-gathered per band plus the closing
+near's halo, ccl 8 W bytes per band, volume 8 bytes.
+
+``Comm`` abstracts the exchanges: ``TorchComm`` (torch.distributed; NCCL on
+device tensors, or gloo, which stages through host memory, in the CPU tests and
+the one-GPU test mode) and ``LocalGroup`` (N bands on one GPU, threads -- the
+bit-exact check against the single-image path).  Collectives raise
+``RunError(..., SLCS_ERR_NCCL)`` on failure.
 """
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from typing import Optional
-
-import numpy as np
 
 from . import _lib
 from .pixlog import Device, DeviceImage, PixelKind, RunError, _check, kernels, reach
+
+SLCS_ERR_NCCL = 6
 
 
 def band_rows(h: int, world: int, rank: int) -> tuple[int, int]:
@@ -43,199 +53,236 @@ def band_rows(h: int, world: int, rank: int) -> tuple[int, int]:
     return r0, r0 + base + (1 if rank < extra else 0)
 
 
-# ---------------------------------------------------------------- cross-band merge
-def border_edges(last_roots: np.ndarray, last_cls: np.ndarray, first_roots: np.ndarray,
-                 first_cls: np.ndarray) -> np.ndarray:
-    """Pixel adjacency between the last row of band r and the first row of band
-    r+1 (8-connectivity: column offsets -1, 0, +1) as unique (root_a, root_b)."""
-    a = last_cls > 0
-    b = first_cls > 0
-    w = a.size
-    pairs = []
-    for d in (-1, 0, 1):
-        lo, hi = max(0, -d), min(w, w - d)
-        m = a[lo:hi] & b[lo + d:hi + d]
-        if m.any():
-            pairs.append(np.stack([last_roots[lo:hi][m], first_roots[lo + d:hi + d][m]], 1))
-    if not pairs:
-        return np.zeros((0, 2), np.uint32)
-    return np.unique(np.concatenate(pairs).astype(np.uint32), axis=0)
+# ---------------------------------------------------------------- device memory views
+class _CudaArray:
+    """__cuda_array_interface__ of raw library memory (zero-copy torch views)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 2, "strides": None}
 
 
-def resolve_border_flags(rows: list) -> list:
-    """rows[r] = (first_roots, first_cls, last_roots, last_cls) of band r.
-
-    Returns, per band, the root nodes that must become seeded because their
-    component crosses a band border into a seeded component (cls 2 = seeded,
-    1 = unseeded, 0 = background).  Nodes are (band, root) pairs; the result is
-    identical on every rank (deterministic)."""
-    nb = len(rows)
-    keys = []   # (band, root) -> node ids via unique over a structured key
-    seeded = []
-    for r, (fr, fc, lr, lc) in enumerate(rows):
-        for roots, cls in ((fr, fc), (lr, lc)):
-            m = cls > 0
-            keys.append(np.stack([np.full(m.sum(), r, np.uint64), roots[m].astype(np.uint64)], 1))
-            seeded.append(cls[m] == 2)
-    if not keys:
-        return [np.zeros(0, np.uint32) for _ in range(nb)]
-    allk = np.concatenate(keys)
-    if allk.size == 0:
-        return [np.zeros(0, np.uint32) for _ in range(nb)]
-    packed = (allk[:, 0] << np.uint64(32)) | allk[:, 1]
-    uniq, inv = np.unique(packed, return_inverse=True)
-    seed_node = np.zeros(uniq.size, bool)
-    np.logical_or.at(seed_node, inv, np.concatenate(seeded))
-    src, dst = [], []
-    for r in range(nb - 1):
-        e = border_edges(rows[r][2], rows[r][3], rows[r + 1][0], rows[r + 1][1])
-        if len(e):
-            src.append(np.searchsorted(uniq, (np.uint64(r) << np.uint64(32)) | e[:, 0].astype(np.uint64)))
-            dst.append(np.searchsorted(uniq, (np.uint64(r + 1) << np.uint64(32)) | e[:, 1].astype(np.uint64)))
-    comp = _components(uniq.size, np.concatenate(src) if src else np.zeros(0, np.int64),
-                       np.concatenate(dst) if dst else np.zeros(0, np.int64))
-    comp_seeded = np.zeros(comp.max() + 1 if comp.size else 0, bool)
-    np.logical_or.at(comp_seeded, comp, seed_node)
-    newly = comp_seeded[comp] & ~seed_node
-    band = (uniq >> np.uint64(32)).astype(np.int64)
-    root = (uniq & np.uint64(0xFFFFFFFF)).astype(np.uint32)
-    return [root[newly & (band == r)] for r in range(nb)]
+def device_bytes(ptr: int, nbytes: int, device: int):
+    """A uint8 torch tensor aliasing `nbytes` of device memory at `ptr` (no copy; the
+    owner -- e.g. a DeviceImage -- must outlive it)."""
+    import torch
+    return torch.as_tensor(_CudaArray(ptr, nbytes), device=torch.device("cuda", device))
 
 
-def merge_band_labels(rows: list, width: int) -> list:
-    """Cross-band CCL label merge.  rows[r] = (first_row_labels,
-    last_row_labels, height) of band r, labels band-local (local max index + 1,
-    0 = background).  Band r's global labels are local + row0_r * W.  Components
-    that touch across a band border (8-connectivity: column offsets -1, 0, +1)
-    are united and take the largest global label of the union -- the canonical
-    label of the whole-image ccl::label (max index + 1, ccl.hpp:52-60).  Returns,
-    per band, (keys: sorted local labels (uint32), vals: new global labels
-    (uint64)) for the labels whose global value changes."""
-    nb = len(rows)
-    row0 = np.cumsum([0] + [int(r[2]) for r in rows[:-1]]).astype(np.uint64)
-    W = np.uint64(width)
-    src, dst = [], []
-    for r in range(nb - 1):
-        a = np.asarray(rows[r][1], np.uint64)
-        b = np.asarray(rows[r + 1][0], np.uint64)
-        for d in (-1, 0, 1):
-            lo, hi = max(0, -d), min(width, width - d)
-            m = (a[lo:hi] > 0) & (b[lo + d:hi + d] > 0)
-            if m.any():
-                src.append(a[lo:hi][m] + row0[r] * W)
-                dst.append(b[lo + d:hi + d][m] + row0[r + 1] * W)
-    if not src:
-        return [(np.zeros(0, np.uint32), np.zeros(0, np.uint64)) for _ in range(nb)]
-    src, dst = np.concatenate(src), np.concatenate(dst)
-    ids, inv = np.unique(np.concatenate([src, dst]), return_inverse=True)
-    comp = _components(ids.size, inv[:src.size], inv[src.size:])
-    cmax = np.zeros(comp.max() + 1, np.uint64)
-    np.maximum.at(cmax, comp, ids)
-    new = cmax[comp]
-    changed = new != ids
-    out = []
-    for r in range(nb):
-        lo_id = row0[r] * W
-        hi_id = lo_id + np.uint64(int(rows[r][2])) * W
-        mine = changed & (ids > lo_id) & (ids <= hi_id)
-        keys = (ids[mine] - lo_id).astype(np.uint32)
-        order = np.argsort(keys)
-        out.append((keys[order], new[mine][order]))
-    return out
-
-
-def _components(n: int, src: np.ndarray, dst: np.ndarray) -> np.ndarray:
-    """Connected components of the undirected border graph (scipy csgraph)."""
-    from scipy.sparse import coo_matrix
-    from scipy.sparse.csgraph import connected_components
-    if n == 0:
-        return np.zeros(0, np.int64)
-    g = coo_matrix((np.ones(src.size, np.int8), (src, dst)), shape=(n, n))
-    return connected_components(g, directed=False)[1].astype(np.int64)
+def _rows_view(img: DeviceImage, r0: int, n: int):
+    """Packed rows [r0, r0 + n) of a Bool band, zero-copy."""
+    ptr, pitch, _ = img.storage()
+    return device_bytes(ptr + r0 * pitch, n * pitch, img.device.device)
 
 
 # ---------------------------------------------------------------- communication
 class Comm:
-    """Exchange primitives a banded computation needs."""
+    """Exchange primitives of a banded computation, on device tensors (uint8 /
+    int64).  Every call is a collective: all ranks make it in the same order."""
 
     rank: int
     world: int
 
-    def neighbours(self, first: np.ndarray, last: np.ndarray):
-        """Send my first row up and my last row down; return (row above, row below)
-        (None at the image edges)."""
+    def halo(self, send_up, send_down, recv_up, recv_down, dev: Device) -> None:
+        """send_up -> rank-1, send_down -> rank+1; recv_up <- rank-1, recv_down
+        <- rank+1 (None where there is no neighbour)."""
         raise NotImplementedError
 
-    def allgather(self, obj) -> list:
+    def allgather(self, src, out, dev: Device) -> None:
+        """out = concatenation of every rank's src, in rank order."""
         raise NotImplementedError
 
-    def allreduce_sum(self, x: int) -> int:
+    def allreduce_sum(self, t, dev: Device) -> None:
+        """In-place SUM over ranks."""
         raise NotImplementedError
+
+    def allgather_object(self, obj) -> list:
+        """Small host metadata (band heights)."""
+        raise NotImplementedError
+
+    _heights: Optional[tuple] = None
+
+    def band_heights(self, h: int) -> list:
+        """Every rank's band height (cached while this rank's height is unchanged)."""
+        if self._heights is None or self._heights[0] != h:
+            self._heights = (h, [int(x) for x in self.allgather_object(int(h))])
+        return self._heights[1]
+
+
+def _streams_differ(dev: Device) -> bool:
+    import torch
+    return dev.stream != torch.cuda.current_stream(dev.device).cuda_stream
 
 
 class TorchComm(Comm):
-    """torch.distributed (NCCL between GPUs, gloo on CPU)."""
+    """torch.distributed.  NCCL works on the device tensors directly; its
+    collectives are ordered after the work on torch's current stream, so a
+    Device built on that stream (``Device(i, stream=torch.cuda.current_stream(i)
+    .cuda_stream)``) needs no host synchronisation.  gloo stages through host
+    memory (CPU tests, the one-GPU test mode)."""
 
     def __init__(self):
         import torch.distributed as dist
         self.dist = dist
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
+        self.staged = dist.get_backend() != "nccl"
 
-    def neighbours(self, first, last):
-        rows = self.allgather((first, last))
-        above = rows[self.rank - 1][1] if self.rank > 0 else None
-        below = rows[self.rank + 1][0] if self.rank + 1 < self.world else None
-        return above, below
+    def _before(self, dev: Optional[Device]):
+        if dev is not None and (self.staged or _streams_differ(dev)):
+            dev.synchronize()
 
-    def allgather(self, obj):
+    def _after(self, dev: Optional[Device]):
+        if dev is not None and (self.staged or _streams_differ(dev)):
+            import torch
+            torch.cuda.current_stream(dev.device).synchronize()
+
+    def _guard(self, fn):
+        try:
+            return fn()
+        except RunError:
+            raise
+        except Exception as e:  # NCCL / gloo failures surface as SLCS_ERR_NCCL
+            raise RunError(f"collective failed: {e}", SLCS_ERR_NCCL) from e
+
+    def halo(self, send_up, send_down, recv_up, recv_down, dev=None):
+        d = self.dist
+        self._before(dev)
+
+        def go():
+            stage = self.staged and any(
+                x is not None and x.is_cuda for x in (send_up, send_down, recv_up, recv_down))
+            host = (lambda x: None if x is None else x.cpu()) if stage else (lambda x: x)
+            su, sd = host(send_up), host(send_down)
+            ru, rd = host(recv_up), host(recv_down)
+            ops = []
+            if self.rank > 0:
+                ops += [d.P2POp(d.isend, su, self.rank - 1), d.P2POp(d.irecv, ru, self.rank - 1)]
+            if self.rank + 1 < self.world:
+                ops += [d.P2POp(d.isend, sd, self.rank + 1), d.P2POp(d.irecv, rd, self.rank + 1)]
+            if ops:
+                for w in d.batch_isend_irecv(ops):
+                    w.wait()
+            if stage:
+                if recv_up is not None and self.rank > 0:
+                    recv_up.copy_(ru)
+                if recv_down is not None and self.rank + 1 < self.world:
+                    recv_down.copy_(rd)
+        self._guard(go)
+        self._after(dev)
+
+    def allgather(self, src, out, dev=None):
+        self._before(dev)
+
+        def go():
+            if self.staged and src.is_cuda:
+                o = out.cpu()
+                self.dist.all_gather_into_tensor(o, src.cpu())
+                out.copy_(o)
+            else:
+                self.dist.all_gather_into_tensor(out, src)
+        self._guard(go)
+        self._after(dev)
+
+    def allreduce_sum(self, t, dev=None):
+        self._before(dev)
+
+        def go():
+            if self.staged and t.is_cuda:
+                h = t.cpu()
+                self.dist.all_reduce(h)
+                t.copy_(h)
+            else:
+                self.dist.all_reduce(t)
+        self._guard(go)
+        self._after(dev)
+
+    def allgather_object(self, obj):
         out = [None] * self.world
-        self.dist.all_gather_object(out, obj)
+        self._guard(lambda: self.dist.all_gather_object(out, obj))
         return out
 
-    def allreduce_sum(self, x):
-        out = [None] * self.world
-        self.dist.all_gather_object(out, int(x))
-        return sum(out)
+
+class SoloComm(Comm):
+    """World size 1: the band is the whole image."""
+
+    rank, world = 0, 1
+
+    def halo(self, send_up, send_down, recv_up, recv_down, dev=None):
+        pass
+
+    def allgather(self, src, out, dev=None):
+        out.copy_(src)
+
+    def allreduce_sum(self, t, dev=None):
+        pass
+
+    def allgather_object(self, obj):
+        return [obj]
 
 
 class LocalGroup:
-    """N bands in one process -- the same protocol, exchanges are list lookups.
-    Runs the banded algorithm on a single GPU for bit-exact checks."""
+    """N bands in one process on one GPU (threads): the same protocol, with
+    device-to-device copies for the exchanges.  Runs the banded algorithm for
+    bit-exact checks against the single-image kernels."""
 
     def __init__(self, world: int):
         self.world = world
 
     def run(self, fn, bands: list):
         """fn(comm, band) for every band, stepping all bands through each exchange."""
-        import threading
+        import torch
         results = [None] * self.world
         errors = []
         barrier = threading.Barrier(self.world)
         shared = {}
+        world = self.world
 
         class _C(Comm):
             def __init__(s, r):
-                s.rank, s.world = r, self.world
+                s.rank, s.world = r, world
 
-            def _exchange(s, obj):
+            def _publish(s, obj, dev):
+                if dev is not None:
+                    dev.synchronize()
                 shared[s.rank] = obj
                 barrier.wait()
-                out = [shared[i] for i in range(self.world)]
+                return [shared[i] for i in range(world)]
+
+            def _done(s):
+                torch.cuda.synchronize()
+                barrier.wait()
+
+            def halo(s, send_up, send_down, recv_up, recv_down, dev=None):
+                peers = s._publish((send_up, send_down), dev)
+                if s.rank > 0 and recv_up is not None:
+                    recv_up.copy_(peers[s.rank - 1][1])
+                if s.rank + 1 < world and recv_down is not None:
+                    recv_down.copy_(peers[s.rank + 1][0])
+                s._done()
+
+            def allgather(s, src, out, dev=None):
+                peers = s._publish(src, dev)
+                n = src.numel()
+                for i, p in enumerate(peers):
+                    out[i * n:(i + 1) * n].copy_(p)
+                s._done()
+
+            def allreduce_sum(s, t, dev=None):
+                if dev is not None:
+                    dev.synchronize()  # t is written on the library's stream
+                peers = s._publish(t.clone(), None)
+                total = peers[0].clone()
+                for p in peers[1:]:
+                    total += p
+                s._done()
+                t.copy_(total)
+                torch.cuda.synchronize()
+
+            def allgather_object(s, obj):
+                out = s._publish(obj, None)
                 barrier.wait()
                 return out
-
-            def neighbours(s, first, last):
-                rows = s._exchange((first, last))
-                above = rows[s.rank - 1][1] if s.rank > 0 else None
-                below = rows[s.rank + 1][0] if s.rank + 1 < s.world else None
-                return above, below
-
-            def allgather(s, obj):
-                return s._exchange(obj)
-
-            def allreduce_sum(s, x):
-                return sum(s._exchange(int(x)))
 
         def body(r):
             try:
@@ -255,136 +302,108 @@ class LocalGroup:
 
 
 # ---------------------------------------------------------------- banded ops (device)
-def _rows(img: DeviceImage, r0: int, n: int) -> DeviceImage:
-    out = C.c_void_p()
-    _check(_lib.load().slcs_image_rows(img.device.handle, img.handle, r0, n, C.byref(out)))
-    return DeviceImage(out, img.device)
-
-
-def _vstack(imgs: list) -> DeviceImage:
-    arr = (C.c_void_p * len(imgs))(*[i.handle for i in imgs])
-    out = C.c_void_p()
-    _check(_lib.load().slcs_image_vstack(imgs[0].device.handle, len(imgs), arr, C.byref(out)))
-    return DeviceImage(out, imgs[0].device)
-
-
-def _row_bytes(img: DeviceImage, r: int) -> np.ndarray:
-    return _rows(img, r, 1).numpy().reshape(-1)
-
-
-def _halo(row: Optional[np.ndarray], w: int, fill: int, dev: Device) -> DeviceImage:
-    a = np.full((1, w), fill, np.uint8) if row is None else row.reshape(1, w).astype(np.uint8)
-    return DeviceImage.upload(a, PixelKind.Bool, dev)
-
-
-def _extend(cur: DeviceImage, above, below, fill: int):
-    """[above; cur; below] with halo rows only where a neighbour exists (at the
-    image edges the kernels clip exactly like the reference)."""
-    dev, w = cur.device, cur.width
-    parts, off = [], 0
-    if above is not None:
-        parts.append(_halo(above, w, fill, dev))
-        off = 1
-    parts.append(cur)
-    if below is not None:
-        parts.append(_halo(below, w, fill, dev))
-    return (_vstack(parts) if len(parts) > 1 else cur), off
-
-
-def _rows_bytes(img: DeviceImage, r0: int, n: int) -> np.ndarray:
-    return _rows(img, r0, n).numpy().reshape(n, -1)
+def _empty(nbytes: int, dev: Device):
+    import torch
+    return torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", dev.device))
 
 
 def near_banded(comm: Comm, band: DeviceImage, k: int = 1, erode: bool = False) -> DeviceImage:
-    """near^k (or interior^k) of the full image, restricted to this band: one exchange
-    of k halo rows with each neighbour, then one fused near^k launch (csrc k_near*).
-    Every branch is taken uniformly by all ranks (each exchange is a collective)."""
+    """near^k (or interior^k) of the full image, restricted to this band: k halo
+    rows from each neighbour, then one fused near^k launch that reads them in
+    place (csrc/bitops.cu, Halo).  Every branch is taken uniformly by all ranks."""
     dev, h = band.device, band.height
-    op = kernels.erodeK if erode else kernels.dilateK
     if comm.world == 1:  # the band is the whole image: no halo
-        return op(band, k, dev)
-    if k > 1 and min(comm.allgather(h)) < k:
+        return (kernels.erodeK if erode else kernels.dilateK)(band, k, dev)
+    if band.kind != PixelKind.Bool:
+        band = kernels.threshold(0, band, 0.0, dev)  # boolArg: p > 0 (executor.cpp:43-50)
+    if k > 1 and min(comm.band_heights(h)) < k:
         # some band is thinner than the halo: every rank takes k single steps
-        # (the decision must be uniform -- each step is a collective exchange)
         cur = band
         for _ in range(k):
             cur = near_banded(comm, cur, 1, erode)
         return cur
-    above, below = comm.neighbours(_rows_bytes(band, 0, k), _rows_bytes(band, h - k, k))
-    parts, off = [], 0
-    if above is not None:
-        parts.append(DeviceImage.upload(above, PixelKind.Bool, dev))
-        off = above.shape[0]
-    parts.append(band)
-    if below is not None:
-        parts.append(DeviceImage.upload(below, PixelKind.Bool, dev))
-    ext = _vstack(parts) if len(parts) > 1 else band
-    out = op(ext, k, dev)
-    return _rows(out, off, h) if out.height != h else out
+    _, pitch, _ = band.storage()
+    up = comm.rank > 0
+    down = comm.rank + 1 < comm.world
+    top = _empty(k * pitch, dev) if up else None
+    bot = _empty(k * pitch, dev) if down else None
+    comm.halo(_rows_view(band, 0, k) if up else None,
+              _rows_view(band, h - k, k) if down else None, top, bot, dev)
+    out = C.c_void_p()
+    _check(_lib.load().slcs_near_k_halo(
+        dev.handle, band.handle, int(k), int(erode), None if top is None else top.data_ptr(),
+        k if up else 0, None if bot is None else bot.data_ptr(), k if down else 0, C.byref(out)))
+    if _streams_differ(dev):  # the halo buffers belong to torch's stream
+        dev.synchronize()
+    return DeviceImage(out, dev)
 
 
 def volume_banded(comm: Comm, band: DeviceImage) -> int:
-    return comm.allreduce_sum(kernels.countTrue(band, band.device))
+    """volume of the full image: device popcount + all-reduce SUM (8 bytes)."""
+    import torch
+    dev = band.device
+    t = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", dev.device))
+    if comm.world == 1:
+        return kernels.countTrue(band, dev)
+    _check(_lib.load().slcs_volume_async(dev.handle, band.handle, C.c_void_p(t.data_ptr())))
+    comm.allreduce_sum(t, dev)
+    return int(t.item())
 
 
 def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> DeviceImage:
     """reach(target, through) of the full image, restricted to this band."""
     L = _lib.load()
-    dev, w, h = target.device, target.width, target.height
+    dev, w = target.device, target.width
     if comm.world == 1:  # the band is the whole image
         return reach(target, through, dev)
-    above, below = comm.neighbours(_row_bytes(target, 0), _row_bytes(target, h - 1))
-    t_ext, off = _extend(target, above, below, 0)
-    zero = np.zeros((1, w), np.uint8)
-    u_ext, _ = _extend(through, None if above is None else zero,
-                       None if below is None else zero, 0)
     st = C.c_void_p()
-    _check(L.slcs_reach_prepare(dev.handle, t_ext.handle, u_ext.handle, C.byref(st)))
+    _check(L.slcs_reach_prepare(dev.handle, target.handle, through.handle, C.byref(st)))
     try:
-        def row(r):
-            roots = np.zeros(w, np.uint32)
-            cls = np.zeros(w, np.uint8)
-            _check(L.slcs_reach_row(st, r, roots.ctypes.data, cls.ctypes.data))
-            return roots, cls
-
-        fr, fc = row(off)
-        lr, lc = row(off + h - 1)
-        rows = comm.allgather((fr, fc, lr, lc))
-        newly = np.ascontiguousarray(resolve_border_flags(rows)[comm.rank], np.uint32)
-        if newly.size:
-            _check(L.slcs_reach_set_flags(st, int(newly.size), newly.ctypes.data))
+        nrec = L.slcs_band_record_bytes(0, w)
+        mine = _empty(nrec, dev)
+        _check(L.slcs_reach_border_record(st, C.c_void_p(mine.data_ptr())))
+        allrec = _empty(nrec * comm.world, dev)
+        comm.allgather(mine, allrec, dev)
+        _check(L.slcs_band_reach_merge(st, comm.world, comm.rank, C.c_void_p(allrec.data_ptr())))
         sel = C.c_void_p()
         _check(L.slcs_reach_finish(st, 0, C.byref(sel)))
-        sel_ext = DeviceImage(sel, dev)
+        sel_band = DeviceImage(sel, dev)
+        # the merge reads `allrec` in stream order before it is freed (torch's
+        # caching allocator may recycle it on its own stream)
+        if _streams_differ(dev):
+            dev.synchronize()
     finally:
         L.slcs_reach_state_destroy(st)
-    sel_band = _rows(sel_ext, off, h) if sel_ext.height != h else sel_ext
-    return near_banded(comm, sel_band, 1)
+    return near_banded(comm, sel_band, 1)  # reach = near(t | S)
 
 
-def ccl_banded(comm: Comm, band: DeviceImage):
-    """ccl::label of the full image, restricted to this band, as global 64-bit labels
-    (a torch.int64 tensor on the band's device): band-local union-find labels, one
-    exchange of the first/last label rows, the cross-band merge above, and a device
-    relabel (slcs_ccl_band_relabel).  Equal to the single-image labels where those
-    fit in 32 bits; 65536^2 (config 5) needs the 64-bit form."""
+def ccl_banded(comm: Comm, band: DeviceImage, local=None):
+    """ccl::label of the full image, restricted to this band, as global 64-bit
+    labels (a torch.int64 tensor on the band's device): band-local union-find
+    labels, a label border record all-gathered, and the device merge + relabel.
+    Equal to the single-image labels where those fit in 32 bits; 65536^2
+    (config 5) needs the 64-bit form.  `local`: the band's labels if already
+    computed."""
     import torch
 
     from .pixlog import ccl
+    L = _lib.load()
     dev, w, h = band.device, band.width, band.height
-    local = ccl.label(band, dev)
-    first = _rows(local, 0, 1).numpy().reshape(-1)
-    last = _rows(local, h - 1, 1).numpy().reshape(-1)
-    rows = comm.allgather((first, last, h))
-    keys, vals = merge_band_labels(rows, w)[comm.rank]
-    row0 = sum(int(r[2]) for r in rows[:comm.rank])
-    tdev = torch.device("cuda", dev.device)
-    out = torch.empty((h, w), dtype=torch.int64, device=tdev)
-    k = torch.from_numpy(keys.astype(np.int32)).to(tdev) if keys.size else None
-    v = torch.from_numpy(vals.astype(np.int64)).to(tdev) if vals.size else None
-    torch.cuda.synchronize(tdev)  # the uploads are on torch's stream
-    _check(_lib.load().slcs_ccl_band_relabel(
-        dev.handle, local.handle, row0, None if k is None else k.data_ptr(),
-        None if v is None else v.data_ptr(), int(keys.size), out.data_ptr()))
-    dev.synchronize()
+    if local is None:
+        local = ccl.label(band, dev)
+    heights = comm.band_heights(h)
+    nrec = L.slcs_band_record_bytes(1, w)
+    allrec = None
+    if comm.world > 1:
+        mine = _empty(nrec, dev)
+        _check(L.slcs_ccl_border_record(dev.handle, local.handle, C.c_void_p(mine.data_ptr())))
+        allrec = _empty(nrec * comm.world, dev)
+        comm.allgather(mine, allrec, dev)
+    out = torch.empty((h, w), dtype=torch.int64, device=torch.device("cuda", dev.device))
+    hs = (C.c_longlong * comm.world)(*heights)
+    _check(L.slcs_band_ccl_relabel(dev.handle, local.handle, comm.world, comm.rank,
+                                   None if allrec is None else C.c_void_p(allrec.data_ptr()), hs,
+                                   C.c_void_p(out.data_ptr())))
+    if _streams_differ(dev):
+        dev.synchronize()
     return out

@@ -829,6 +829,8 @@ struct slcs_reach_state {
   uint32_t* d_roots = nullptr;
   uint8_t* d_cls = nullptr;
   int d_cap = 0;
+  void* merge = nullptr;  // cross-band merge scratch (bands.cu)
+  size_t merge_bytes = 0;
 };
 
 extern "C" {
@@ -896,6 +898,48 @@ int slcs_reach_set_flags(slcs_reach_state* st, int n, const uint32_t* roots) {
   });
 }
 
+int slcs_reach_border_record(slcs_reach_state* st, void* record_dev) {
+  return guard([&] {
+    if (!st || !record_dev) fail(SLCS_ERR_ARG, "null argument");
+    slcs_ctx* ctx = st->ctx;
+    LOCKED(ctx);
+    const Geo& g = st->u->geo;
+    size_t roots[2], cls[2], tgt[2];
+    band_reach_record_offsets(g.w, g.pitch, roots, cls, tgt);
+    char* rec = static_cast<char*>(record_dev);
+    const int rows[2] = {0, g.h - 1};
+    for (int side = 0; side < 2; ++side) {
+      ctx->launches += launch_reach_row(words(st->u), st->cs, g, rows[side],
+                                        reinterpret_cast<uint32_t*>(rec + roots[side]),
+                                        reinterpret_cast<uint8_t*>(rec + cls[side]), ctx->stream);
+      cuda_check(cudaMemcpyAsync(rec + tgt[side], words(st->t) + size_t(rows[side]) * g.pitch,
+                                 g.pitch * 4, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "border record");
+    }
+  });
+}
+
+int slcs_band_reach_merge(slcs_reach_state* st, int nb, int me, const void* records_dev) {
+  return guard([&] {
+    if (!st || !records_dev) fail(SLCS_ERR_ARG, "null argument");
+    if (nb < 1 || me < 0 || me >= nb) fail(SLCS_ERR_ARG, "bad band index");
+    slcs_ctx* ctx = st->ctx;
+    LOCKED(ctx);
+    const Geo& g = st->u->geo;
+    const size_t need = band_merge_scratch_bytes(nb, g.w);
+    if (st->merge_bytes < need) {
+      ctx->release(st->merge);
+      st->merge = ctx->alloc(need);
+      st->merge_bytes = need;
+    }
+    uint32_t* roots = nullptr;
+    int* count = nullptr;
+    ctx->launches += launch_band_reach_merge(nb, g.w, g.pitch, me, records_dev, st->merge, &roots,
+                                             &count, ctx->stream);
+    ctx->launches += launch_reach_set_flags_dev(st->cs, g, roots, count, 2 * g.w, ctx->stream);
+  });
+}
+
 int slcs_reach_finish(slcs_reach_state* st, int k_out, slcs_image** out) {
   return guard([&] {
     if (!st || !out) fail(SLCS_ERR_ARG, "null argument");
@@ -919,6 +963,7 @@ int slcs_reach_state_destroy(slcs_reach_state* st) {
       ctx->release(st->scratch);
       ctx->release(st->d_roots);
       ctx->release(st->d_cls);
+      ctx->release(st->merge);
     }
     slcs_image_release(st->t);
     slcs_image_release(st->u);
@@ -1111,19 +1156,72 @@ int slcs_png_save(slcs_ctx* ctx, const slcs_image* img, const char* path) {
 
 void slcs_label_color(uint32_t packed, uint8_t rgb[3]) { png_label_color(packed, rgb); }
 
-int slcs_ccl_band_relabel(slcs_ctx* ctx, const slcs_image* labels, uint64_t row0,
-                          const uint32_t* keys_dev, const uint64_t* vals_dev, int nkeys,
+size_t slcs_band_record_bytes(int kind, int w) {
+  if (w < 1 || (kind != 0 && kind != 1)) return 0;
+  return band_record_bytes(kind, w, bool_geo(w, 1, 1).pitch);
+}
+
+int slcs_ccl_border_record(slcs_ctx* ctx, const slcs_image* labels, void* record_dev) {
+  return guard([&] {
+    LOCKED(ctx);
+    need_img(labels);
+    if (labels->kind != SLCS_LABEL) fail(SLCS_ERR_KIND, "border record expects a label image");
+    if (labels->geo.batch != 1) fail(SLCS_ERR_ARG, "row bands take single images");
+    if (!record_dev) fail(SLCS_ERR_ARG, "null record");
+    const Geo& g = labels->geo;
+    size_t off[2];
+    band_label_record_offsets(g.w, off);
+    const size_t rowb = size_t(g.w) * 4;
+    const char* base = static_cast<const char*>(labels->data);
+    char* rec = static_cast<char*>(record_dev);
+    cuda_check(cudaMemcpyAsync(rec + off[0], base, rowb, cudaMemcpyDeviceToDevice, ctx->stream),
+               "border record");
+    cuda_check(cudaMemcpyAsync(rec + off[1], base + size_t(g.h - 1) * rowb, rowb,
+                               cudaMemcpyDeviceToDevice, ctx->stream),
+               "border record");
+  });
+}
+
+int slcs_band_ccl_relabel(slcs_ctx* ctx, const slcs_image* labels, int nb, int me,
+                          const void* records_dev, const long long* band_heights,
                           uint64_t* out_dev) {
   return guard([&] {
     LOCKED(ctx);
     need_img(labels);
     if (labels->kind != SLCS_LABEL) fail(SLCS_ERR_KIND, "band relabel expects a label image");
-    if (!out_dev || (nkeys > 0 && (!keys_dev || !vals_dev))) fail(SLCS_ERR_ARG, "null argument");
+    if (nb < 1 || me < 0 || me >= nb || !band_heights || !out_dev || (nb > 1 && !records_dev))
+      fail(SLCS_ERR_ARG, "bad band relabel arguments");
     const Geo& g = labels->geo;
-    const size_t n = size_t(g.w) * size_t(g.h) * size_t(g.batch);
-    ctx->launches += launch_relabel_u64(
-        static_cast<const uint32_t*>(labels->data), n, (unsigned long long)(row0) * g.w, keys_dev,
-        reinterpret_cast<const unsigned long long*>(vals_dev), nkeys,
-        reinterpret_cast<unsigned long long*>(out_dev), ctx->stream);
+    if (band_heights[me] != g.h) fail(SLCS_ERR_SHAPE, "band height does not match the labels");
+    std::vector<unsigned long long> row0w(static_cast<size_t>(nb));
+    unsigned long long r0 = 0;
+    for (int b = 0; b < nb; ++b) {
+      row0w[size_t(b)] = r0 * (unsigned long long)g.w;
+      r0 += (unsigned long long)band_heights[b];
+    }
+    void* scratch = ctx->alloc(band_merge_scratch_bytes(nb, g.w));
+    ctx->launches += launch_band_ccl_merge_relabel(
+        nb, g.w, me, records_dev, row0w.data(), scratch, static_cast<const uint32_t*>(labels->data),
+        size_t(g.w) * size_t(g.h), reinterpret_cast<unsigned long long*>(out_dev), ctx->stream);
+    ctx->release(scratch);  // stream-ordered; row0w (pageable) was consumed by the enqueue
+  });
+}
+
+int slcs_near_k_halo(slcs_ctx* ctx, const slcs_image* a, int k, int erode, const void* top_dev,
+                     int top_rows, const void* bot_dev, int bot_rows, slcs_image** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out) fail(SLCS_ERR_ARG, "null output");
+    if (k < 1 || k > 8) fail(SLCS_ERR_ARG, "near with halo rows: k must be in 1..8");
+    if (top_rows < 0 || bot_rows < 0) fail(SLCS_ERR_ARG, "negative halo row count");
+    Ref x(bool_arg(ctx, a, erode ? "interior" : "near"));
+    const Geo& g = x.p->geo;
+    if (g.batch != 1) fail(SLCS_ERR_ARG, "halo rows need a single image");
+    Ref o(new_image(ctx, SLCS_BOOL, g.w, g.h, 1));
+    ctx->launches += launch_near_halo(words(x.p), words(o.p), g, k, erode != 0,
+                                      static_cast<const uint32_t*>(top_dev), top_rows,
+                                      static_cast<const uint32_t*>(bot_dev), bot_rows,
+                                      ctx->stream);
+    *out = o.release();
   });
 }

@@ -305,6 +305,23 @@ __global__ void k_binop(const uint4* __restrict__ a, const uint4* __restrict__ b
   for (; q < n4; q += stride) out[q] = bin_group<OP>(__ldg(a + q), __ldg(b + q));
 }
 
+// Rows above / below the image supplied by a neighbouring row band:
+// image row r < 0 is top[(r + ntop) * pitch], r >= h is bot[(r - h) * pitch];
+// rows beyond the halo are absent (the clipping identity).  An empty Halo (the
+// default) is a whole image.  Single images only (batch 1).
+struct Halo {
+  const uint32_t* top = nullptr;
+  const uint32_t* bot = nullptr;
+  int ntop = 0, nbot = 0;
+};
+__device__ __forceinline__ const uint32_t* row_at(const uint32_t* src, int r, int h, size_t pitch,
+                                                  const Halo& hl) {
+  if (r >= 0 && r < h) return src + size_t(r) * pitch;
+  if (r < 0 && r >= -hl.ntop) return hl.top + size_t(r + hl.ntop) * pitch;
+  if (r >= h && r < h + hl.nbot) return hl.bot + size_t(r - h) * pitch;
+  return nullptr;
+}
+
 // k-fold near / interior.  Thread = (16 B column group q of 4 words, strip of
 // S rows).  All S + 2K input rows are loaded up front (one uint4 plus the two
 // neighbouring words per row, independent loads -> deep memory-level
@@ -317,7 +334,7 @@ template <int K, bool ERODE, int S>
 __global__ void __launch_bounds__(128) k_near(const uint32_t* __restrict__ in,
                                               uint32_t* __restrict__ out, int h, int wpr,
                                               uint32_t lastmask, int pitch4, size_t slice,
-                                              int nstrips) {
+                                              int nstrips, Halo hl) {
   slcs_pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = t / pitch4, q = t - s * pitch4;
@@ -342,11 +359,11 @@ __global__ void __launch_bounds__(128) k_near(const uint32_t* __restrict__ in,
   for (int i = 0; i < S + 2 * K; ++i) {
     const int r = r0 - K + i;
     uint32_t w[6];
-    if (r < 0 || r >= h) {
+    const uint32_t* row = row_at(src, r, h, pitch, hl);
+    if (!row) {
 #pragma unroll
       for (int e = 0; e < 6; ++e) w[e] = ID;
     } else {
-      const uint32_t* row = src + size_t(r) * pitch;
       const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + j0));
       w[0] = has_l ? __ldg(row + j0 - 1) : ID;
       w[1] = c.x | pad[0];
@@ -393,7 +410,7 @@ template <int K, bool ERODE, int S, int P>
 __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict__ in,
                                                      uint32_t* __restrict__ out, int h, int wpr,
                                                      uint32_t lastmask, int pitch4, size_t slice,
-                                                     int nstrips) {
+                                                     int nstrips, Halo hl) {
   slcs_pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = t / pitch4, q = t - s * pitch4;
@@ -418,11 +435,11 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
 
   auto hrow = [&](int r, uint32_t (&o)[4]) {
     uint32_t w[6];
-    if (r < 0 || r >= h) {
+    const uint32_t* row = row_at(src, r, h, pitch, hl);
+    if (!row) {
 #pragma unroll
       for (int e = 0; e < 6; ++e) w[e] = ID;
     } else {
-      const uint32_t* row = src + size_t(r) * pitch;
       const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + j0));
       w[0] = has_l ? __ldg(row + j0 - 1) : ID;
       w[1] = c.x | pad[0];
@@ -514,7 +531,7 @@ template <int K, bool ERODE>
 __global__ void __launch_bounds__(256) k_near_bulk(const uint32_t* __restrict__ in,
                                                    uint32_t* __restrict__ out, int h, int wpr,
                                                    uint32_t lastmask, int pitch4, size_t slice,
-                                                   int R, int slabs_per_slice, int total) {
+                                                   int R, int slabs_per_slice, int total, Halo hl) {
   slcs_pdl_wait();
   extern __shared__ __align__(128) unsigned char smem[];
   const size_t pitch = size_t(pitch4) * 4;
@@ -529,13 +546,28 @@ __global__ void __launch_bounds__(256) k_near_bulk(const uint32_t* __restrict__ 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // slab rows [r0 - K, r0 + R + K): up to three contiguous pieces -- the top
+  // halo, the image, the bottom halo -- copied on one mbarrier
   auto issue = [&](int slab, int st) {  // thread 0
     const int sl = slab / slabs_per_slice, r0 = (slab % slabs_per_slice) * R;
-    const int lo = max(0, r0 - K), hi = min(h, r0 + R + K);
-    const unsigned bytes = unsigned(size_t(hi - lo) * pitch * 4);
+    const int want_lo = r0 - K, want_hi = r0 + R + K;
+    uint32_t* base = buf0 + st * stage_words;
+    const int lo = max(0, want_lo), hi = min(h, want_hi);
+    const int tlo = max(want_lo, -hl.ntop), thi = min(want_hi, 0);
+    const int blo = max(want_lo, h), bhi = min(want_hi, h + hl.nbot);
+    const size_t rowb = pitch * 4;
+    unsigned bytes = unsigned(size_t(hi - lo) * rowb);
+    if (thi > tlo) bytes += unsigned(size_t(thi - tlo) * rowb);
+    if (bhi > blo) bytes += unsigned(size_t(bhi - blo) * rowb);
     mbar_expect_tx(&bar[st], bytes);
-    bulk_g2s(buf0 + st * stage_words + size_t(lo - (r0 - K)) * pitch,
-             in + size_t(sl) * slice + size_t(lo) * pitch, bytes, &bar[st]);
+    bulk_g2s(base + size_t(lo - want_lo) * pitch, in + size_t(sl) * slice + size_t(lo) * pitch,
+             unsigned(size_t(hi - lo) * rowb), &bar[st]);
+    if (thi > tlo)
+      bulk_g2s(base + size_t(tlo - want_lo) * pitch, hl.top + size_t(tlo + hl.ntop) * pitch,
+               unsigned(size_t(thi - tlo) * rowb), &bar[st]);
+    if (bhi > blo)
+      bulk_g2s(base + size_t(blo - want_lo) * pitch, hl.bot + size_t(blo - h) * pitch,
+               unsigned(size_t(bhi - blo) * rowb), &bar[st]);
   };
   if (threadIdx.x == 0 && int(blockIdx.x) < total) issue(blockIdx.x, 0);
   int it = 0;
@@ -544,8 +576,8 @@ __global__ void __launch_bounds__(256) k_near_bulk(const uint32_t* __restrict__ 
     if (threadIdx.x == 0 && slab + int(gridDim.x) < total) issue(slab + gridDim.x, st ^ 1);
     const int sl = slab / slabs_per_slice, r0 = (slab % slabs_per_slice) * R;
     uint32_t* b = buf0 + st * stage_words;
-    // rows outside the image (not part of the copy) read as the identity
-    const int top = max(0, K - r0), bot = max(0, r0 + R + K - h);
+    // rows outside the image and its halo (not part of the copy) read as the identity
+    const int top = max(0, K - r0 - hl.ntop), bot = max(0, r0 + R + K - h - hl.nbot);
     for (size_t q = threadIdx.x; q < size_t(top) * pitch; q += blockDim.x) b[q] = ID;
     for (size_t q = threadIdx.x; q < size_t(bot) * pitch; q += blockDim.x)
       b[size_t(rows_in - bot) * pitch + q] = ID;
@@ -626,7 +658,8 @@ inline int bulk_slab_rows(const Geo& g, int k) {
 }
 
 template <int K, bool ERODE>
-bool near_bulk_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
+bool near_bulk_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st,
+                      const Halo& hl) {
   static const bool off = [] {
     const char* e = std::getenv("SLCS_NO_BULK_NEAR");
     return e && *e && *e != '0';
@@ -640,13 +673,14 @@ bool near_bulk_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream
   const int total = per_slice * g.batch;
   const int ctas = std::min(total, device_sm_count() * 2);
   pdl(k_near_bulk<K, ERODE>, ctas, 256, smem, st, a, out, g.h, g.wpr, g.lastmask,
-      int(g.pitch / 4), g.slice, R, per_slice, total);
+      int(g.pitch / 4), g.slice, R, per_slice, total, hl);
   return true;
 }
 
 template <int K, bool ERODE>
-void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st) {
-  if (near_bulk_launch<K, ERODE>(a, out, g, st)) return;
+void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st,
+                 const Halo& hl) {
+  if (near_bulk_launch<K, ERODE>(a, out, g, st, hl)) return;
   const int pitch4 = int(g.pitch / 4);
   const int block = 128;
   if (K == 1) {
@@ -655,7 +689,7 @@ void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st
     const size_t threads = size_t(pitch4) * size_t(nstrips);
     dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
     pdl(k_near<K, ERODE, S>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, pitch4, g.slice,
-        nstrips);
+        nstrips, hl);
   } else {
     // long strips amortise the 2K halo rows; short images keep >= ~2 waves
 #ifndef SLCS_NS_P
@@ -672,24 +706,25 @@ void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st
     dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
     if (S == 32)
       pdl(k_near_stream<K, ERODE, 32, P>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask,
-          pitch4, g.slice, nstrips);
+          pitch4, g.slice, nstrips, hl);
     else
       pdl(k_near_stream<K, ERODE, 16, P>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask,
-          pitch4, g.slice, nstrips);
+          pitch4, g.slice, nstrips, hl);
   }
 }
 
 template <bool ERODE>
-void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaStream_t st) {
+void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaStream_t st,
+                   const Halo& hl) {
   switch (k) {
-    case 1: near_launch<1, ERODE>(a, out, g, st); break;
-    case 2: near_launch<2, ERODE>(a, out, g, st); break;
-    case 3: near_launch<3, ERODE>(a, out, g, st); break;
-    case 4: near_launch<4, ERODE>(a, out, g, st); break;
-    case 5: near_launch<5, ERODE>(a, out, g, st); break;
-    case 6: near_launch<6, ERODE>(a, out, g, st); break;
-    case 7: near_launch<7, ERODE>(a, out, g, st); break;
-    case 8: near_launch<8, ERODE>(a, out, g, st); break;
+    case 1: near_launch<1, ERODE>(a, out, g, st, hl); break;
+    case 2: near_launch<2, ERODE>(a, out, g, st, hl); break;
+    case 3: near_launch<3, ERODE>(a, out, g, st, hl); break;
+    case 4: near_launch<4, ERODE>(a, out, g, st, hl); break;
+    case 5: near_launch<5, ERODE>(a, out, g, st, hl); break;
+    case 6: near_launch<6, ERODE>(a, out, g, st, hl); break;
+    case 7: near_launch<7, ERODE>(a, out, g, st, hl); break;
+    case 8: near_launch<8, ERODE>(a, out, g, st, hl); break;
     default: fail(SLCS_ERR_ARG, "near: k out of range");
   }
 }
@@ -892,11 +927,23 @@ int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
 
 int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
                 cudaStream_t st) {
+  return launch_near_halo(a, out, g, k, erode, nullptr, 0, nullptr, 0, st);
+}
+
+int launch_near_halo(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
+                     const uint32_t* top, int ntop, const uint32_t* bot, int nbot,
+                     cudaStream_t st) {
   if (k < 1 || k > 8) fail(SLCS_ERR_ARG, "near: k must be in 1..8 per launch");
+  if ((ntop > 0 || nbot > 0) && g.batch != 1) fail(SLCS_ERR_ARG, "halo rows need a single image");
+  Halo hl;
+  hl.top = top;
+  hl.ntop = top ? ntop : 0;
+  hl.bot = bot;
+  hl.nbot = bot ? nbot : 0;
   if (erode)
-    near_dispatch<true>(a, out, g, k, st);
+    near_dispatch<true>(a, out, g, k, st, hl);
   else
-    near_dispatch<false>(a, out, g, k, st);
+    near_dispatch<false>(a, out, g, k, st, hl);
   return 1;
 }
 

@@ -1013,6 +1013,15 @@ __global__ void k_band_set_flags(const uint32_t* __restrict__ roots, int n, uint
   if (i < n) F[gblk(g, roots[i])] = 1;
 }
 
+// the same with the list and its length in device memory (cross-band merge
+// output, bands.cu); the grid covers the list's capacity
+__global__ void k_band_set_flags_dev(const uint32_t* __restrict__ roots, const int* n, uint8_t* F,
+                                     G g) {
+  slcs_pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *n) F[gblk(g, roots[i])] = 1;
+}
+
 __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
   uint32_t lab = 0;
 #pragma unroll
@@ -1912,37 +1921,6 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   stamp();  // 11: near
 }
 
-// ---- row-band CCL: band-local labels -> global 64-bit labels ---------------------
-// A band's labels are the reference's packed form for the band alone
-// (local max index + 1).  Globally the same component's label is the local one
-// plus row0 * W; components that cross band borders take the merged
-// component's max (the canonical label), looked up in a sorted key table.
-__global__ void k_relabel_u64(const uint32_t* __restrict__ lab, size_t n, unsigned long long offset,
-                              const uint32_t* __restrict__ keys,
-                              const unsigned long long* __restrict__ vals, int nkeys,
-                              unsigned long long* __restrict__ out) {
-  slcs_pdl_wait();
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t l = lab[i];
-    unsigned long long v = 0;
-    if (l) {
-      v = offset + l;
-      int lo = 0, hi = nkeys - 1;
-      while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const uint32_t k = __ldg(keys + mid);
-        if (k == l) {
-          v = __ldg(vals + mid);
-          break;
-        }
-        if (k < l) lo = mid + 1;
-        else hi = mid - 1;
-      }
-    }
-    out[i] = v;
-  }
-}
 
 int grid_blocks(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
@@ -2098,6 +2076,14 @@ int launch_reach_set_flags(const CclScratch& s, const Geo& gb, const uint32_t* r
   if (n <= 0) return 0;
   G g = make_g(gb);
   pdl(k_band_set_flags, (n + 255) / 256, 256, 0, st, roots, n, s.flag, g);
+  return 1;
+}
+
+int launch_reach_set_flags_dev(const CclScratch& s, const Geo& gb, const uint32_t* roots,
+                               const int* n_dev, int max_n, cudaStream_t st) {
+  if (max_n <= 0) return 0;
+  G g = make_g(gb);
+  pdl(k_band_set_flags_dev, (max_n + 255) / 256, 256, 0, st, roots, n_dev, s.flag, g);
   return 1;
 }
 
@@ -2318,12 +2304,5 @@ int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch
   return launches + 2;
 }
 
-int launch_relabel_u64(const uint32_t* lab, size_t n, unsigned long long offset,
-                       const uint32_t* keys, const unsigned long long* vals, int nkeys,
-                       unsigned long long* out, cudaStream_t st) {
-  pdl(k_relabel_u64, unsigned(std::min<size_t>((n + 255) / 256, 148 * 32)), 256, 0, st, lab, n,
-      offset, keys, vals, nkeys, out);
-  return 1;
-}
 
 }  // namespace slcs

@@ -171,6 +171,12 @@ int launch_or(const uint32_t* a, const uint32_t* b, uint32_t* out, const Geo& g,
 // k-fold near (dilate) or interior (erode), 1 <= k <= 31 per launch
 int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
                 cudaStream_t st);
+// the same with halo rows from neighbouring row bands: ntop packed rows (pitch of
+// g) directly above row 0 at `top`, nbot rows directly below row h-1 at `bot`;
+// rows beyond them are absent (0 for near, 1 for interior)
+int launch_near_halo(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
+                     const uint32_t* top, int ntop, const uint32_t* bot, int nbot,
+                     cudaStream_t st);
 // counts (u64) and/or dbl (double) per slice; vscratch = 2*batch zeroed u64
 // (accumulators + done counters), left zeroed by the kernel
 int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
@@ -270,10 +276,28 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
                          uint32_t* flags32, uint32_t idx, uint32_t* out,
                          uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out = 1);
 
-// row-band CCL: out[i] = 0 | vals[k] if lab[i] == keys[k] (keys sorted) | offset + lab[i]
-int launch_relabel_u64(const uint32_t* lab, size_t n, unsigned long long offset,
-                       const uint32_t* keys, const unsigned long long* vals, int nkeys,
-                       unsigned long long* out, cudaStream_t st);
+int launch_reach_set_flags_dev(const CclScratch& s, const Geo& gb, const uint32_t* roots,
+                               const int* n_dev, int max_n, cudaStream_t st);
+
+// ---- row bands: cross-band merges (bands.cu) ---------------------------------
+// border record bytes: kind 0 = reach (roots/classes/target of the first and last
+// row), 1 = labels (band-local labels of the first and last row)
+size_t band_record_bytes(int kind, int w, size_t pitch_words);
+void band_reach_record_offsets(int w, size_t pitch_words, size_t* roots, size_t* cls,
+                               size_t* tgt);
+void band_label_record_offsets(int w, size_t* lab);
+size_t band_merge_scratch_bytes(int nb, int w);
+// union-find over all bands' reach records; this band's newly seeded roots and
+// their count land in scratch (*roots_out, *count_out)
+int launch_band_reach_merge(int nb, int w, size_t pitch_words, int me, const void* records,
+                            void* scratch, uint32_t** roots_out, int** count_out,
+                            cudaStream_t st);
+// union-find over all bands' label records + relabel of this band's labels to
+// global 64-bit labels (row0w_host[b] = first row of band b times W)
+int launch_band_ccl_merge_relabel(int nb, int w, int me, const void* records,
+                                  const unsigned long long* row0w_host, void* scratch,
+                                  const uint32_t* labels, size_t npx, unsigned long long* out,
+                                  cudaStream_t st);
 
 // ---- PNG ingest/egress (png.cu) --------------------------------------------------
 struct PngInfo {

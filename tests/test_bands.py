@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 
 import oracle as O
-from paper_2010_07284_b200.bands import band_rows, border_edges, resolve_border_flags
+from band_oracle import border_edges, merge_band_labels, resolve_border_flags
+from paper_2010_07284_b200.bands import band_rows
 
 
 def test_band_rows_partition():
@@ -30,7 +31,7 @@ def emulate_band(t_full, u_full, r0, r1):
     """What the device exports for one band: per-pixel (root, class) rows + labels."""
     u = u_full[r0:r1]
     lab = O.flood_fill_label(u)                 # band-local components
-    nt = O.dilate(t_full)[r0:r1]                # near(t) with the neighbours' halo rows
+    nt = O.dilate(t_full[r0:r1])                # near(t) from the band's own target rows
     seeded = np.zeros(lab.max() + 1, bool)
     seeded[lab[(u > 0) & (nt > 0)]] = True
     seeded[0] = False
@@ -51,7 +52,7 @@ def banded_reach_cpu(t, u, world):
         r0, r1 = band_rows(h, world, r)
         lab, roots, cls, seeded = emulate_band(t, u, r0, r1)
         parts.append((r0, r1, lab, roots, cls, seeded))
-    rows = [(p[3][0], p[4][0], p[3][-1], p[4][-1]) for p in parts]
+    rows = [(p[3][0], p[4][0], p[3][-1], p[4][-1], t[p[0]], t[p[1] - 1]) for p in parts]
     newly = resolve_border_flags(rows)
     S = np.zeros_like(u)
     for (r0, r1, lab, roots, cls, seeded), nw in zip(parts, newly):
@@ -91,21 +92,44 @@ def test_long_component_crossing_many_bands():
 
 
 def _gloo_worker(rank, world, port, t, u, out):
+    """The banded reach protocol through TorchComm (gloo, CPU tensors): border
+    records all-gathered as bytes, the merge rule resolved on every rank, halo
+    rows exchanged with the neighbours, volume all-reduced."""
+    import torch
     import torch.distributed as dist
     from paper_2010_07284_b200.bands import TorchComm
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     comm = TorchComm()
-    r0, r1 = band_rows(t.shape[0], world, rank)
+    h, w = t.shape
+    r0, r1 = band_rows(h, world, rank)
     lab, roots, cls, seeded = emulate_band(t, u, r0, r1)
-    rows = comm.allgather((roots[0], cls[0], roots[-1], cls[-1]))
+    assert comm.band_heights(r1 - r0) == [b - a for a, b in (band_rows(h, world, r)
+                                                              for r in range(world))]
+    # border record: roots (u32) + classes + target rows, as one byte tensor
+    rec = np.concatenate([roots[0].view(np.uint8), roots[-1].view(np.uint8), cls[0], cls[-1],
+                          t[r0], t[r1 - 1]]).astype(np.uint8)
+    allrec = torch.empty(world * rec.size, dtype=torch.uint8)
+    comm.allgather(torch.from_numpy(rec), allrec)
+    recs = allrec.numpy().reshape(world, -1)
+    rows = []
+    for x in recs:
+        rows.append((x[:4 * w].view(np.uint32), x[8 * w:9 * w], x[4 * w:8 * w].view(np.uint32),
+                     x[9 * w:10 * w], x[10 * w:11 * w], x[11 * w:12 * w]))
     newly = resolve_border_flags(rows)[rank]
     S = finish_band(lab, roots, seeded, newly).astype(np.uint8)
-    above, below = comm.neighbours(S[0] | t[r0], S[-1] | t[r1 - 1])
-    parts = comm.allgather(S)
-    assert comm.allreduce_sum(int(S.sum())) == sum(int(p.sum()) for p in parts)
+    band = np.logical_or(t[r0:r1], S).astype(np.uint8)
+    # halo: one row up / down, then the closing near of the band
+    up = torch.zeros(w, dtype=torch.uint8)
+    down = torch.zeros(w, dtype=torch.uint8)
+    comm.halo(torch.from_numpy(band[0].copy()), torch.from_numpy(band[-1].copy()), up, down)
+    ext = np.concatenate([up.numpy()[None], band, down.numpy()[None]])
+    closed = O.dilate(ext)[1:-1]
+    vol = torch.tensor([int(closed.sum())], dtype=torch.int64)
+    comm.allreduce_sum(vol)
+    parts = comm.allgather_object(closed)
     if rank == 0:
-        out.put(np.concatenate(parts))
+        out.put((np.concatenate(parts), int(vol.item())))
     dist.destroy_process_group()
 
 
@@ -122,11 +146,13 @@ def test_two_process_gloo_banded_reach():
     procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, t, u, q)) for r in range(2)]
     for p in procs:
         p.start()
-    S = q.get(timeout=120)
+    got, vol = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert np.array_equal(O.dilate(O.logical_or(t, S)), O.reach(t, u))
+    want = O.reach(t, u)
+    assert np.array_equal(got, want)
+    assert vol == int(want.sum())
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
@@ -134,7 +160,6 @@ def test_two_process_gloo_banded_reach():
 def test_cross_band_label_merge_matches_whole_image(world, w, h, d):
     # band-local oracle labels + merge_band_labels + the relabel rule must give the
     # whole-image ccl::label labels (canonical max index + 1)
-    from paper_2010_07284_b200.bands import band_rows, merge_band_labels
     a = O.random_mask(w, h, d, O.Rng(w * h + world))
     bands = [a[slice(*band_rows(h, world, r))] for r in range(world)]
     local = [O.flood_fill_label(b).astype(np.uint64) for b in bands]

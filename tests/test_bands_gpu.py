@@ -87,3 +87,54 @@ def test_banded_ccl_blob_and_64bit_offsets(dev):
     u = O.threshold(0, img, 56360)
     got = LocalGroup(6).run(lambda c, b: ccl_banded(c, b).cpu().numpy(), split(dev, u, 6))
     assert np.array_equal(np.concatenate(got), O.flood_fill_label(u).astype(np.int64))
+
+
+def _storage_bytes(img):
+    from paper_2010_07284_b200.bands import device_bytes
+    ptr, pitch, _ = img.storage()
+    return device_bytes(ptr, pitch * img.height, img.device.device)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_banded_c5_scale_equals_whole_image(dev, world):
+    """Config 5's banded path at the largest size a single image still labels in
+    32 bits (65535^2, image.cpp:26-28): banded near^4 / volume / reach / ccl equal
+    the whole-image kernels bit for bit (compared on the device)."""
+    import torch
+    from paper_2010_07284_b200 import ccl
+    from paper_2010_07284_b200.bands import ccl_banded, device_bytes
+    from paper_2010_07284_b200.pixlog import random_mask_device
+    n = 65535
+    spans = [band_rows(n, world, r) for r in range(world)]
+    masks = [random_mask_device(n, r1 - r0, 0.5, 1, r0, dev) for r0, r1 in spans]
+    tgts = [random_mask_device(n, r1 - r0, 0.05, 2, r0, dev) for r0, r1 in spans]
+    whole_m = random_mask_device(n, n, 0.5, 1, 0, dev)
+    whole_t = random_mask_device(n, n, 0.05, 2, 0, dev)
+    grp = LocalGroup(world)
+
+    def same_rows(parts, whole):
+        dev.synchronize()  # the library's stream -> torch's
+        w_all = _storage_bytes(whole)
+        _, pitch, _ = whole.storage()
+        for (r0, r1), p in zip(spans, parts):
+            assert torch.equal(_storage_bytes(p), w_all[r0 * pitch:r1 * pitch]), (r0, r1)
+
+    # near^4 and volume
+    got = grp.run(lambda c, b: near_banded(c, b, 4), masks)
+    same_rows(got, kernels.dilateK(whole_m, 4, dev))
+    del got
+    vols = grp.run(lambda c, b: volume_banded(c, b), masks)
+    assert all(v == kernels.countTrue(whole_m, dev) for v in vols)
+    # reach
+    got = grp.run(lambda c, b: reach_banded(c, b[0], b[1]), list(zip(tgts, masks)))
+    same_rows(got, reach(whole_t, whole_m, dev))
+    del got
+    # ccl: 64-bit band labels vs the whole image's 32-bit canonical labels
+    whole_lab = ccl.label(whole_m, dev)
+    dev.synchronize()
+    ptr, _, _ = whole_lab.storage()
+    lab = device_bytes(ptr, n * n * 4, dev.device).view(torch.int32)
+    labs = grp.run(lambda c, b: ccl_banded(c, b), masks)
+    for (r0, r1), l64 in zip(spans, labs):
+        want = lab[r0 * n:r1 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(l64.view(-1), want), (r0, r1)
