@@ -14,7 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("args", [["--config", "c3"], ["--config", "c5", "--size", "8192"],
-                                  ["--config", "c2", "--depth", "20", "--alt-steps", "0"]])
+                                  ["--config", "c2", "--depth", "20", "--alt-steps", "0",
+                                   "--c5-size", "8192"]])
 def test_two_rank_bench_prints_one_line(args):
     env = dict(os.environ, BENCH_DIST_BACKEND="gloo", OMP_NUM_THREADS="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
