@@ -307,6 +307,12 @@ def _empty(nbytes: int, dev: Device):
     return torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", dev.device))
 
 
+def _zeros(nbytes: int, dev: Device):
+    """Border records: alignment gaps are sent too, so they are zero (initcheck-clean)."""
+    import torch
+    return torch.zeros(nbytes, dtype=torch.uint8, device=torch.device("cuda", dev.device))
+
+
 def near_banded(comm: Comm, band: DeviceImage, k: int = 1, erode: bool = False) -> DeviceImage:
     """near^k (or interior^k) of the full image, restricted to this band: k halo
     rows from each neighbour, then one fused near^k launch that reads them in
@@ -360,7 +366,7 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
     _check(L.slcs_reach_prepare(dev.handle, target.handle, through.handle, C.byref(st)))
     try:
         nrec = L.slcs_band_record_bytes(0, w)
-        mine = _empty(nrec, dev)
+        mine = _zeros(nrec, dev)
         _check(L.slcs_reach_border_record(st, C.c_void_p(mine.data_ptr())))
         allrec = _empty(nrec * comm.world, dev)
         comm.allgather(mine, allrec, dev)
@@ -395,7 +401,7 @@ def ccl_banded(comm: Comm, band: DeviceImage, local=None):
     nrec = L.slcs_band_record_bytes(1, w)
     allrec = None
     if comm.world > 1:
-        mine = _empty(nrec, dev)
+        mine = _zeros(nrec, dev)
         _check(L.slcs_ccl_border_record(dev.handle, local.handle, C.c_void_p(mine.data_ptr())))
         allrec = _empty(nrec * comm.world, dev)
         comm.allgather(mine, allrec, dev)
