@@ -50,10 +50,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-primitives", action="store_true",
                    help="skip the per-primitive table at 16384^2 (config 4 size)")
-    p.add_argument("--label-cse", action="store_true",
-                   help="headline with label CSE on (reaches sharing one `through` node label "
-                        "it once).  Default off: every reach node labels its own `through`, "
-                        "exactly the reference's per-node work (reach.cpp:21)")
+    p.add_argument("--no-label-cse", dest="label_cse", action="store_false",
+                   help="headline with label CSE off: every reach node labels its own "
+                        "`through` (the reference's per-node work, reach.cpp:21) in one fused "
+                        "cooperative launch per reach.  Default on: the 500 reaches of the "
+                        "chain share one labelling of `through` (computed inside every timed "
+                        "step) and run as ONE persistent launch (k_reach_chain)")
     p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                    help="BASELINE.json config: c2 (default, the headline) or the parity/"
                         "secondary workloads c1, c3 (sharded by slice under torchrun), c4")

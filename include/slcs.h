@@ -236,7 +236,9 @@ int slcs_program_destroy(slcs_program* prog);
 /* Binds the image loaded by `load` tasks with payload `name`. */
 int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* img);
 /* flags: bit 0 = capture/replay as a CUDA graph, bit 1 = disable fusion,
- * bit 2 = disable label CSE (reaches sharing one `through` node label it once). */
+ * bit 2 = disable label CSE (reaches sharing one `through` node label it once),
+ * bit 3 = disable reach chains (consecutive label-CSE reaches in one persistent
+ * cooperative launch). */
 int slcs_program_run(slcs_program* prog, int flags);
 /* Copies host pixels (reference layout) straight into the program's input
  * slot for `load` name `name` -- the end-to-end path: no intermediate image. */

@@ -1922,6 +1922,291 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
 }
 
 
+// ---- chains of reaches against ONE labelling: one persistent launch ----------------
+// The config-2 chain  x -> near -> reach(., u) -> near -> reach(., u) ...  runs
+// 500 reaches of ONE `through` image u.  With label CSE the program labels u
+// once (launch_labels); what is left of every reach is flag propagation:
+//   seeds   S_s = components of u touching near(T_s)
+//   select  U_s = T_s | S_s,     reach_s = near^k(U_s),  T_{s+1} = reach_s.
+// k_reach_chain keeps a grid of co-resident tiles alive for the whole chain
+// (cooperative launch, two grid barriers per reach):
+//   setup   each tile finds the global root of every run of u it owns (two
+//           loads per run, once) and gives the tile's distinct roots compact
+//           local ids (shared-memory hash); runs keep their local id.
+//   seed    the tile stages its slice of the previous U (+3-row / 1-word halo,
+//           L2) in shared memory, applies near^(a+1) (a = the previous closing
+//           radius), marks the local ids of runs touching it, then publishes
+//           one flag stamp per seeded distinct root (F[root] = gen).
+//   --- grid barrier ---
+//   select  one flag load per distinct root of the tile, U = near^a(prev) | S
+//           (same staged window), stored for the next step.
+//   --- grid barrier ---
+// No per-reach labelling, no per-run root lookups, and per step only the
+// staged window, the tile's roots' flags and the U words touch L2.  Runs of
+// tiles with more than CH_MAXL distinct roots fall back to a direct root
+// lookup (correct, slower).  Flags are the label-CSE stamps (gen = reach
+// index + 1; the labelling step zeroes them once per run).
+constexpr int CH_TW = 8;    // words per tile row (256 px)
+constexpr int CH_TB = 64;   // bands per tile (128 rows)
+constexpr int CH_THREADS = 256;
+constexpr int CH_UPT = CH_TW * CH_TB / CH_THREADS;  // units (band, word) per thread
+constexpr int CH_R = 3;                              // max stencil radius
+constexpr int CH_ROWS = 2 * CH_TB + 2 * CH_R;        // staged rows
+constexpr int CH_SW = CH_TW + 2;                     // staged words per row
+constexpr int CH_MAXL = 2048;                        // distinct roots with a local id
+constexpr int CH_HASH = 4096;
+constexpr uint16_t CH_NOL = 0xffffu;
+constexpr size_t CH_SMEM_LIDS = size_t(CH_TW) * CH_TB * 16 * 2;
+constexpr size_t CH_SMEM_ROOTS = size_t(CH_MAXL) * 4;
+constexpr size_t CH_SMEM_FLAGS = size_t(CH_MAXL);
+constexpr size_t CH_SMEM_REGION =
+    size_t(CH_HASH) * 6 > size_t(CH_ROWS) * CH_SW * 4 ? size_t(CH_HASH) * 6
+                                                      : size_t(CH_ROWS) * CH_SW * 4;
+constexpr size_t CH_SMEM = CH_SMEM_LIDS + CH_SMEM_ROOTS + CH_SMEM_FLAGS + CH_SMEM_REGION;
+
+struct ChainArgs {
+  const uint32_t* x;  // target of the first reach
+  const uint32_t* u;  // through
+  const uint32_t* P;  // labelling of u (launch_labels)
+  uint32_t* F;        // flag stamps per 2x2 block
+  uint32_t* buf0;     // U ping-pong
+  uint32_t* buf1;
+  uint32_t* out;      // near^klast(U of the last reach)
+  int steps;
+  int kmid;           // closing radius of every reach but the last (0..2)
+  int klast;          // closing radius of the last reach (1..8 -> clamp 3 here)
+  uint32_t gen0;      // flag stamp of the first reach
+};
+
+// rows lr and lr + 1 of the staged window, dilated by R (clipped window, the
+// staged zeros stand for out-of-image pixels)
+template <int R>
+__device__ __forceinline__ void ch_near2(const uint32_t* st, int lr, int lw, uint32_t& o0,
+                                         uint32_t& o1) {
+  uint32_t h[2 * R + 2];
+#pragma unroll
+  for (int i = 0; i < 2 * R + 2; ++i) {
+    const uint32_t* p = st + (lr - R + i) * CH_SW + lw;
+    const uint32_t c = p[0];
+    uint32_t d = c;
+    if (R > 0) {
+      const uint32_t l = p[-1], r = p[1];
+#pragma unroll
+      for (int k = 1; k <= R; ++k) d |= __funnelshift_l(l, c, k) | __funnelshift_r(c, r, k);
+    }
+    h[i] = d;
+  }
+  uint32_t a = h[0], b = h[2 * R + 1];
+#pragma unroll
+  for (int i = 1; i <= 2 * R; ++i) {
+    a |= h[i];
+    b |= h[i];
+  }
+  o0 = a;
+  o1 = b;
+}
+
+__device__ __forceinline__ void ch_near2_dyn(const uint32_t* st, int lr, int lw, int R,
+                                             uint32_t& o0, uint32_t& o1) {
+  switch (R) {
+    case 0: ch_near2<0>(st, lr, lw, o0, o1); break;
+    case 1: ch_near2<1>(st, lr, lw, o0, o1); break;
+    case 2: ch_near2<2>(st, lr, lw, o0, o1); break;
+    default: ch_near2<3>(st, lr, lw, o0, o1); break;
+  }
+}
+
+__device__ __forceinline__ uint32_t ch_hash(uint32_t key) { return (key * 0x9E3779B1u) >> 20; }
+
+__global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g) {
+  slcs_pdl_wait();
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint16_t* lids = reinterpret_cast<uint16_t*>(smem);
+  uint32_t* lroot = reinterpret_cast<uint32_t*>(smem + CH_SMEM_LIDS);
+  uint8_t* lflag = smem + CH_SMEM_LIDS + CH_SMEM_ROOTS;
+  unsigned char* region = smem + CH_SMEM_LIDS + CH_SMEM_ROOTS + CH_SMEM_FLAGS;
+  uint32_t* hkeys = reinterpret_cast<uint32_t*>(region);
+  uint16_t* hlid = reinterpret_cast<uint16_t*>(region + size_t(CH_HASH) * 4);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(region);
+  __shared__ int nl_sh;
+
+  const int tid = threadIdx.x;
+  const int tiles_x = (int(g.pitch) + CH_TW - 1) / CH_TW;
+  const int j0 = (int(blockIdx.x) % tiles_x) * CH_TW;
+  const int k0 = (int(blockIdx.x) / tiles_x) * CH_TB;
+  const uint32_t EMPTYK = 0xffffffffu;
+
+  // ---- setup: runs of u, their roots, compact local ids ----
+  for (int i = tid; i < CH_HASH; i += CH_THREADS) hkeys[i] = EMPTYK;
+  if (tid == 0) nl_sh = 0;
+  uint32_t T[CH_UPT], B[CH_UPT];
+#pragma unroll
+  for (int q = 0; q < CH_UPT; ++q) {
+    const int unit = tid + q * CH_THREADS;
+    const int k = k0 + unit / CH_TW, j = j0 + unit % CH_TW;
+    T[q] = B[q] = 0u;
+    if (k < g.BH && j < g.wpr) {
+      const uint32_t* row = a.u + size_t(2 * k) * g.pitch + j;
+      T[q] = __ldg(row);
+      B[q] = 2 * k + 1 < g.H ? __ldg(row + g.pitch) : 0u;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < CH_UPT; ++q) {
+    const int unit = tid + q * CH_THREADS;
+    const int k = k0 + unit / CH_TW, j = j0 + unit % CH_TW;
+    for (uint32_t x = T[q] | B[q]; x;) {
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      const uint32_t rb = gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q], m)));
+      uint32_t h = ch_hash(rb);
+      for (int probe = 0; probe < CH_HASH; ++probe, h = (h + 1) & (CH_HASH - 1)) {
+        const uint32_t old = atomicCAS(hkeys + h, EMPTYK, rb);
+        if (old == EMPTYK || old == rb) break;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < CH_HASH; i += CH_THREADS) {
+    if (hkeys[i] == EMPTYK) continue;
+    const int l = atomicAdd(&nl_sh, 1);
+    hlid[i] = l < CH_MAXL ? uint16_t(l) : CH_NOL;
+    if (l < CH_MAXL) lroot[l] = hkeys[i];
+  }
+  __syncthreads();
+  const int nl = min(nl_sh, CH_MAXL);
+#pragma unroll
+  for (int q = 0; q < CH_UPT; ++q) {
+    const int unit = tid + q * CH_THREADS;
+    const int k = k0 + unit / CH_TW, j = j0 + unit % CH_TW;
+    int ri = 0;
+    for (uint32_t x = T[q] | B[q]; x; ++ri) {
+      const uint32_t m = first_run(x);
+      x &= ~m;
+      const uint32_t rb = gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q], m)));
+      uint16_t l = CH_NOL;
+      uint32_t h = ch_hash(rb);
+      for (int probe = 0; probe < CH_HASH; ++probe, h = (h + 1) & (CH_HASH - 1)) {
+        const uint32_t kk = hkeys[h];
+        if (kk == rb) {
+          l = hlid[h];
+          break;
+        }
+        if (kk == EMPTYK) break;
+      }
+      lids[unit * 16 + ri] = l;
+    }
+  }
+  for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = 0;
+  __syncthreads();  // the hash region becomes the staging window
+
+  auto stage_rows = [&](const uint32_t* src) {
+    for (int i = tid; i < CH_ROWS * CH_SW; i += CH_THREADS) {
+      const int r = i / CH_SW, w = i - r * CH_SW;
+      const int gr = 2 * k0 - CH_R + r, gw = j0 - 1 + w;
+      stage[i] = (gr >= 0 && gr < g.H && gw >= 0 && gw < g.wpr)
+                     ? __ldcg(src + size_t(gr) * g.pitch + gw)
+                     : 0u;
+    }
+  };
+
+  for (int s = 0; s < a.steps; ++s) {
+    const int ra = s == 0 ? 0 : a.kmid;  // prev -> target radius
+    const uint32_t* src = s == 0 ? a.x : ((s & 1) ? a.buf0 : a.buf1);
+    uint32_t* dst = (s & 1) ? a.buf1 : a.buf0;
+    const uint32_t gen = a.gen0 + uint32_t(s);
+    stage_rows(src);
+    __syncthreads();
+    // seed: runs of u touching near(target) = near^(ra+1)(prev)
+#pragma unroll
+    for (int q = 0; q < CH_UPT; ++q) {
+      const int unit = tid + q * CH_THREADS;
+      const int kb = unit / CH_TW, jw = unit % CH_TW;
+      if (!(T[q] | B[q])) continue;
+      uint32_t n0, n1;
+      ch_near2_dyn(stage, CH_R + 2 * kb, jw + 1, ra + 1, n0, n1);
+      const uint32_t sd = (T[q] & n0) | (B[q] & n1);
+      if (!sd) continue;
+      int ri = 0;
+      for (uint32_t x = T[q] | B[q]; x; ++ri) {
+        const uint32_t m = first_run(x);
+        x &= ~m;
+        if (!(sd & m)) continue;
+        const uint16_t l = lids[unit * 16 + ri];
+        if (l != CH_NOL) {
+          lflag[l] = 1;
+        } else {
+          const int k = k0 + kb, j = j0 + jw;
+          __stcg(a.F + gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q], m))), gen);
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < nl; i += CH_THREADS)
+      if (lflag[i]) __stcg(a.F + lroot[i], gen);
+    grid.sync();
+    // select: U = near^ra(prev) | seeded components
+    for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = __ldcg(a.F + lroot[i]) == gen ? 1 : 0;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < CH_UPT; ++q) {
+      const int unit = tid + q * CH_THREADS;
+      const int kb = unit / CH_TW, jw = unit % CH_TW;
+      const int k = k0 + kb, j = j0 + jw;
+      if (k >= g.BH || j >= int(g.pitch)) continue;
+      uint32_t u0 = 0, u1 = 0;
+      if (j < g.wpr) {
+        ch_near2_dyn(stage, CH_R + 2 * kb, jw + 1, ra, u0, u1);
+        int ri = 0;
+        for (uint32_t x = T[q] | B[q]; x; ++ri) {
+          const uint32_t m = first_run(x);
+          x &= ~m;
+          const uint16_t l = lids[unit * 16 + ri];
+          const bool sel = l != CH_NOL
+                               ? lflag[l] != 0
+                               : __ldcg(a.F + gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q],
+                                                                         m)))) == gen;
+          if (sel) {
+            u0 |= T[q] & m;
+            u1 |= B[q] & m;
+          }
+        }
+        const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
+        u0 &= vm;
+        u1 &= vm;
+      }
+      __stcg(dst + size_t(2 * k) * g.pitch + j, u0);
+      if (2 * k + 1 < g.H) __stcg(dst + size_t(2 * k + 1) * g.pitch + j, u1);
+    }
+    __syncthreads();
+    for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = 0;
+    grid.sync();
+  }
+
+  // closing near of the last reach
+  const uint32_t* last = ((a.steps - 1) & 1) ? a.buf1 : a.buf0;
+  stage_rows(last);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < CH_UPT; ++q) {
+    const int unit = tid + q * CH_THREADS;
+    const int kb = unit / CH_TW, jw = unit % CH_TW;
+    const int k = k0 + kb, j = j0 + jw;
+    if (k >= g.BH || j >= int(g.pitch)) continue;
+    uint32_t o0 = 0, o1 = 0;
+    if (j < g.wpr) {
+      ch_near2_dyn(stage, CH_R + 2 * kb, jw + 1, a.klast, o0, o1);
+      const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
+      o0 &= vm;
+      o1 &= vm;
+    }
+    a.out[size_t(2 * k) * g.pitch + j] = o0;
+    if (2 * k + 1 < g.H) a.out[size_t(2 * k + 1) * g.pitch + j] = o1;
+  }
+}
+
 int grid_blocks(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -2037,6 +2322,60 @@ int launch_labels(const uint32_t* through, void* labels, const Geo& gb, cudaStre
   int launches = 0;
   large_local_and_merge(through, nullptr, g, gb.batch, s, MODE_CCL, st, launches);
   return launches;
+}
+
+bool reach_chain_fits(const Geo& gb, int steps, int kmid, int klast) {
+  if (gb.batch != 1 || steps < 1 || kmid < 0 || kmid > 2 || klast < 1 || klast > CH_R) return false;
+  static PerDevice<int> cap;
+  const int capacity = cap.get([](int dev) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaFuncSetAttribute(k_reach_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(CH_SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reach_chain, CH_THREADS, CH_SMEM) !=
+            cudaSuccess)
+      per = 0;
+    cudaGetLastError();
+    return per * sms;
+  });
+  const size_t tiles = size_t((gb.pitch + CH_TW - 1) / CH_TW) *
+                       size_t((size_t(gb.h) + 2 * CH_TB - 1) / (2 * CH_TB));
+  return tiles <= size_t(capacity);
+}
+
+int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* labels,
+                       uint32_t* flags32, uint32_t idx0, int steps, int kmid, int klast,
+                       uint32_t* out, uint32_t* tmp2, const Geo& gb, cudaStream_t st) {
+  if (!reach_chain_fits(gb, steps, kmid, klast))
+    fail(SLCS_ERR_ARG, "reach chain does not fit one cooperative launch");
+  if (idx0 + uint32_t(steps) > 4096u) fail(SLCS_ERR_ARG, "too many reaches share one labelling");
+  G g = make_g(gb);
+  ChainArgs a;
+  a.x = x;
+  a.u = through;
+  a.P = static_cast<const uint32_t*>(labels);
+  a.F = flags32;
+  a.buf0 = tmp2;
+  a.buf1 = tmp2 + gb.slice;
+  a.out = out;
+  a.steps = steps;
+  a.kmid = kmid;
+  a.klast = klast;
+  a.gen0 = idx0 + 1u;
+  const unsigned tiles = unsigned(((gb.pitch + CH_TW - 1) / CH_TW) *
+                                  ((size_t(gb.h) + 2 * CH_TB - 1) / (2 * CH_TB)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(CH_THREADS);
+  cfg.dynamicSmemBytes = CH_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, k_reach_chain, a, g), "reach chain launch");
+  return 1;
 }
 
 int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const void* labels,

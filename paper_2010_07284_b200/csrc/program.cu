@@ -104,6 +104,10 @@ struct LG {
   int num_out = -1, num_a = -1, num_b = -1;
   double ca = 0, cb = 0;
   int gen_idx = -1;  // LG_REACH against an LG_LABELS input (label CSE)
+  // label-CSE reach chain in one persistent launch (k_reach_chain): this node is
+  // the last of chain_len reaches; in[0] is the first one's target, the
+  // intermediate reaches close with near^chain_kmid, this one with near^k
+  int chain_len = 1, chain_kmid = 0, chain_idx0 = -1;
   std::string name;  // LG_INPUT
   bool dead = false, output = false;
   int group = -1;  // leader of its shared launch (EW siblings, batched small reaches)
@@ -435,7 +439,7 @@ struct slcs_program {
     return add_expr(e);
   }
 
-  void plan(int fusion, bool label_cse) {
+  void plan(int fusion, bool label_cse, bool chain) {
     release_plan();
     vals.assign(tasks.size(), Val{});
     lgs.clear();
@@ -852,6 +856,36 @@ struct slcs_program {
       }
     }
 
+    // ---- chains of label-CSE reaches (same labelling, each the next one's only
+    // input) run as ONE persistent cooperative launch (k_reach_chain) when the
+    // tile grid is co-resident: the config-2 chain's 500 reaches become 1 launch
+    if (fuse && label_cse && chain) {
+      for (LG& n : lgs) n.consumers = 0;
+      for (const LG& n : lgs)
+        if (!n.dead)
+          for (int q : n.in) lgs[q].consumers++;
+      for (LG& n : lgs) {
+        if (n.dead || n.kind != LG_REACH || n.gen_idx < 0) continue;
+        if (n.chain_idx0 < 0) n.chain_idx0 = n.gen_idx;
+        LG& m = lgs[n.in[0]];
+        if (m.dead || m.kind != LG_REACH || m.gen_idx < 0 || m.consumers != 1 || m.output ||
+            m.in[1] != n.in[1] || m.in[2] != n.in[2] || m.k > 2 ||
+            (m.chain_len > 1 && m.chain_kmid != m.k) || m.w != n.w || m.h != n.h ||
+            m.batch != n.batch)
+          continue;
+        const int idx0 = m.chain_idx0 < 0 ? m.gen_idx : m.chain_idx0;
+        if (n.gen_idx != idx0 + m.chain_len) continue;
+        if (!reach_chain_fits(bool_geo(n.w, n.h, n.batch), m.chain_len + 1, m.k,
+                              std::max(1, n.k)))
+          continue;
+        n.chain_len = m.chain_len + 1;
+        n.chain_kmid = m.k;
+        n.chain_idx0 = idx0;
+        n.in[0] = m.in[0];
+        m.dead = true;
+      }
+    }
+
     // ---- small-image maxvol absorbs a bool-only elementwise operand (prologue)
     // and a bool-only elementwise consumer (epilogue): k_small evaluates them
     // per word, so grow -> maxvol -> "| surrounded" (C3) is one launch
@@ -1066,7 +1100,8 @@ struct slcs_program {
         n.offset = alloc(n.bytes);
       }
       if (n.kind == LG_REACH && n.gen_idx >= 0) {
-        scratch_need = std::max(scratch_need, bool_geo(n.w, n.h, n.batch).slice * n.batch * 4);
+        scratch_need = std::max(scratch_need, bool_geo(n.w, n.h, n.batch).slice * n.batch * 4 *
+                                                  (n.chain_len > 1 ? 2 : 1));
       } else if (n.kind == LG_REACH) {
         size_t s = ccl_scratch_bytes(n.w, n.h, n.batch, true, false);
         if (!ccl_small_path(n.w, n.h)) s += bool_geo(n.w, n.h, n.batch).slice * n.batch * 4;
@@ -1130,6 +1165,9 @@ struct slcs_program {
       if (n.group >= 0)
         os << (n.group == q ? " [launch group lead]" : " [with step " + std::to_string(n.group) + "]");
       if (n.kind == LG_REACH && n.gen_idx >= 0) os << " (shared labelling)";
+      if (n.kind == LG_REACH && n.chain_len > 1)
+        os << " chain of " << n.chain_len << " reaches (one persistent launch, inner closing near^"
+           << n.chain_kmid << ")";
       if (n.kind == LG_REACH && n.tk > 0) os << " target near^" << n.tk;
       if (n.kind == LG_REACH && n.k == 0) os << " emits selection";
       if (n.kind == LG_REACH && n.k > 1) os << " closing near^" << n.k;
@@ -1291,6 +1329,17 @@ struct slcs_program {
             launches += launch_reach_small_multi(tg, th, ou, int(members.size()), gb, st);
             break;
           }
+          if (n.gen_idx >= 0 && n.chain_len > 1) {
+            const LG& lab = lgs[n.in[2]];
+            size_t lb = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256);
+            launches += launch_reach_chain(
+                static_cast<const uint32_t*>(lgs[n.in[0]].ptr),
+                static_cast<const uint32_t*>(lgs[n.in[1]].ptr), lab.ptr,
+                reinterpret_cast<uint32_t*>(static_cast<char*>(lab.ptr) + lb),
+                uint32_t(n.chain_idx0), n.chain_len, n.chain_kmid, std::max(1, n.k),
+                static_cast<uint32_t*>(n.ptr), static_cast<uint32_t*>(scratch), gb, st);
+            break;
+          }
           if (n.gen_idx >= 0) {
             const LG& lab = lgs[n.in[2]];
             size_t lb = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256);
@@ -1366,8 +1415,9 @@ struct slcs_program {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     const int fusion = (flags & 2) ? 0 : 1;
     const bool label_cse = fusion && !(flags & 4);
-    const int mode = fusion | (label_cse ? 2 : 0);
-    if (!planned || planned_fusion != mode) plan(fusion, label_cse);
+    const bool chain = label_cse && !(flags & 8);
+    const int mode = fusion | (label_cse ? 2 : 0) | (chain ? 4 : 0);
+    if (!planned || planned_fusion != mode) plan(fusion, label_cse, chain);
     planned_fusion = mode;
     // order after work already queued on the context stream
     cuda_check(cudaEventRecord(ev_in, ctx->stream), "event");

@@ -276,6 +276,13 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
                          uint32_t* flags32, uint32_t idx, uint32_t* out,
                          uint32_t* tmp_bits, const Geo& gb, cudaStream_t st, int k_out = 1);
 
+// a chain of `steps` reaches on one labelling (label CSE) in ONE cooperative
+// launch: reach s (idx0 + s) targets near^kmid of the previous selection (the
+// first targets x), the last closes with near^klast; tmp2 = two bool images
+bool reach_chain_fits(const Geo& gb, int steps, int kmid, int klast);
+int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* labels,
+                       uint32_t* flags32, uint32_t idx0, int steps, int kmid, int klast,
+                       uint32_t* out, uint32_t* tmp2, const Geo& gb, cudaStream_t st);
 int launch_reach_set_flags_dev(const CclScratch& s, const Geo& gb, const uint32_t* roots,
                                const int* n_dev, int max_n, cudaStream_t st);
 

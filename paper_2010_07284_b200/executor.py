@@ -27,6 +27,7 @@ from .pixlog import (_DTYPE, Device, DeviceImage, ImageBuffer, PixelKind, RunErr
 FLAG_GRAPH = 1
 FLAG_NO_FUSION = 2
 FLAG_NO_LABEL_CSE = 4
+FLAG_NO_CHAIN = 8
 
 
 def format_number(v: float) -> str:
@@ -44,6 +45,7 @@ class RunOptions:
     fusion: bool = True
     cuda_graph: bool = True
     label_cse: bool = True
+    chain: bool = True
     # RunOptions::baseDir (executor.hpp:16-26): when set, `load` paths not supplied
     # in `images` are read as PNG from here and every `save` writes its PNG here
     baseDir: Optional[str] = None
@@ -109,9 +111,10 @@ class Program:
         _check(_lib.load().slcs_program_set_input_host(self.handle, name.encode(), int(kind), w,
                                                        h, b, C.c_void_p(a.ctypes.data)))
 
-    def run(self, fusion: bool = True, cuda_graph: bool = True, label_cse: bool = True) -> None:
+    def run(self, fusion: bool = True, cuda_graph: bool = True, label_cse: bool = True,
+            chain: bool = True) -> None:
         flags = ((FLAG_GRAPH if cuda_graph else 0) | (0 if fusion else FLAG_NO_FUSION)
-                 | (0 if label_cse else FLAG_NO_LABEL_CSE))
+                 | (0 if label_cse else FLAG_NO_LABEL_CSE) | (0 if chain else FLAG_NO_CHAIN))
         _check(_lib.load().slcs_program_run(self.handle, flags))
 
     def result(self, task: int) -> Union[DeviceImage, float]:
@@ -162,7 +165,7 @@ def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) ->
     t0 = time.perf_counter()
     err: Optional[RunError] = None
     try:
-        prog.run(options.fusion, options.cuda_graph, options.label_cse)
+        prog.run(options.fusion, options.cuda_graph, options.label_cse, options.chain)
     except RunError as e:
         err = e
     prog.device.synchronize()

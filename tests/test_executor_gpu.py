@@ -398,3 +398,33 @@ def test_nan_and_inf_prints_match_reference_executor(dev):
     want = R.run(spec, {"m.png": img}, STDLIB)["prints"]
     rep = run_text(spec, {"m.png": B(img)})
     assert rep.printLines == want
+
+
+@pytest.mark.parametrize("w,h,depth", [(700, 500, 20), (1000, 1001, 12), (4100, 37, 9),
+                                       (300, 2600, 30), (2048, 2048, 41)])
+def test_reach_chain_one_launch_matches_oracle(dev, w, h, depth):
+    """The config-2 chain with label CSE runs its reaches as ONE persistent launch
+    (k_reach_chain); results equal the unchained label-CSE path, the per-reach
+    fused path, and the CPU oracle of the same chain."""
+    from paper_2010_07284_b200 import synth as S
+    img = O.blob_noise(w, h, 5)
+    graph = compile_text(S.near_reach_chain(depth))
+    out_task = [i for i, t in enumerate(graph.nodes) if t.opcode == "save"][0]
+    res = {}
+    for name, kw in {"chain": {}, "cse": {"chain": False}, "fused": {"label_cse": False}}.items():
+        prog = Program(graph, dev)
+        prog.set_input_host("img.png", img, PixelKind.U16)
+        for _ in range(2):
+            prog.run(**kw)
+        out = np.zeros((h, w), np.uint8)
+        prog.download(out_task, out)
+        res[name] = out
+        if name == "chain":
+            assert "chain of" in prog.plan, prog.plan
+    b = O.threshold(0, img, 56360)
+    x = O.threshold(0, img, 62258)
+    for k in range(depth):
+        x = O.dilate(x) if k % 2 == 0 else O.reach(x, b)
+    assert np.array_equal(res["chain"], x)
+    assert np.array_equal(res["cse"], x)
+    assert np.array_equal(res["fused"], x)
