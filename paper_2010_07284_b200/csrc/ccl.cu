@@ -1946,73 +1946,85 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
 // tiles with more than CH_MAXL distinct roots fall back to a direct root
 // lookup (correct, slower).  Flags are the label-CSE stamps (gen = reach
 // index + 1; the labelling step zeroes them once per run).
-constexpr int CH_TW = 8;    // words per tile row (256 px)
-constexpr int CH_TB = 64;   // bands per tile (128 rows)
-constexpr int CH_THREADS = 256;
-constexpr int CH_UPT = CH_TW * CH_TB / CH_THREADS;  // units (band, word) per thread
-constexpr int CH_R = 3;                              // max stencil radius
-constexpr int CH_ROWS = 2 * CH_TB + 2 * CH_R;        // staged rows
-constexpr int CH_SW = CH_TW + 2;                     // staged words per row
-constexpr int CH_MAXL = 2048;                        // distinct roots with a local id
+constexpr int CH_TW = 8;     // words per tile row (256 px)
+constexpr int CH_TB = 56;    // bands per tile (112 rows): 4096^2 -> 16 x 37 = 592 tiles = 4 per SM
+constexpr int CH_THREADS = CH_TW * CH_TB / 2;  // a thread owns two stacked bands of one word
+constexpr int CH_R = 3;                       // max stencil radius
+constexpr int CH_ROWS = 2 * CH_TB + 2 * CH_R;  // staged rows
+constexpr int CH_SW = 16;     // staged row stride: halo word, 8 words (16 B aligned), halo word
+constexpr int CH_C0 = 4;      // column of the tile's first word in a staged row
+constexpr int CH_MAXL = 2048;  // distinct roots with a local id
 constexpr int CH_HASH = 4096;
 constexpr uint16_t CH_NOL = 0xffffu;
 constexpr size_t CH_SMEM_LIDS = size_t(CH_TW) * CH_TB * 16 * 2;
 constexpr size_t CH_SMEM_ROOTS = size_t(CH_MAXL) * 4;
 constexpr size_t CH_SMEM_FLAGS = size_t(CH_MAXL);
-constexpr size_t CH_SMEM_REGION =
-    size_t(CH_HASH) * 6 > size_t(CH_ROWS) * CH_SW * 4 ? size_t(CH_HASH) * 6
-                                                      : size_t(CH_ROWS) * CH_SW * 4;
+constexpr size_t CH_SMEM_STAGE = size_t(CH_ROWS) * CH_SW * 4;
+constexpr size_t CH_SMEM_HROWS = 2 * size_t(CH_ROWS) * CH_TW * 4;  // H_a, H_(a+1)
+constexpr size_t CH_SMEM_REGION = size_t(CH_HASH) * 6 > CH_SMEM_STAGE + CH_SMEM_HROWS
+                                      ? size_t(CH_HASH) * 6
+                                      : CH_SMEM_STAGE + CH_SMEM_HROWS;
 constexpr size_t CH_SMEM = CH_SMEM_LIDS + CH_SMEM_ROOTS + CH_SMEM_FLAGS + CH_SMEM_REGION;
+// a tile's halo record (u64 = step tag << 32 | word): its top 3 rows and bottom 3
+// rows (8 words each), its first and last word of every row
+constexpr int CH_H_TOP = 0, CH_H_BOT = 3 * CH_TW, CH_H_LEFT = 6 * CH_TW,
+              CH_H_RIGHT = 6 * CH_TW + 2 * CH_TB, CH_HALO = 6 * CH_TW + 4 * CH_TB;
 
 struct ChainArgs {
   const uint32_t* x;  // target of the first reach
   const uint32_t* u;  // through
   const uint32_t* P;  // labelling of u (launch_labels)
-  uint32_t* F;        // flag stamps per 2x2 block
-  uint32_t* buf0;     // U ping-pong
-  uint32_t* buf1;
+  uint32_t* F;        // flag stamps per 2x2 block, two copies (step parity)
+  unsigned long long* halo;  // per tile: its boundary words of every step, tagged (ch_halo)
   uint32_t* out;      // near^klast(U of the last reach)
   int steps;
   int kmid;           // closing radius of every reach but the last (0..2)
-  int klast;          // closing radius of the last reach (1..8 -> clamp 3 here)
+  int klast;          // closing radius of the last reach (1..3)
   uint32_t gen0;      // flag stamp of the first reach
+  unsigned long long* ts;  // diagnostics (SLCS_PHASE_TIMING=1): per CTA phase ns sums, or null
 };
 
-// rows lr and lr + 1 of the staged window, dilated by R (clipped window, the
-// staged zeros stand for out-of-image pixels)
-template <int R>
-__device__ __forceinline__ void ch_near2(const uint32_t* st, int lr, int lw, uint32_t& o0,
-                                         uint32_t& o1) {
-  uint32_t h[2 * R + 2];
-#pragma unroll
-  for (int i = 0; i < 2 * R + 2; ++i) {
-    const uint32_t* p = st + (lr - R + i) * CH_SW + lw;
-    const uint32_t c = p[0];
-    uint32_t d = c;
-    if (R > 0) {
-      const uint32_t l = p[-1], r = p[1];
-#pragma unroll
-      for (int k = 1; k <= R; ++k) d |= __funnelshift_l(l, c, k) | __funnelshift_r(c, r, k);
-    }
-    h[i] = d;
-  }
-  uint32_t a = h[0], b = h[2 * R + 1];
-#pragma unroll
-  for (int i = 1; i <= 2 * R; ++i) {
-    a |= h[i];
-    b |= h[i];
-  }
-  o0 = a;
-  o1 = b;
+__device__ __forceinline__ unsigned long long ch_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
-__device__ __forceinline__ void ch_near2_dyn(const uint32_t* st, int lr, int lw, int R,
-                                             uint32_t& o0, uint32_t& o1) {
+// horizontal dilations of staged word (row r, column c) by R and R + 1 bits
+template <int R>
+__device__ __forceinline__ void ch_hdil2(const uint32_t* st, int r, int c, uint32_t& da,
+                                         uint32_t& db) {
+  const uint32_t* p = st + r * CH_SW + c;
+  const uint32_t m = p[0], l = p[-1], rr = p[1];
+  uint32_t d = m;
+#pragma unroll
+  for (int k = 1; k <= R; ++k) d |= __funnelshift_l(l, m, k) | __funnelshift_r(m, rr, k);
+  da = d;
+  db = d | __funnelshift_l(l, m, R + 1) | __funnelshift_r(m, rr, R + 1);
+}
+
+// rows r0 .. r0+3 of a vertical R-window OR over the per-row dilations H
+template <int R>
+__device__ __forceinline__ void ch_vwin4(const uint32_t* H, int r0, int c, uint32_t (&o)[4]) {
+  uint32_t v[4 + 2 * R];
+#pragma unroll
+  for (int i = 0; i < 4 + 2 * R; ++i) v[i] = H[(r0 - R + i) * CH_TW + c];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t acc = v[q];
+#pragma unroll
+    for (int i = 1; i <= 2 * R; ++i) acc |= v[q + i];
+    o[q] = acc;
+  }
+}
+
+__device__ __forceinline__ void ch_vwin4_dyn(const uint32_t* H, int r0, int c, int R,
+                                             uint32_t (&o)[4]) {
   switch (R) {
-    case 0: ch_near2<0>(st, lr, lw, o0, o1); break;
-    case 1: ch_near2<1>(st, lr, lw, o0, o1); break;
-    case 2: ch_near2<2>(st, lr, lw, o0, o1); break;
-    default: ch_near2<3>(st, lr, lw, o0, o1); break;
+    case 0: ch_vwin4<0>(H, r0, c, o); break;
+    case 1: ch_vwin4<1>(H, r0, c, o); break;
+    case 2: ch_vwin4<2>(H, r0, c, o); break;
+    default: ch_vwin4<3>(H, r0, c, o); break;
   }
 }
 
@@ -2029,22 +2041,26 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   uint32_t* hkeys = reinterpret_cast<uint32_t*>(region);
   uint16_t* hlid = reinterpret_cast<uint16_t*>(region + size_t(CH_HASH) * 4);
   uint32_t* stage = reinterpret_cast<uint32_t*>(region);
+  uint32_t* Ha = reinterpret_cast<uint32_t*>(region + CH_SMEM_STAGE);  // [row][word]
+  uint32_t* Hb = Ha + CH_ROWS * CH_TW;
   __shared__ int nl_sh;
 
   const int tid = threadIdx.x;
   const int tiles_x = (int(g.pitch) + CH_TW - 1) / CH_TW;
   const int j0 = (int(blockIdx.x) % tiles_x) * CH_TW;
   const int k0 = (int(blockIdx.x) / tiles_x) * CH_TB;
+  const int jw = tid % CH_TW, kb0 = 2 * (tid / CH_TW);  // bands kb0, kb0 + 1 of word jw
+  const int j = j0 + jw;
   const uint32_t EMPTYK = 0xffffffffu;
+  const unsigned long long t_start = (a.ts != nullptr && tid == 0) ? ch_now() : 0ull;
 
   // ---- setup: runs of u, their roots, compact local ids ----
   for (int i = tid; i < CH_HASH; i += CH_THREADS) hkeys[i] = EMPTYK;
   if (tid == 0) nl_sh = 0;
-  uint32_t T[CH_UPT], B[CH_UPT];
+  uint32_t T[2], B[2];
 #pragma unroll
-  for (int q = 0; q < CH_UPT; ++q) {
-    const int unit = tid + q * CH_THREADS;
-    const int k = k0 + unit / CH_TW, j = j0 + unit % CH_TW;
+  for (int q = 0; q < 2; ++q) {
+    const int k = k0 + kb0 + q;
     T[q] = B[q] = 0u;
     if (k < g.BH && j < g.wpr) {
       const uint32_t* row = a.u + size_t(2 * k) * g.pitch + j;
@@ -2054,9 +2070,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < CH_UPT; ++q) {
-    const int unit = tid + q * CH_THREADS;
-    const int k = k0 + unit / CH_TW, j = j0 + unit % CH_TW;
+  for (int q = 0; q < 2; ++q) {
+    const int k = k0 + kb0 + q;
     for (uint32_t x = T[q] | B[q]; x;) {
       const uint32_t m = first_run(x);
       x &= ~m;
@@ -2078,9 +2093,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   __syncthreads();
   const int nl = min(nl_sh, CH_MAXL);
 #pragma unroll
-  for (int q = 0; q < CH_UPT; ++q) {
-    const int unit = tid + q * CH_THREADS;
-    const int k = k0 + unit / CH_TW, j = j0 + unit % CH_TW;
+  for (int q = 0; q < 2; ++q) {
+    const int k = k0 + kb0 + q, unit = (kb0 + q) * CH_TW + jw;
     int ri = 0;
     for (uint32_t x = T[q] | B[q]; x; ++ri) {
       const uint32_t m = first_run(x);
@@ -2101,109 +2115,210 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   }
   for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = 0;
   __syncthreads();  // the hash region becomes the staging window
+  unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0}, tprev = 0;
+  const bool timing = a.ts != nullptr && tid == 0;
+  auto mark = [&](int ph) {
+    if (timing) {
+      const unsigned long long t = ch_now();
+      tacc[ph] += t - tprev;
+      tprev = t;
+    }
+  };
+  if (timing) {
+    tprev = ch_now();
+    tacc[0] = tprev - t_start;
+  }
 
+  // stage rows [2 k0 - 3, 2 k0 + 2 CH_TB + 3) of the first target: two 16 B loads
+  // per row for the tile's 8 words, one word of halo on each side; zeros outside
   auto stage_rows = [&](const uint32_t* src) {
-    for (int i = tid; i < CH_ROWS * CH_SW; i += CH_THREADS) {
-      const int r = i / CH_SW, w = i - r * CH_SW;
-      const int gr = 2 * k0 - CH_R + r, gw = j0 - 1 + w;
-      stage[i] = (gr >= 0 && gr < g.H && gw >= 0 && gw < g.wpr)
-                     ? __ldcg(src + size_t(gr) * g.pitch + gw)
-                     : 0u;
+    for (int i = tid; i < CH_ROWS * 4; i += CH_THREADS) {
+      const int r = i >> 2, part = i & 3;
+      const int gr = 2 * k0 - CH_R + r;
+      const bool in_row = gr >= 0 && gr < g.H;
+      const uint32_t* row = src + size_t(gr) * g.pitch;
+      uint32_t* dst = stage + r * CH_SW;
+      if (part < 2) {
+        const int w = j0 + 4 * part;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (in_row && w < int(g.pitch)) v = __ldcg(reinterpret_cast<const uint4*>(row + w));
+        *reinterpret_cast<uint4*>(dst + CH_C0 + 4 * part) = v;
+      } else if (part == 2) {
+        dst[CH_C0 - 1] = in_row && j0 > 0 ? __ldcg(row + j0 - 1) : 0u;
+      } else {
+        dst[CH_C0 + CH_TW] = in_row && j0 + CH_TW < g.wpr ? __ldcg(row + j0 + CH_TW) : 0u;
+      }
+    }
+  };
+  // later steps: the tile's own rows are already in the window (its select wrote
+  // them); the neighbours' boundary words come from their halo records, each
+  // word tagged with its step, so waiting for the data IS the synchronisation
+  // (no grid barrier between a step's select and the next step's seed)
+  const int tx = int(blockIdx.x) % tiles_x, ty = int(blockIdx.x) / tiles_x;
+  const int tiles_y = (g.BH + CH_TB - 1) / CH_TB;
+  auto halo_word = [&](int ntx, int nty, int idx, unsigned long long tag) -> uint32_t {
+    if (ntx < 0 || ntx >= tiles_x || nty < 0 || nty >= tiles_y) return 0u;
+    const unsigned long long* p =
+        a.halo + (size_t(nty) * tiles_x + ntx) * CH_HALO + size_t(idx);
+    for (int spin = 0;; ++spin) {
+      const unsigned long long v = __ldcg(p);
+      if ((v >> 32) == tag) return uint32_t(v);
+      if (spin > (1 << 22)) __trap();  // a producer never arrived: fail, never hang
+    }
+  };
+  auto stage_halo = [&](unsigned long long tag) {
+    // rows above (the tile above's bottom rows), rows below (the tile below's top
+    // rows), 10 words each; the left / right halo word of the tile's own rows
+    for (int i = tid; i < 6 * (CH_TW + 2) + 2 * 2 * CH_TB; i += CH_THREADS) {
+      if (i < 6 * (CH_TW + 2)) {
+        const int rr = i / (CH_TW + 2), c = i - rr * (CH_TW + 2);  // c: staged col - (C0-1)
+        const bool above = rr < 3;
+        const int r = above ? rr : CH_R + 2 * CH_TB + (rr - 3);
+        const int nty = above ? ty - 1 : ty + 1;
+        const int base = above ? CH_H_BOT + rr * CH_TW : CH_H_TOP + (rr - 3) * CH_TW;
+        uint32_t v;
+        if (c == 0) v = halo_word(tx - 1, nty, base + CH_TW - 1, tag);
+        else if (c == CH_TW + 1) v = halo_word(tx + 1, nty, base, tag);
+        else v = halo_word(tx, nty, base + c - 1, tag);
+        stage[r * CH_SW + CH_C0 - 1 + c] = v;
+      } else {
+        const int q = i - 6 * (CH_TW + 2);
+        const int row = q >> 1, right = q & 1;
+        const uint32_t v = right ? halo_word(tx + 1, ty, CH_H_LEFT + row, tag)
+                                 : halo_word(tx - 1, ty, CH_H_RIGHT + row, tag);
+        stage[(CH_R + row) * CH_SW + (right ? CH_C0 + CH_TW : CH_C0 - 1)] = v;
+      }
+    }
+  };
+  unsigned long long* my_halo = a.halo + size_t(blockIdx.x) * CH_HALO;
+
+  // per staged row, the tile's words dilated horizontally by ra and ra + 1
+  auto hrows = [&](int ra) {
+    for (int i = tid; i < CH_ROWS * CH_TW; i += CH_THREADS) {
+      const int r = i / CH_TW, c = i - r * CH_TW;
+      switch (ra) {
+        case 0: ch_hdil2<0>(stage, r, CH_C0 + c, Ha[i], Hb[i]); break;
+        case 1: ch_hdil2<1>(stage, r, CH_C0 + c, Ha[i], Hb[i]); break;
+        case 2: ch_hdil2<2>(stage, r, CH_C0 + c, Ha[i], Hb[i]); break;
+        default: ch_hdil2<3>(stage, r, CH_C0 + c, Ha[i], Hb[i]); break;
+      }
     }
   };
 
+  const int lr0 = CH_R + 2 * kb0;  // staged row of this thread's first row
   for (int s = 0; s < a.steps; ++s) {
     const int ra = s == 0 ? 0 : a.kmid;  // prev -> target radius
-    const uint32_t* src = s == 0 ? a.x : ((s & 1) ? a.buf0 : a.buf1);
-    uint32_t* dst = (s & 1) ? a.buf1 : a.buf0;
     const uint32_t gen = a.gen0 + uint32_t(s);
-    stage_rows(src);
+    uint32_t* F = a.F + (s & 1) * size_t(g.sb);  // step parity: a fast tile seeding
+                                                 // step s+1 never touches step s's flags
+    if (s == 0) stage_rows(a.x);
+    else stage_halo((unsigned long long)s);
     __syncthreads();
+    mark(6);
+    hrows(ra);
+    __syncthreads();
+    mark(1);
     // seed: runs of u touching near(target) = near^(ra+1)(prev)
+    if (T[0] | B[0] | T[1] | B[1]) {
+      uint32_t n[4];
+      ch_vwin4_dyn(Hb, lr0, jw, ra + 1, n);
 #pragma unroll
-    for (int q = 0; q < CH_UPT; ++q) {
-      const int unit = tid + q * CH_THREADS;
-      const int kb = unit / CH_TW, jw = unit % CH_TW;
-      if (!(T[q] | B[q])) continue;
-      uint32_t n0, n1;
-      ch_near2_dyn(stage, CH_R + 2 * kb, jw + 1, ra + 1, n0, n1);
-      const uint32_t sd = (T[q] & n0) | (B[q] & n1);
-      if (!sd) continue;
-      int ri = 0;
-      for (uint32_t x = T[q] | B[q]; x; ++ri) {
-        const uint32_t m = first_run(x);
-        x &= ~m;
-        if (!(sd & m)) continue;
-        const uint16_t l = lids[unit * 16 + ri];
-        if (l != CH_NOL) {
-          lflag[l] = 1;
-        } else {
-          const int k = k0 + kb, j = j0 + jw;
-          __stcg(a.F + gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q], m))), gen);
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t sd = (T[q] & n[2 * q]) | (B[q] & n[2 * q + 1]);
+        if (!sd) continue;
+        const int unit = (kb0 + q) * CH_TW + jw;
+        int ri = 0;
+        for (uint32_t x = T[q] | B[q]; x; ++ri) {
+          const uint32_t m = first_run(x);
+          x &= ~m;
+          if (!(sd & m)) continue;
+          const uint16_t l = lids[unit * 16 + ri];
+          if (l != CH_NOL) {
+            lflag[l] = 1;
+          } else {
+            __stcg(F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))), gen);
+          }
         }
       }
     }
     __syncthreads();
     for (int i = tid; i < nl; i += CH_THREADS)
-      if (lflag[i]) __stcg(a.F + lroot[i], gen);
+      if (lflag[i]) __stcg(F + lroot[i], gen);
+    mark(2);
     grid.sync();
+    mark(3);
     // select: U = near^ra(prev) | seeded components
-    for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = __ldcg(a.F + lroot[i]) == gen ? 1 : 0;
+    for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = __ldcg(F + lroot[i]) == gen ? 1 : 0;
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < CH_UPT; ++q) {
-      const int unit = tid + q * CH_THREADS;
-      const int kb = unit / CH_TW, jw = unit % CH_TW;
-      const int k = k0 + kb, j = j0 + jw;
-      if (k >= g.BH || j >= int(g.pitch)) continue;
-      uint32_t u0 = 0, u1 = 0;
+    uint32_t uo_keep[4] = {0u, 0u, 0u, 0u};
+    if (j < int(g.pitch)) {
+      uint32_t (&uo)[4] = uo_keep;
       if (j < g.wpr) {
-        ch_near2_dyn(stage, CH_R + 2 * kb, jw + 1, ra, u0, u1);
-        int ri = 0;
-        for (uint32_t x = T[q] | B[q]; x; ++ri) {
-          const uint32_t m = first_run(x);
-          x &= ~m;
-          const uint16_t l = lids[unit * 16 + ri];
-          const bool sel = l != CH_NOL
-                               ? lflag[l] != 0
-                               : __ldcg(a.F + gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q],
-                                                                         m)))) == gen;
-          if (sel) {
-            u0 |= T[q] & m;
-            u1 |= B[q] & m;
+        ch_vwin4_dyn(Ha, lr0, jw, ra, uo);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int unit = (kb0 + q) * CH_TW + jw;
+          int ri = 0;
+          for (uint32_t x = T[q] | B[q]; x; ++ri) {
+            const uint32_t m = first_run(x);
+            x &= ~m;
+            const uint16_t l = lids[unit * 16 + ri];
+            const bool sel =
+                l != CH_NOL ? lflag[l] != 0
+                            : __ldcg(F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q],
+                                                                    B[q], m)))) == gen;
+            if (sel) {
+              uo[2 * q] |= T[q] & m;
+              uo[2 * q + 1] |= B[q] & m;
+            }
           }
         }
         const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
-        u0 &= vm;
-        u1 &= vm;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) uo[i] &= vm;
       }
-      __stcg(dst + size_t(2 * k) * g.pitch + j, u0);
-      if (2 * k + 1 < g.H) __stcg(dst + size_t(2 * k + 1) * g.pitch + j, u1);
+    }
+    // the next window's own rows (stage is free: this step read it through Ha/Hb),
+    // and this tile's boundary words for its neighbours, tagged with the step
+#pragma unroll
+    for (int i = 0; i < 4; ++i) stage[(lr0 + i) * CH_SW + CH_C0 + jw] = uo_keep[i];
+    {
+      const unsigned long long tag = (unsigned long long)(s + 1) << 32;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 2 * kb0 + i;  // tile-relative
+        const unsigned long long v = tag | uo_keep[i];
+        if (row < 3) __stcg(my_halo + CH_H_TOP + row * CH_TW + jw, v);
+        if (row >= 2 * CH_TB - 3) __stcg(my_halo + CH_H_BOT + (row - (2 * CH_TB - 3)) * CH_TW + jw, v);
+        if (jw == 0) __stcg(my_halo + CH_H_LEFT + row, v);
+        if (jw == CH_TW - 1) __stcg(my_halo + CH_H_RIGHT + row, v);
+      }
     }
     __syncthreads();
     for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = 0;
-    grid.sync();
+    mark(4);
   }
+  if (timing)
+    for (int i = 0; i < 7; ++i) a.ts[size_t(blockIdx.x) * 8 + i] = tacc[i];
 
   // closing near of the last reach
-  const uint32_t* last = ((a.steps - 1) & 1) ? a.buf1 : a.buf0;
-  stage_rows(last);
+  stage_halo((unsigned long long)a.steps);
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < CH_UPT; ++q) {
-    const int unit = tid + q * CH_THREADS;
-    const int kb = unit / CH_TW, jw = unit % CH_TW;
-    const int k = k0 + kb, j = j0 + jw;
-    if (k >= g.BH || j >= int(g.pitch)) continue;
-    uint32_t o0 = 0, o1 = 0;
+  hrows(a.klast);
+  __syncthreads();
+  if (j < int(g.pitch)) {
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
     if (j < g.wpr) {
-      ch_near2_dyn(stage, CH_R + 2 * kb, jw + 1, a.klast, o0, o1);
+      ch_vwin4_dyn(Ha, lr0, jw, a.klast, o);
       const uint32_t vm = valid_mask(j, g.wpr, g.lastmask);
-      o0 &= vm;
-      o1 &= vm;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] &= vm;
     }
-    a.out[size_t(2 * k) * g.pitch + j] = o0;
-    if (2 * k + 1 < g.H) a.out[size_t(2 * k + 1) * g.pitch + j] = o1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 2 * (k0 + kb0) + i;
+      if (r < g.H) a.out[size_t(r) * g.pitch + j] = o[i];
+    }
   }
 }
 
@@ -2355,13 +2470,17 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
   a.u = through;
   a.P = static_cast<const uint32_t*>(labels);
   a.F = flags32;
-  a.buf0 = tmp2;
-  a.buf1 = tmp2 + gb.slice;
+  a.halo = reinterpret_cast<unsigned long long*>(tmp2);
   a.out = out;
   a.steps = steps;
   a.kmid = kmid;
   a.klast = klast;
   a.gen0 = idx0 + 1u;
+  a.ts = nullptr;
+  static const bool timing = [] {
+    const char* e = std::getenv("SLCS_PHASE_TIMING");
+    return e && *e == '1';
+  }();
   const unsigned tiles = unsigned(((gb.pitch + CH_TW - 1) / CH_TW) *
                                   ((size_t(gb.h) + 2 * CH_TB - 1) / (2 * CH_TB)));
   cudaLaunchConfig_t cfg = {};
@@ -2374,7 +2493,29 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  cuda_check(cudaMemsetAsync(a.halo, 0, size_t(tiles) * CH_HALO * 8, st), "chain halo");
+  if (timing) cuda_check(cudaMalloc(&a.ts, size_t(tiles) * 8 * 8), "timing buffer");
   cuda_check(cudaLaunchKernelEx(&cfg, k_reach_chain, a, g), "reach chain launch");
+  if (timing) {  // diagnostics only: per-step phase times, mean and max over CTAs (us)
+    std::vector<unsigned long long> h(size_t(tiles) * 8);
+    cuda_check(cudaStreamSynchronize(st), "timing sync");
+    cuda_check(cudaMemcpy(h.data(), a.ts, h.size() * 8, cudaMemcpyDeviceToHost), "timing copy");
+    cudaFree(a.ts);
+    const char* names[] = {"setup", "hdil", "seed+publish", "barrier", "select+store",
+                           "-", "stage/halo wait"};
+    std::fprintf(stderr, "[reach chain: %u tiles, %d steps; us per step (setup: total), mean/max]",
+                 tiles, steps);
+    for (int ph = 0; ph < 7; ++ph) {
+      double sum = 0, mx = 0;
+      for (unsigned t = 0; t < tiles; ++t) {
+        const double v = double(h[size_t(t) * 8 + ph]) / 1e3 / (ph ? steps : 1);
+        sum += v;
+        mx = v > mx ? v : mx;
+      }
+      std::fprintf(stderr, " %s %.2f/%.2f", names[ph], sum / tiles, mx);
+    }
+    std::fprintf(stderr, "\n");
+  }
   return 1;
 }
 

@@ -1090,9 +1090,10 @@ struct slcs_program {
       for (size_t p = pos; p < end; ++p) {
       LG& n = lgs[order[p]];
       if (n.type == VT_AUX) {
-        // labelling + the reach flag stamps (one uint32 per 2x2 block)
+        // labelling + the reach flag stamps (one uint32 per 2x2 block, two copies:
+        // a reach chain alternates them by step parity)
         n.bytes = round_up(ccl_labels_bytes(n.w, n.h, n.batch), 256) +
-                  key_geo(n.w, n.h).slice_blocks * size_t(n.batch) * 4;
+                  key_geo(n.w, n.h).slice_blocks * size_t(n.batch) * 4 * 2;
         n.offset = alloc(n.bytes);
       } else if (n.type != VT_NUM) {
         Geo g = geo_of(n.type, n.w, n.h, n.batch);
