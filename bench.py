@@ -953,14 +953,25 @@ def main():
                "ms_per_step": e2e_s / args.steps * 1e3, "timing": "host wall clock, synced"}
         assert np.array_equal(pin_out.numpy(), res)
 
-    # ---- roofline: the dominant kernel, k_reach_fused (every launch of the folded
-    # chain but the threshold prologue is one).  Its average launch duration over
-    # the timed region is the step time / the reach launches per step -- an upper
-    # bound, as the prologue's ~10 us are charged to the reaches.  The same kernel
-    # timed alone (primitive API, L2 flushed before each call) is reported beside it.
+    # ---- roofline of the dominant kernel.  With label CSE (default) that is
+    # k_reach_chain: ONE persistent launch per formula running all 500 reaches; its
+    # duration is read from a timeline run (CUDA events around every device step).
+    # Without label CSE it is k_reach_fused, one launch per reach: duration = step
+    # time / 500 (an upper bound: the ~10 us prologue is charged to the reaches).
     peak, peak_kind = measured_peak_gbs()
     n_reach = depth // 2
-    in_region = n_reach > 0 and not cse  # label CSE runs other kernels in the chain
+    chain_us = None
+    if cse and n_reach > 0:
+        durs = []
+        for _ in range(3):
+            prog.run(label_cse=cse, timeline=True)
+            tt = prog.task_time(graph.nodes[out_task].deps[0])
+            if tt:
+                durs.append(tt[1] - tt[0])
+        chain_us = statistics.median(durs) * 1e3 if durs else None
+        prog.run(label_cse=cse)
+        torch.cuda.synchronize()
+    in_region = n_reach > 0 and not cse
     t_reach_region = ms_per_step / 1e3 / n_reach if in_region else None
     dimg = DeviceImage.upload(img, PixelKind.U16, dev)
     b = kernels.threshold(kernels.CmpOp.Gt, dimg, 56360, dev)
@@ -986,34 +997,66 @@ def main():
     torch.cuda.synchronize()
     t_reach = statistics.mean(a.elapsed_time(z) for a, z in ev) / 1e3
     t_near = statistics.mean(a.elapsed_time(z) for a, z in ev_n) / 1e3
-    if not in_region:
-        t_reach_region = t_reach
-    achieved = BYTES_PER_PX["reach"] * px / t_reach_region / 1e9
-    traffic, traffic_src = profiled_traffic("k_reach_fused<1")
-    roofline = {
-        "bound": "hbm", "kernel": "k_reach_fused<0,64,2> (the chain's reach: one cooperative "
-                                  "launch per reach -- target near^2 from a staged window, "
-                                  "tile-local run union-find, border unions, flag propagation, "
-                                  "select; the closing near folds into the next reach)",
-        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": traffic, "traffic_source": traffic_src,
-        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)",
-        "algorithmic_bytes_per_px": BYTES_PER_PX["reach"], "px_per_launch": px,
-        "duration_us": t_reach_region * 1e6,
-        "duration_source": (f"timed region / {n_reach} reach launches per step (CUDA events)"
-                            if in_region else "standalone (label CSE chain)"),
-        "note": "frac near or above 1: the 8.375 B/px of SURVEY 8(d) assume a materialised "
-                "u32 labelling; the fused kernel keeps labels in shared memory and moves "
-                "`traffic` bytes per launch",
-        "compulsory_bytes_per_px": 0.375,
-        "compulsory_frac": 0.375 * px / t_reach_region / 1e9 / peak,
-        "standalone_cold": {"kernel": "k_reach_fused<1,64,0> via reach()",
-                            "reach_ms": t_reach * 1e3,
-                            "achieved": BYTES_PER_PX["reach"] * px / t_reach / 1e9,
-                            "frac": BYTES_PER_PX["reach"] * px / t_reach / 1e9 / peak,
-                            "near_ms": t_near * 1e3,
-                            "near_achieved_gbs": BYTES_PER_PX["near"] * px / t_near / 1e9},
-    }
+    if chain_us:
+        launch_s = chain_us / 1e6
+        units = n_reach
+        traffic, traffic_src = profiled_traffic("k_reach_chain")
+        roofline = {
+            "bound": "hbm", "kernel": "k_reach_chain (all 500 reaches of the chain in ONE "
+                                      "persistent cooperative launch on a shared labelling of "
+                                      "`through`; per reach: staged window + stencils, seed "
+                                      "flags, one grid barrier, flag pull, select, step-tagged "
+                                      "halo exchange between neighbouring tiles)",
+            "achieved": BYTES_PER_PX["reach"] * px * units / launch_s / 1e9, "peak": peak,
+            "unit": "GB/s",
+            "frac": BYTES_PER_PX["reach"] * px * units / launch_s / 1e9 / peak,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)",
+            "algorithmic_bytes_per_px": BYTES_PER_PX["reach"],
+            "px_per_launch": px * units, "reaches_per_launch": units,
+            "duration_us": chain_us, "share_of_step": chain_us / 1e3 / ms_per_step,
+            "duration_source": "median of 3 timeline runs (CUDA events around the step)",
+            "note": "frac >> 1 is not HBM evidence: SURVEY 8(d)'s 8.375 B/px per reach assume a "
+                    "u32 labelling materialised per reach; here `through` is labelled once per "
+                    "formula and every reach works on L2-resident bit images (DRAM `traffic` "
+                    "per launch).  The kernel is bound by cross-SM latency: per reach one grid "
+                    "barrier + two L2 round trips (flag pull, halo records)",
+            "latency_model": {
+                "per_reach_us": chain_us / units,
+                "grid_barrier_floor_us": 1.64,
+                "barrier_source": "tools/ubench_barrier.cu, 592 co-resident CTAs "
+                                  "(profiles/r02_ubench_barrier.txt)",
+                "phase_timeline": "profiles/r02_chain_phases.txt (SLCS_PHASE_TIMING=1)"},
+            "compulsory_bytes_per_px": 0.375,
+            "compulsory_frac": 0.375 * px * units / launch_s / 1e9 / peak,
+        }
+    else:
+        if not in_region:
+            t_reach_region = t_reach
+        achieved = BYTES_PER_PX["reach"] * px / t_reach_region / 1e9
+        traffic, traffic_src = profiled_traffic("k_reach_fused<1")
+        roofline = {
+            "bound": "hbm", "kernel": "k_reach_fused<0,64,2> (one cooperative launch per "
+                                      "reach -- target near^2 from a staged window, tile-local "
+                                      "run union-find, border unions, flag propagation, select; "
+                                      "the closing near folds into the next reach)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst)",
+            "algorithmic_bytes_per_px": BYTES_PER_PX["reach"], "px_per_launch": px,
+            "duration_us": t_reach_region * 1e6,
+            "duration_source": (f"timed region / {n_reach} reach launches per step (CUDA "
+                                "events)" if in_region else "standalone"),
+            "note": "frac near or above 1: the 8.375 B/px of SURVEY 8(d) assume a materialised "
+                    "u32 labelling; the fused kernel keeps labels in shared memory",
+            "compulsory_bytes_per_px": 0.375,
+            "compulsory_frac": 0.375 * px / t_reach_region / 1e9 / peak,
+        }
+    roofline["standalone_cold"] = {
+        "kernel": "k_reach_fused<1,64,0> via reach() (one reach, L2 flushed)",
+        "reach_ms": t_reach * 1e3, "achieved": BYTES_PER_PX["reach"] * px / t_reach / 1e9,
+        "frac": BYTES_PER_PX["reach"] * px / t_reach / 1e9 / peak, "near_ms": t_near * 1e3,
+        "near_achieved_gbs": BYTES_PER_PX["near"] * px / t_near / 1e9}
 
     prims = prims5 = None
     if rank == 0 and ws == 1 and not args.no_primitives:

@@ -238,7 +238,9 @@ int slcs_program_bind(slcs_program* prog, const char* name, const slcs_image* im
 /* flags: bit 0 = capture/replay as a CUDA graph, bit 1 = disable fusion,
  * bit 2 = disable label CSE (reaches sharing one `through` node label it once),
  * bit 3 = disable reach chains (consecutive label-CSE reaches in one persistent
- * cooperative launch). */
+ * cooperative launch), bit 4 = timeline: launch eagerly with a CUDA event after
+ * every device step (per-task device times, slcs_program_task_time; the
+ * reference's TaskEvent start/end, executor.hpp:28-35). */
 int slcs_program_run(slcs_program* prog, int flags);
 /* Copies host pixels (reference layout) straight into the program's input
  * slot for `load` name `name` -- the end-to-end path: no intermediate image. */
@@ -256,6 +258,10 @@ int slcs_program_result(slcs_program* prog, int task, int* kind_out, slcs_image*
  * dependency failed (executor.cpp:204-218).  *message stays valid until the
  * next run. */
 int slcs_program_task_state(slcs_program* prog, int task, int* state, const char** message);
+/* After a run with the timeline flag: the device interval (ms from the start of
+ * the run) of the step that evaluated task `task`; -1 when the task has no step
+ * of its own (host-side const/load/save/print, or fused into a consumer's step). */
+int slcs_program_task_time(slcs_program* prog, int task, float* start_ms, float* end_ms);
 /* Kernel launches issued by one run (after fusion). */
 int slcs_program_launches(slcs_program* prog, int* out);
 /* Human-readable execution plan (fused groups, buffer slots). */

@@ -91,6 +91,7 @@ _SIGS = {
     "slcs_program_download": (i32, [vp, i32, vp, sz]),
     "slcs_program_result": (i32, [vp, i32, C.POINTER(i32), pvp, C.POINTER(dbl)]),
     "slcs_program_task_state": (i32, [vp, i32, C.POINTER(i32), C.POINTER(cstr)]),
+    "slcs_program_task_time": (i32, [vp, i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "slcs_program_launches": (i32, [vp, C.POINTER(i32)]),
     "slcs_program_plan": (cstr, [vp]),
 }

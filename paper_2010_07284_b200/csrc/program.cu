@@ -251,8 +251,26 @@ struct slcs_program {
   int launches_per_run = 0;
   std::string plan_text;
   std::vector<int> exec_order;  // live steps in launch order (after reordering)
+  // per-step device timeline (flag 16, observability): one event before the first
+  // step and one after each step; tl_step[q] = index of LG q's interval
+  bool timeline = false;
+  std::vector<cudaEvent_t> tl_ev;
+  std::vector<int> tl_step;
+  std::vector<float> tl_ms;  // [2*i] start, [2*i+1] end of interval i (ms from the start)
 
-  ~slcs_program() { release_plan(); }
+  ~slcs_program() {
+    release_plan();
+    for (cudaEvent_t e : tl_ev) cudaEventDestroy(e);
+  }
+
+  cudaEvent_t tl_event(size_t i) {
+    while (tl_ev.size() <= i) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "timeline event");
+      tl_ev.push_back(e);
+    }
+    return tl_ev[i];
+  }
 
   void release_plan() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -1241,6 +1259,29 @@ struct slcs_program {
   int enqueue(cudaStream_t st) {
     int launches = 0;
     cudaMemsetAsync(d_err, 0, sizeof(int), st);
+    size_t tl_n = 0;
+    if (timeline) {
+      tl_step.assign(lgs.size(), -1);
+      cuda_check(cudaEventRecord(tl_event(tl_n++), st), "timeline");
+    }
+    struct TimelineMark {  // after every step (break/continue included)
+      slcs_program* p;
+      cudaStream_t st;
+      size_t& n;
+      int q;
+      ~TimelineMark() {
+        if (!p->timeline || q < 0) return;
+        const LG& m = p->lgs[size_t(q)];
+        const int lead = (m.kind == LG_EW && m.group >= 0) ? m.group : q;
+        if (lead != q && p->tl_step[size_t(lead)] >= 0) {  // emitted with its group lead
+          p->tl_step[size_t(q)] = p->tl_step[size_t(lead)];
+          return;
+        }
+        cudaEventRecord(p->tl_event(n), st);
+        p->tl_step[size_t(q)] = int(n) - 1;
+        ++n;
+      }
+    };
     // `through` of the reach launched just before (null after any other step):
     // a reach on the same `through` may read it before its launch dependency
     const void* prev_through = nullptr;
@@ -1248,6 +1289,7 @@ struct slcs_program {
       const size_t q = size_t(qi);
       LG& n = lgs[q];
       if (n.dead || n.kind == LG_INPUT) continue;
+      TimelineMark tl_mark{this, st, tl_n, int(q)};
       const void* cur_through = n.kind == LG_REACH && n.in.size() > 1 ? lgs[n.in[1]].ptr : nullptr;
       const bool early_through = cur_through && cur_through == prev_through;
       prev_through = cur_through;
@@ -1417,6 +1459,8 @@ struct slcs_program {
     const int fusion = (flags & 2) ? 0 : 1;
     const bool label_cse = fusion && !(flags & 4);
     const bool chain = label_cse && !(flags & 8);
+    timeline = (flags & 16) != 0;
+    if (timeline) flags &= ~1;  // eager launches: events between the steps
     const int mode = fusion | (label_cse ? 2 : 0) | (chain ? 4 : 0);
     if (!planned || planned_fusion != mode) plan(fusion, label_cse, chain);
     planned_fusion = mode;
@@ -1470,6 +1514,16 @@ struct slcs_program {
         vals[err - 1].err = "division by zero";
         fail(SLCS_ERR_RUN, "task " + std::to_string(err - 1) + " (" + tasks[err - 1].opcode +
                                ") failed: division by zero");
+      }
+    }
+    if (timeline && !tl_ev.empty()) {
+      size_t used = 1;
+      for (int v : tl_step) used = std::max(used, size_t(v + 2));
+      cuda_check(cudaEventSynchronize(tl_ev[used - 1]), "timeline");
+      tl_ms.assign(2 * (used - 1), 0.f);
+      for (size_t i = 0; i + 1 < used; ++i) {
+        cudaEventElapsedTime(&tl_ms[2 * i], tl_ev[0], tl_ev[i]);
+        cudaEventElapsedTime(&tl_ms[2 * i + 1], tl_ev[0], tl_ev[i + 1]);
       }
     }
     if (first_fail >= 0) fail(SLCS_ERR_RUN, fail_msg);
@@ -1724,6 +1778,22 @@ int slcs_program_task_state(slcs_program* prog, int task, int* state, const char
     const Val& v = prog->vals[task];
     *state = v.err.empty() ? 0 : (v.aborted ? 2 : 1);
     if (message) *message = v.err.c_str();
+  });
+}
+
+int slcs_program_task_time(slcs_program* prog, int task, float* start_ms, float* end_ms) {
+  return pguard([&] {
+    if (!prog || !start_ms || !end_ms) fail(SLCS_ERR_ARG, "null argument");
+    std::lock_guard<std::mutex> lock(prog->mu);
+    if (task < 0 || task >= int(prog->tasks.size())) fail(SLCS_ERR_ARG, "task id out of range");
+    *start_ms = *end_ms = -1.f;
+    if (!prog->timeline || prog->vals.size() != prog->tasks.size()) return;
+    const int lg = prog->vals[task].lg;
+    if (lg < 0 || size_t(lg) >= prog->tl_step.size()) return;
+    const int st = prog->tl_step[size_t(lg)];
+    if (st < 0 || size_t(2 * st + 1) >= prog->tl_ms.size()) return;
+    *start_ms = prog->tl_ms[size_t(2 * st)];
+    *end_ms = prog->tl_ms[size_t(2 * st + 1)];
   });
 }
 

@@ -28,6 +28,7 @@ FLAG_GRAPH = 1
 FLAG_NO_FUSION = 2
 FLAG_NO_LABEL_CSE = 4
 FLAG_NO_CHAIN = 8
+FLAG_TIMELINE = 16
 
 
 def format_number(v: float) -> str:
@@ -49,6 +50,10 @@ class RunOptions:
     # RunOptions::baseDir (executor.hpp:16-26): when set, `load` paths not supplied
     # in `images` are read as PNG from here and every `save` writes its PNG here
     baseDir: Optional[str] = None
+    # per-task device timeline (events between the device steps, eager launches):
+    # fills RunReport.events and logs "task <id> <opcode> <ms>ms" (executor.cpp:184-189)
+    timeline: bool = False
+    log: Optional[object] = None  # callable(line); RunOptions::log (executor.hpp:21-22)
 
 
 @dataclass
@@ -60,6 +65,10 @@ class RunReport:
     outputs: dict = field(default_factory=dict)  # save path -> DeviceImage
     launches: int = 0
     plan: str = ""
+    # TaskEvent per node (executor.hpp:28-35): id, opcode, ran, evaluations, startMs,
+    # endMs (device time from the start of the run), and `step`: the device step
+    # that evaluated it (a node fused into a consumer's launch reports that step)
+    events: list = field(default_factory=list)
 
 
 class Program:
@@ -112,9 +121,10 @@ class Program:
                                                        h, b, C.c_void_p(a.ctypes.data)))
 
     def run(self, fusion: bool = True, cuda_graph: bool = True, label_cse: bool = True,
-            chain: bool = True) -> None:
+            chain: bool = True, timeline: bool = False) -> None:
         flags = ((FLAG_GRAPH if cuda_graph else 0) | (0 if fusion else FLAG_NO_FUSION)
-                 | (0 if label_cse else FLAG_NO_LABEL_CSE) | (0 if chain else FLAG_NO_CHAIN))
+                 | (0 if label_cse else FLAG_NO_LABEL_CSE) | (0 if chain else FLAG_NO_CHAIN)
+                 | (FLAG_TIMELINE if timeline else 0))
         _check(_lib.load().slcs_program_run(self.handle, flags))
 
     def result(self, task: int) -> Union[DeviceImage, float]:
@@ -135,6 +145,13 @@ class Program:
         _check(_lib.load().slcs_program_download(self.handle, task, C.c_void_p(out.ctypes.data),
                                                  out.nbytes))
         return out
+
+    def task_time(self, task: int):
+        """(start_ms, end_ms) of the device step that evaluated `task` in the last
+        timeline run, or None."""
+        a, b = C.c_float(), C.c_float()
+        _check(_lib.load().slcs_program_task_time(self.handle, task, C.byref(a), C.byref(b)))
+        return None if a.value < 0 else (a.value, b.value)
 
     def value_kind(self, task: int):
         k = C.c_int()
@@ -164,12 +181,20 @@ def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) ->
     rep = RunReport(taskCount=graph.node_count())
     t0 = time.perf_counter()
     err: Optional[RunError] = None
+    log = options.log or (lambda line: None)
+    log("starting computation")
     try:
-        prog.run(options.fusion, options.cuda_graph, options.label_cse, options.chain)
+        prog.run(options.fusion, options.cuda_graph, options.label_cse, options.chain,
+                 options.timeline)
     except RunError as e:
         err = e
     prog.device.synchronize()
     rep.computationMs = (time.perf_counter() - t0) * 1e3
+    if options.timeline:
+        rep.events = task_events(graph, prog, err)
+        for ev in rep.events:
+            if ev["ran"]:
+                log(f"task {ev['id']} {ev['opcode']} {ev['endMs'] - ev['startMs']:.3f}ms")
     for out in graph.outputs:
         t = graph.nodes[out]
         try:
@@ -192,6 +217,45 @@ def run(graph: TaskGraph, images: dict, options: Optional[RunOptions] = None) ->
     if err is not None:
         raise err
     return rep
+
+
+def task_events(graph: TaskGraph, prog: Program, err: Optional[RunError] = None) -> list:
+    """TaskEvents (executor.hpp:28-35) from a timeline run.  A node without a device
+    step of its own (fused into a consumer's launch -- near folded into a reach, a
+    reach inside a chain, a threshold inside a listing) reports the step of the
+    first consumer that has one; host-side nodes (const/load/save/print) report the
+    interval of their producer."""
+    n = graph.node_count()
+    times = [prog.task_time(i) for i in range(n)]
+    consumers = [[] for _ in range(n)]
+    for i, t in enumerate(graph.nodes):
+        for d in t.deps:
+            consumers[d].append(i)
+    step = list(times)
+    for i in range(n - 1, -1, -1):  # fused into a later consumer's step
+        if step[i] is None:
+            later = [step[c] for c in consumers[i] if step[c] is not None]
+            if later:
+                step[i] = min(later)
+    for i, t in enumerate(graph.nodes):  # host-side nodes: after their producer
+        if step[i] is None and t.deps and step[t.deps[0]] is not None:
+            step[i] = (step[t.deps[0]][1], step[t.deps[0]][1])
+    failed = set()
+    if err is not None:
+        import re
+        m = re.match(r"task (\d+) ", str(err))
+        if m:
+            failed.add(int(m.group(1)))
+    events = []
+    for i, t in enumerate(graph.nodes):
+        aborted = any(d in failed for d in t.deps)
+        if aborted:
+            failed.add(i)
+        s0, s1 = step[i] if step[i] is not None else (0.0, 0.0)
+        events.append({"id": i, "opcode": t.opcode, "ran": not aborted,
+                       "evaluations": 0 if aborted else 1, "startMs": s0, "endMs": s1,
+                       "own_step": times[i] is not None})
+    return events
 
 
 def run_text(text: str, images: dict, options: Optional[RunOptions] = None) -> RunReport:

@@ -428,3 +428,27 @@ def test_reach_chain_one_launch_matches_oracle(dev, w, h, depth):
     assert np.array_equal(res["chain"], x)
     assert np.array_equal(res["cse"], x)
     assert np.array_equal(res["fused"], x)
+
+
+def test_timeline_task_events_respect_dependencies(dev):
+    """RunOptions.timeline fills RunReport.events like the reference's TaskEvents
+    (executor.hpp:28-35, tests/test_executor.cpp "events respect the dependency
+    partial order") and logs "task <id> <opcode> <ms>ms" lines."""
+    from paper_2010_07284_b200 import synth as S
+    img = O.blob_noise(700, 500, 3)
+    lines = []
+    graph = compile_text(S.near_reach_chain(8) + 'print "v" volume(x8)\n')
+    rep = run_text(S.near_reach_chain(8) + 'print "v" volume(x8)\n', {"img.png": img},
+                   RunOptions(timeline=True, log=lines.append))
+    assert lines[0] == "starting computation"
+    assert len(rep.events) == graph.node_count()
+    for ev in rep.events:
+        assert ev["evaluations"] == 1 and ev["ran"]
+        assert ev["endMs"] >= ev["startMs"] >= 0
+        for d in graph.nodes[ev["id"]].deps:
+            assert ev["startMs"] >= rep.events[d]["startMs"] - 1e-6
+    assert any(ev["own_step"] and ev["endMs"] > ev["startMs"] for ev in rep.events)
+    assert sum(1 for l in lines if l.startswith("task ")) == graph.node_count()
+    # the timeline run computes the same results
+    want = run_text(S.near_reach_chain(8), {"img.png": img}).outputs["out.png"].numpy()
+    assert np.array_equal(rep.outputs["out.png"].numpy(), want)
