@@ -20,7 +20,7 @@
 // reference's canonical max index + 1 (ccl.hpp:52-60): no relabel pass.
 //
 // Passes (large images; images <= 256x256 run everything in one CTA):
-//   tile_local  128x128-px tile in shared memory: runs, unions with the band
+//   tile_local  128x256-px tile in shared memory: runs, unions with the band
 //               above / the word to the right, flatten; writes per run
 //               P = local root, per tile the list of ring-touching roots
 //   tile_merge  unions across tile borders on the global P (bit-parallel)
@@ -508,7 +508,7 @@ struct RunTile {
 };
 
 // ===========================================================================
-// Large-image path: 256x256-px tiles (128 bands x 8 words = 1024 threads).
+// Large-image path: 128x256-px tiles (64 bands x 8 words = 512 threads, 4 CTAs per SM).
 constexpr int LKW = 8;
 constexpr int LTWW = 8;
 constexpr int LTNB = 64;
