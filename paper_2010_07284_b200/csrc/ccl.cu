@@ -1958,7 +1958,7 @@ constexpr int CH_HASH = 4096;
 constexpr uint16_t CH_NOL = 0xffffu;
 constexpr size_t CH_SMEM_LIDS = size_t(CH_TW) * CH_TB * 16 * 2;
 constexpr size_t CH_SMEM_ROOTS = size_t(CH_MAXL) * 4;
-constexpr size_t CH_SMEM_FLAGS = size_t(CH_MAXL);
+constexpr size_t CH_SMEM_FLAGS = 2 * size_t(CH_MAXL);  // flags + neighbour masks
 constexpr size_t CH_SMEM_STAGE = size_t(CH_ROWS) * CH_SW * 4;
 constexpr size_t CH_SMEM_HROWS = 2 * size_t(CH_ROWS) * CH_TW * 4;  // H_a, H_(a+1)
 constexpr size_t CH_SMEM_REGION = size_t(CH_HASH) * 6 > CH_SMEM_STAGE + CH_SMEM_HROWS
@@ -1974,8 +1974,12 @@ struct ChainArgs {
   const uint32_t* x;  // target of the first reach
   const uint32_t* u;  // through
   const uint32_t* P;  // labelling of u (launch_labels)
-  uint32_t* F;        // flag stamps per 2x2 block, two copies (step parity)
+  uint32_t* F;        // per root block: the first step that seeded it (min stamp; 0xff..)
   unsigned long long* halo;  // per tile: its boundary words of every step, tagged (ch_halo)
+  unsigned int* arrive;      // per step: tiles that published that step's seeds (zeroed)
+  unsigned int* tilecnt;     // per root block: tiles holding the root (zeroed)
+  unsigned int* tile_arrive;  // per tile: 1 + the last step it published seeds for (zeroed)
+  unsigned int* tile_roots;   // per tile: count + its distinct roots (CH_MAXL + 1 words)
   uint32_t* out;      // near^klast(U of the last reach)
   int steps;
   int kmid;           // closing radius of every reach but the last (0..2)
@@ -2037,13 +2041,14 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   uint16_t* lids = reinterpret_cast<uint16_t*>(smem);
   uint32_t* lroot = reinterpret_cast<uint32_t*>(smem + CH_SMEM_LIDS);
   uint8_t* lflag = smem + CH_SMEM_LIDS + CH_SMEM_ROOTS;
+  uint8_t* lnbr = lflag + CH_MAXL;  // per root: which of the 8 neighbour tiles hold it
   unsigned char* region = smem + CH_SMEM_LIDS + CH_SMEM_ROOTS + CH_SMEM_FLAGS;
   uint32_t* hkeys = reinterpret_cast<uint32_t*>(region);
   uint16_t* hlid = reinterpret_cast<uint16_t*>(region + size_t(CH_HASH) * 4);
   uint32_t* stage = reinterpret_cast<uint32_t*>(region);
   uint32_t* Ha = reinterpret_cast<uint32_t*>(region + CH_SMEM_STAGE);  // [row][word]
   uint32_t* Hb = Ha + CH_ROWS * CH_TW;
-  __shared__ int nl_sh;
+  __shared__ int nl_sh, has_nol, pend_global, pend_mask;
 
   const int tid = threadIdx.x;
   const int tiles_x = (int(g.pitch) + CH_TW - 1) / CH_TW;
@@ -2056,7 +2061,10 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
 
   // ---- setup: runs of u, their roots, compact local ids ----
   for (int i = tid; i < CH_HASH; i += CH_THREADS) hkeys[i] = EMPTYK;
-  if (tid == 0) nl_sh = 0;
+  if (tid == 0) {
+    nl_sh = 0;
+    has_nol = 0;
+  }
   uint32_t T[2], B[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -2111,9 +2119,54 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
         if (kk == EMPTYK) break;
       }
       lids[unit * 16 + ri] = l;
+      if (l == CH_NOL) has_nol = 1;
     }
   }
-  for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = 0;
+  // roots held by more than one tile ("shared") can be seeded elsewhere; the
+  // others only here.  A shared root whose holders are all among the 8
+  // neighbouring tiles only ever needs those neighbours' progress.  lflag bits:
+  // 1 seeded (sticky), 2 shared, 4 seeded this step, 8 held beyond the neighbours
+  const int tiles_y = (g.BH + CH_TB - 1) / CH_TB;
+  const int tx = int(blockIdx.x) % tiles_x, ty = int(blockIdx.x) / tiles_x;
+  {
+    unsigned int* mine = a.tile_roots + size_t(blockIdx.x) * (CH_MAXL + 1);
+    for (int i = tid; i < nl; i += CH_THREADS) {
+      atomicAdd(a.tilecnt + lroot[i], 1u);
+      mine[1 + i] = lroot[i];
+      lnbr[i] = 0;
+    }
+    if (tid == 0) mine[0] = unsigned(nl);
+  }
+  grid.sync();
+  for (int n = 0; n < 8; ++n) {
+    const int dx = n < 3 ? n - 1 : (n == 3 ? -1 : (n == 4 ? 1 : n - 6));
+    const int dy = n < 3 ? -1 : (n < 5 ? 0 : 1);
+    const int ntx = tx + dx, nty = ty + dy;
+    if (ntx < 0 || ntx >= tiles_x || nty < 0 || nty >= tiles_y) continue;
+    const unsigned int* list = a.tile_roots + (size_t(nty) * tiles_x + ntx) * (CH_MAXL + 1);
+    const int cnt = int(__ldcg(list));
+    for (int e = tid; e < cnt; e += CH_THREADS) {
+      const uint32_t rb = __ldcg(list + 1 + e);
+      uint32_t h = ch_hash(rb);
+      for (int probe = 0; probe < CH_HASH; ++probe, h = (h + 1) & (CH_HASH - 1)) {
+        const uint32_t kk = hkeys[h];
+        if (kk == rb) {
+          const uint16_t l = hlid[h];
+          if (l != CH_NOL)
+            atomicOr(reinterpret_cast<unsigned*>(lnbr + (l & ~3)), (1u << n) << (8 * (l & 3)));
+          break;
+        }
+        if (kk == EMPTYK) break;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nl; i += CH_THREADS) {
+    const unsigned cnt = __ldcg(a.tilecnt + lroot[i]);
+    uint8_t f = cnt > 1u ? 2 : 0;
+    if (cnt > 1u && unsigned(__popc(lnbr[i])) + 1u < cnt) f |= 8;
+    lflag[i] = f;
+  }
   __syncthreads();  // the hash region becomes the staging window
   unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0}, tprev = 0;
   const bool timing = a.ts != nullptr && tid == 0;
@@ -2154,12 +2207,14 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   // them); the neighbours' boundary words come from their halo records, each
   // word tagged with its step, so waiting for the data IS the synchronisation
   // (no grid barrier between a step's select and the next step's seed)
-  const int tx = int(blockIdx.x) % tiles_x, ty = int(blockIdx.x) / tiles_x;
-  const int tiles_y = (g.BH + CH_TB - 1) / CH_TB;
+  // records are double-buffered by tag parity: a tile that does not wait for the
+  // others can run one step ahead of a neighbour, never two (it needs that
+  // neighbour's previous step to stage its own)
+  const size_t halo_bank = size_t(gridDim.x) * CH_HALO;
   auto halo_word = [&](int ntx, int nty, int idx, unsigned long long tag) -> uint32_t {
     if (ntx < 0 || ntx >= tiles_x || nty < 0 || nty >= tiles_y) return 0u;
-    const unsigned long long* p =
-        a.halo + (size_t(nty) * tiles_x + ntx) * CH_HALO + size_t(idx);
+    const unsigned long long* p = a.halo + (tag & 1) * halo_bank +
+                                  (size_t(nty) * tiles_x + ntx) * CH_HALO + size_t(idx);
     for (int spin = 0;; ++spin) {
       const unsigned long long v = __ldcg(p);
       if ((v >> 32) == tag) return uint32_t(v);
@@ -2190,7 +2245,6 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       }
     }
   };
-  unsigned long long* my_halo = a.halo + size_t(blockIdx.x) * CH_HALO;
 
   // per staged row, the tile's words dilated horizontally by ra and ra + 1
   auto hrows = [&](int ra) {
@@ -2206,11 +2260,15 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   };
 
   const int lr0 = CH_R + 2 * kb0;  // staged row of this thread's first row
+  const unsigned ntiles = gridDim.x;
+  // The chain is monotone: T(s+1) = near^kmid(U(s)) contains U(s), which contains
+  // T(s), so a component seeded once stays seeded.  Seeds are therefore sticky:
+  // a tile publishes a root only the step it becomes seeded (F = min stamp), and
+  // waits for the other tiles only while it still holds SHARED roots that are
+  // unseeded -- a tile whose roots are all seeded or all its own never waits.
   for (int s = 0; s < a.steps; ++s) {
     const int ra = s == 0 ? 0 : a.kmid;  // prev -> target radius
     const uint32_t gen = a.gen0 + uint32_t(s);
-    uint32_t* F = a.F + (s & 1) * size_t(g.sb);  // step parity: a fast tile seeding
-                                                 // step s+1 never touches step s's flags
     if (s == 0) stage_rows(a.x);
     else stage_halo((unsigned long long)s);
     __syncthreads();
@@ -2218,7 +2276,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     hrows(ra);
     __syncthreads();
     mark(1);
-    // seed: runs of u touching near(target) = near^(ra+1)(prev)
+    // seed: runs of u touching near(target) = near^(ra+1)(prev), not yet seeded
     if (T[0] | B[0] | T[1] | B[1]) {
       uint32_t n[4];
       ch_vwin4_dyn(Hb, lr0, jw, ra + 1, n);
@@ -2234,22 +2292,72 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
           if (!(sd & m)) continue;
           const uint16_t l = lids[unit * 16 + ri];
           if (l != CH_NOL) {
-            lflag[l] = 1;
+            if (!(lflag[l] & 1)) lflag[l] |= 4;
           } else {
-            __stcg(F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))), gen);
+            atomicMin(a.F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))),
+                      gen);
           }
         }
       }
     }
+    if (tid == 0) {
+      pend_global = has_nol;
+      pend_mask = 0;
+    }
     __syncthreads();
-    for (int i = tid; i < nl; i += CH_THREADS)
-      if (lflag[i]) __stcg(F + lroot[i], gen);
+    for (int i = tid; i < nl; i += CH_THREADS) {
+      uint8_t f = lflag[i];
+      if (f & 4) {
+        f = uint8_t((f & ~4) | 1);
+        lflag[i] = f;
+        if (f & 2) atomicMin(a.F + lroot[i], gen);
+      }
+      if ((f & 3) == 2) {  // shared and still unseeded: another tile may seed it
+        if (f & 8) pend_global = 1;
+        else atomicOr(&pend_mask, int(lnbr[i]));
+      }
+    }
+    __syncthreads();
     mark(2);
-    grid.sync();
-    mark(3);
-    // select: U = near^ra(prev) | seeded components
-    for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = __ldcg(F + lroot[i]) == gen ? 1 : 0;
+    // arrive (this tile's seeds of step s are published); then wait for the
+    // tiles that can still seed one of this tile's unseeded shared roots: all
+    // of them, only some neighbours, or none
+    const bool wait = pend_global || pend_mask;
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(a.arrive + s, 1u);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tile_arrive + blockIdx.x),
+                   "r"(unsigned(s + 1))
+                   : "memory");
+      auto spin_until = [&](const unsigned* p, unsigned target) {
+        for (int spin = 0;; ++spin) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+          if (v >= target) return;
+          if (spin > (1 << 24)) __trap();  // never hang
+        }
+      };
+      if (pend_global) {
+        spin_until(a.arrive + s, ntiles);
+      } else {
+        for (int n = 0; n < 8; ++n) {
+          if (!((pend_mask >> n) & 1)) continue;
+          const int dx = n < 3 ? n - 1 : (n == 3 ? -1 : (n == 4 ? 1 : n - 6));
+          const int dy = n < 3 ? -1 : (n < 5 ? 0 : 1);
+          spin_until(a.tile_arrive + (size_t(ty + dy) * tiles_x + (tx + dx)), unsigned(s + 1));
+        }
+      }
+    }
     __syncthreads();
+    mark(3);
+    if (wait) {  // shared roots seeded elsewhere this step
+      for (int i = tid; i < nl; i += CH_THREADS) {
+        const uint8_t f = lflag[i];
+        if ((f & 3) == 2 && __ldcg(a.F + lroot[i]) <= gen) lflag[i] = uint8_t(f | 1);
+      }
+      __syncthreads();
+    }
+    // select: U = near^ra(prev) | seeded components
     uint32_t uo_keep[4] = {0u, 0u, 0u, 0u};
     if (j < int(g.pitch)) {
       uint32_t (&uo)[4] = uo_keep;
@@ -2264,9 +2372,9 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
             x &= ~m;
             const uint16_t l = lids[unit * 16 + ri];
             const bool sel =
-                l != CH_NOL ? lflag[l] != 0
-                            : __ldcg(F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q],
-                                                                    B[q], m)))) == gen;
+                l != CH_NOL ? (lflag[l] & 1) != 0
+                            : __ldcg(a.F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q],
+                                                                      B[q], m)))) <= gen;
             if (sel) {
               uo[2 * q] |= T[q] & m;
               uo[2 * q + 1] |= B[q] & m;
@@ -2284,6 +2392,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     for (int i = 0; i < 4; ++i) stage[(lr0 + i) * CH_SW + CH_C0 + jw] = uo_keep[i];
     {
       const unsigned long long tag = (unsigned long long)(s + 1) << 32;
+      unsigned long long* my_halo = a.halo + ((s + 1) & 1) * halo_bank +
+                                    size_t(blockIdx.x) * CH_HALO;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 2 * kb0 + i;  // tile-relative
@@ -2295,7 +2405,6 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       }
     }
     __syncthreads();
-    for (int i = tid; i < nl; i += CH_THREADS) lflag[i] = 0;
     mark(4);
   }
   if (timing)
@@ -2458,6 +2567,12 @@ bool reach_chain_fits(const Geo& gb, int steps, int kmid, int klast) {
   return tiles <= size_t(capacity);
 }
 
+size_t reach_chain_scratch_bytes(const Geo& gb, int steps) {
+  const size_t tiles = size_t((gb.pitch + CH_TW - 1) / CH_TW) *
+                       size_t((size_t(gb.h) + 2 * CH_TB - 1) / (2 * CH_TB));
+  return 2 * tiles * CH_HALO * 8 + (size_t(steps) + tiles + tiles * (CH_MAXL + 1)) * 4;
+}
+
 int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* labels,
                        uint32_t* flags32, uint32_t idx0, int steps, int kmid, int klast,
                        uint32_t* out, uint32_t* tmp2, const Geo& gb, cudaStream_t st) {
@@ -2470,7 +2585,15 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
   a.u = through;
   a.P = static_cast<const uint32_t*>(labels);
   a.F = flags32;
+  const unsigned tiles = unsigned(((gb.pitch + CH_TW - 1) / CH_TW) *
+                                  ((size_t(gb.h) + 2 * CH_TB - 1) / (2 * CH_TB)));
+  // scratch: halo records, per-step arrival counters; the labelling's two flag
+  // copies: min seed stamps (0xff..) and per-root tile counts (0)
   a.halo = reinterpret_cast<unsigned long long*>(tmp2);
+  a.arrive = reinterpret_cast<unsigned int*>(a.halo + 2 * size_t(tiles) * CH_HALO);
+  a.tile_arrive = a.arrive + steps;
+  a.tile_roots = a.tile_arrive + tiles;
+  a.tilecnt = flags32 + g.sb;
   a.out = out;
   a.steps = steps;
   a.kmid = kmid;
@@ -2481,8 +2604,6 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
     const char* e = std::getenv("SLCS_PHASE_TIMING");
     return e && *e == '1';
   }();
-  const unsigned tiles = unsigned(((gb.pitch + CH_TW - 1) / CH_TW) *
-                                  ((size_t(gb.h) + 2 * CH_TB - 1) / (2 * CH_TB)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles);
   cfg.blockDim = dim3(CH_THREADS);
@@ -2493,7 +2614,11 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cuda_check(cudaMemsetAsync(a.halo, 0, size_t(tiles) * CH_HALO * 8, st), "chain halo");
+  cuda_check(cudaMemsetAsync(a.halo, 0,
+                             2 * size_t(tiles) * CH_HALO * 8 + (size_t(steps) + tiles) * 4, st),
+             "chain halo");
+  cuda_check(cudaMemsetAsync(a.F, 0xff, size_t(g.sb) * 4, st), "chain flags");
+  cuda_check(cudaMemsetAsync(a.tilecnt, 0, size_t(g.sb) * 4, st), "chain tile counts");
   if (timing) cuda_check(cudaMalloc(&a.ts, size_t(tiles) * 8 * 8), "timing buffer");
   cuda_check(cudaLaunchKernelEx(&cfg, k_reach_chain, a, g), "reach chain launch");
   if (timing) {  // diagnostics only: per-step phase times, mean and max over CTAs (us)
@@ -2501,7 +2626,7 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
     cuda_check(cudaStreamSynchronize(st), "timing sync");
     cuda_check(cudaMemcpy(h.data(), a.ts, h.size() * 8, cudaMemcpyDeviceToHost), "timing copy");
     cudaFree(a.ts);
-    const char* names[] = {"setup", "hdil", "seed+publish", "barrier", "select+store",
+    const char* names[] = {"setup", "hdil", "seed+publish", "arrive/wait", "select+store",
                            "-", "stage/halo wait"};
     std::fprintf(stderr, "[reach chain: %u tiles, %d steps; us per step (setup: total), mean/max]",
                  tiles, steps);

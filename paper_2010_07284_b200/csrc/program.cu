@@ -1119,8 +1119,10 @@ struct slcs_program {
         n.offset = alloc(n.bytes);
       }
       if (n.kind == LG_REACH && n.gen_idx >= 0) {
-        scratch_need = std::max(scratch_need, bool_geo(n.w, n.h, n.batch).slice * n.batch * 4 *
-                                                  (n.chain_len > 1 ? 2 : 1));
+        scratch_need = std::max(
+            scratch_need, n.chain_len > 1
+                              ? reach_chain_scratch_bytes(bool_geo(n.w, n.h, n.batch), n.chain_len)
+                              : bool_geo(n.w, n.h, n.batch).slice * n.batch * 4);
       } else if (n.kind == LG_REACH) {
         size_t s = ccl_scratch_bytes(n.w, n.h, n.batch, true, false);
         if (!ccl_small_path(n.w, n.h)) s += bool_geo(n.w, n.h, n.batch).slice * n.batch * 4;

@@ -280,6 +280,7 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
 // launch: reach s (idx0 + s) targets near^kmid of the previous selection (the
 // first targets x), the last closes with near^klast; tmp2 = two bool images
 bool reach_chain_fits(const Geo& gb, int steps, int kmid, int klast);
+size_t reach_chain_scratch_bytes(const Geo& gb, int steps);
 int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* labels,
                        uint32_t* flags32, uint32_t idx0, int steps, int kmid, int klast,
                        uint32_t* out, uint32_t* tmp2, const Geo& gb, cudaStream_t st);

@@ -20,3 +20,18 @@ for _ in range(runs):
     prog.run(cuda_graph=False)
 dev.synchronize()
 print(prog.plan.splitlines()[:6])
+
+if "--time" in sys.argv:
+    import time
+    prog.run()  # graph capture
+    dev.synchronize()
+    t0 = time.perf_counter()
+    reps = 20
+    for _ in range(reps):
+        prog.run()
+    dev.synchronize()
+    print(f"formula: {(time.perf_counter() - t0) / reps * 1e3:.3f} ms (host-timed, back to back)")
+    prog.run(timeline=True)
+    out = [i for i, t in enumerate(prog.graph.nodes) if t.opcode == "save"][0]
+    tt = prog.task_time(prog.graph.nodes[out].deps[0])
+    print(f"chain kernel step: {tt[1] - tt[0]:.3f} ms")
