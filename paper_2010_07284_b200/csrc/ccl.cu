@@ -2171,7 +2171,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0}, tprev = 0;
   const bool timing = a.ts != nullptr && tid == 0;
   auto mark = [&](int ph) {
-    if (timing) {
+    if (a.ts != nullptr && timing) {
       const unsigned long long t = ch_now();
       tacc[ph] += t - tprev;
       tprev = t;
@@ -2206,46 +2206,65 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   // later steps: the tile's own rows are already in the window (its select wrote
   // them); the neighbours' boundary words come from their halo records, each
   // word tagged with its step, so waiting for the data IS the synchronisation
-  // (no grid barrier between a step's select and the next step's seed)
+  // (no grid barrier between a step's select and the next step's seed).
+  // Each thread owns at most two halo words of the window; where they come from
+  // is fixed for the whole chain, so it is resolved once.  Words outside the
+  // image stay the zeros the first full staging wrote.
+  constexpr int CH_NHALO = 6 * (CH_TW + 2) + 2 * 2 * CH_TB;
+  const unsigned long long* hsrc[2] = {nullptr, nullptr};
+  int hdst[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int i = tid + q * CH_THREADS;
+    if (i >= CH_NHALO) continue;
+    int ntx, nty, idx, dst;
+    if (i < 6 * (CH_TW + 2)) {
+      const int rr = i / (CH_TW + 2), c = i - rr * (CH_TW + 2);  // c: staged col - (C0-1)
+      const bool above = rr < 3;
+      const int r = above ? rr : CH_R + 2 * CH_TB + (rr - 3);
+      nty = above ? ty - 1 : ty + 1;
+      const int base = above ? CH_H_BOT + rr * CH_TW : CH_H_TOP + (rr - 3) * CH_TW;
+      if (c == 0) {
+        ntx = tx - 1;
+        idx = base + CH_TW - 1;
+      } else if (c == CH_TW + 1) {
+        ntx = tx + 1;
+        idx = base;
+      } else {
+        ntx = tx;
+        idx = base + c - 1;
+      }
+      dst = r * CH_SW + CH_C0 - 1 + c;
+    } else {
+      const int qq = i - 6 * (CH_TW + 2);
+      const int row = qq >> 1, right = qq & 1;
+      nty = ty;
+      ntx = right ? tx + 1 : tx - 1;
+      idx = right ? CH_H_LEFT + row : CH_H_RIGHT + row;
+      dst = (CH_R + row) * CH_SW + (right ? CH_C0 + CH_TW : CH_C0 - 1);
+    }
+    if (ntx < 0 || ntx >= tiles_x || nty < 0 || nty >= tiles_y) continue;
+    hsrc[q] = a.halo + (size_t(nty) * tiles_x + ntx) * CH_HALO + size_t(idx);
+    hdst[q] = dst;
+  }
   // records are double-buffered by tag parity: a tile that does not wait for the
   // others can run one step ahead of a neighbour, never two (it needs that
   // neighbour's previous step to stage its own)
   const size_t halo_bank = size_t(gridDim.x) * CH_HALO;
-  auto halo_word = [&](int ntx, int nty, int idx, unsigned long long tag) -> uint32_t {
-    if (ntx < 0 || ntx >= tiles_x || nty < 0 || nty >= tiles_y) return 0u;
-    const unsigned long long* p = a.halo + (tag & 1) * halo_bank +
-                                  (size_t(nty) * tiles_x + ntx) * CH_HALO + size_t(idx);
-    for (int spin = 0;; ++spin) {
-      const unsigned long long v = __ldcg(p);
-      if ((v >> 32) == tag) return uint32_t(v);
-      if (spin > (1 << 22)) __trap();  // a producer never arrived: fail, never hang
-    }
-  };
   auto stage_halo = [&](unsigned long long tag) {
-    // rows above (the tile above's bottom rows), rows below (the tile below's top
-    // rows), 10 words each; the left / right halo word of the tile's own rows
-    for (int i = tid; i < 6 * (CH_TW + 2) + 2 * 2 * CH_TB; i += CH_THREADS) {
-      if (i < 6 * (CH_TW + 2)) {
-        const int rr = i / (CH_TW + 2), c = i - rr * (CH_TW + 2);  // c: staged col - (C0-1)
-        const bool above = rr < 3;
-        const int r = above ? rr : CH_R + 2 * CH_TB + (rr - 3);
-        const int nty = above ? ty - 1 : ty + 1;
-        const int base = above ? CH_H_BOT + rr * CH_TW : CH_H_TOP + (rr - 3) * CH_TW;
-        uint32_t v;
-        if (c == 0) v = halo_word(tx - 1, nty, base + CH_TW - 1, tag);
-        else if (c == CH_TW + 1) v = halo_word(tx + 1, nty, base, tag);
-        else v = halo_word(tx, nty, base + c - 1, tag);
-        stage[r * CH_SW + CH_C0 - 1 + c] = v;
-      } else {
-        const int q = i - 6 * (CH_TW + 2);
-        const int row = q >> 1, right = q & 1;
-        const uint32_t v = right ? halo_word(tx + 1, ty, CH_H_LEFT + row, tag)
-                                 : halo_word(tx - 1, ty, CH_H_RIGHT + row, tag);
-        stage[(CH_R + row) * CH_SW + (right ? CH_C0 + CH_TW : CH_C0 - 1)] = v;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!hsrc[q]) continue;
+      const unsigned long long* p = hsrc[q] + (tag & 1) * halo_bank;
+      unsigned long long v = __ldcg(p);
+      for (int spin = 0; (v >> 32) != tag; ++spin) {
+        if (spin > (1 << 22)) __trap();  // a producer never arrived: fail, never hang
+        __nanosleep(32);
+        v = __ldcg(p);
       }
+      stage[hdst[q]] = uint32_t(v);
     }
   };
-
   // per staged row, the tile's words dilated horizontally by ra and ra + 1
   auto hrows = [&](int ra) {
     for (int i = tid; i < CH_ROWS * CH_TW; i += CH_THREADS) {
@@ -2335,6 +2354,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
           if (v >= target) return;
           if (spin > (1 << 24)) __trap();  // never hang
+          __nanosleep(32);
         }
       };
       if (pend_global) {
