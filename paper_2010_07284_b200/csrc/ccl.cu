@@ -2168,7 +2168,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     lflag[i] = f;
   }
   __syncthreads();  // the hash region becomes the staging window
-  unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0}, tprev = 0;
+  unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0}, tprev = 0, nbr_waits = 0;
   const bool timing = a.ts != nullptr && tid == 0;
   auto mark = [&](int ph) {
     if (a.ts != nullptr && timing) {
@@ -2280,6 +2280,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
 
   const int lr0 = CH_R + 2 * kb0;  // staged row of this thread's first row
   const unsigned ntiles = gridDim.x;
+  bool unseeded = (T[0] | B[0] | T[1] | B[1]) != 0u;  // this thread has unseeded runs
   // The chain is monotone: T(s+1) = near^kmid(U(s)) contains U(s), which contains
   // T(s), so a component seeded once stays seeded.  Seeds are therefore sticky:
   // a tile publishes a root only the step it becomes seeded (F = min stamp), and
@@ -2296,7 +2297,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     __syncthreads();
     mark(1);
     // seed: runs of u touching near(target) = near^(ra+1)(prev), not yet seeded
-    if (T[0] | B[0] | T[1] | B[1]) {
+    // (a thread whose runs were all seeded at its last select has nothing to do)
+    if (unseeded) {
       uint32_t n[4];
       ch_vwin4_dyn(Hb, lr0, jw, ra + 1, n);
 #pragma unroll
@@ -2342,9 +2344,14 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     // tiles that can still seed one of this tile's unseeded shared roots: all
     // of them, only some neighbours, or none
     const bool wait = pend_global || pend_mask;
+    if (a.ts != nullptr && tid == 0) {  // diagnostics: steps with a global / neighbour wait
+      if (pend_global) tacc[5] += 1000;
+      else if (pend_mask) ++nbr_waits;
+    }
     if (tid == 0) {
-      __threadfence();
-      atomicAdd(a.arrive + s, 1u);
+      // release: the block barrier above ordered every thread's seed stamps before
+      // this thread's arrival (cumulativity), no full fence needed
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.arrive + s) : "memory");
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tile_arrive + blockIdx.x),
                    "r"(unsigned(s + 1))
                    : "memory");
@@ -2368,9 +2375,9 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
         }
       }
     }
-    __syncthreads();
     mark(3);
     if (wait) {  // shared roots seeded elsewhere this step
+      __syncthreads();
       for (int i = tid; i < nl; i += CH_THREADS) {
         const uint8_t f = lflag[i];
         if ((f & 3) == 2 && __ldcg(a.F + lroot[i]) <= gen) lflag[i] = uint8_t(f | 1);
@@ -2379,6 +2386,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     }
     // select: U = near^ra(prev) | seeded components
     uint32_t uo_keep[4] = {0u, 0u, 0u, 0u};
+    bool still_unseeded = false;
     if (j < int(g.pitch)) {
       uint32_t (&uo)[4] = uo_keep;
       if (j < g.wpr) {
@@ -2398,6 +2406,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
             if (sel) {
               uo[2 * q] |= T[q] & m;
               uo[2 * q + 1] |= B[q] & m;
+            } else {
+              still_unseeded = true;
             }
           }
         }
@@ -2408,6 +2418,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     }
     // the next window's own rows (stage is free: this step read it through Ha/Hb),
     // and this tile's boundary words for its neighbours, tagged with the step
+    unseeded = still_unseeded;
 #pragma unroll
     for (int i = 0; i < 4; ++i) stage[(lr0 + i) * CH_SW + CH_C0 + jw] = uo_keep[i];
     {
@@ -2428,7 +2439,10 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     mark(4);
   }
   if (timing)
+  {
     for (int i = 0; i < 7; ++i) a.ts[size_t(blockIdx.x) * 8 + i] = tacc[i];
+    a.ts[size_t(blockIdx.x) * 8 + 7] = nbr_waits * 1000;
+  }
 
   // closing near of the last reach
   stage_halo((unsigned long long)a.steps);
@@ -2647,10 +2661,10 @@ int launch_reach_chain(const uint32_t* x, const uint32_t* through, const void* l
     cuda_check(cudaMemcpy(h.data(), a.ts, h.size() * 8, cudaMemcpyDeviceToHost), "timing copy");
     cudaFree(a.ts);
     const char* names[] = {"setup", "hdil", "seed+publish", "arrive/wait", "select+store",
-                           "-", "stage/halo wait"};
+                           "global-wait share", "stage/halo wait", "neighbour-wait share"};
     std::fprintf(stderr, "[reach chain: %u tiles, %d steps; us per step (setup: total), mean/max]",
                  tiles, steps);
-    for (int ph = 0; ph < 7; ++ph) {
+    for (int ph = 0; ph < 8; ++ph) {
       double sum = 0, mx = 0;
       for (unsigned t = 0; t < tiles; ++t) {
         const double v = double(h[size_t(t) * 8 + ph]) / 1e3 / (ph ? steps : 1);
