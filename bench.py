@@ -1067,11 +1067,21 @@ def main():
     # (C3 slices over ranks, C5 row bands), every rank taking part
     extra = {}
     if not args.no_extra:
-        extra["segmentation_c3"] = formula_result(args, ws, rank, local, dev, stream, "c3")
-        extra["bands_c5"] = c5_result(args, ws, rank, local, dev, stream, n=args.c5_size)
+        def guarded(fn, *a, **kw):
+            # a failing sub-result is reported in the line, never fatal to the headline
+            try:
+                return fn(*a, **kw)
+            except Exception as e:  # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return {"error": f"{type(e).__name__}: {e}"[:500]}
+        extra["segmentation_c3"] = guarded(formula_result, args, ws, rank, local, dev, stream,
+                                           "c3")
+        extra["bands_c5"] = guarded(c5_result, args, ws, rank, local, dev, stream,
+                                    n=args.c5_size)
         if ws == 1:
-            extra["ccl_reach_c4"] = c4_result(args, ws, rank, local, dev, stream)
-            extra["fig3_grow_7680"] = fig3_result(args, dev, stream, local)
+            extra["ccl_reach_c4"] = guarded(c4_result, args, ws, rank, local, dev, stream)
+            extra["fig3_grow_7680"] = guarded(fig3_result, args, dev, stream, local)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
