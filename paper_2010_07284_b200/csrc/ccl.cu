@@ -1604,8 +1604,6 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   const int r = 2 * kb;
   const bool in = kb < g.BH && j < g.wpr;
   const bool two = r + 1 < g.H;
-  const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
-  const uint32_t Bw = (in && two) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
 #if !SLCS_COOP_PDL
   (void)early;
 #else
@@ -1613,8 +1611,12 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
   // previous launch (early), everything up to the flattened tile union-find
   // reads only `through` and shared memory, so it runs while the previous
   // kernel drains; the target window and all scratch writes wait for it.
+  // Otherwise even `through` is read only after the wait: the previous grid's
+  // writes are guaranteed visible only once griddepcontrol.wait returns.
   if (!early) slcs_pdl_wait();
 #endif
+  const uint32_t Tw = in ? __ldcg(u + size_t(r) * g.pitch + j) : 0u;
+  const uint32_t Bw = (in && two) ? __ldcg(u + size_t(r + 1) * g.pitch + j) : 0u;
   uint32_t tT, tB, seedT, seedB;
   auto stage_target = [&]() {
     // target window: rows R0-TH .. R0+2NB+TH-1, columns j0-1 .. j0+8 (halo words by
