@@ -2051,6 +2051,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   uint32_t* Ha = reinterpret_cast<uint32_t*>(region + CH_SMEM_STAGE);  // [row][word]
   uint32_t* Hb = Ha + CH_ROWS * CH_TW;
   __shared__ int nl_sh, has_nol, pend_global, pend_mask;
+  __shared__ volatile uint32_t done_sink;
 
   const int tid = threadIdx.x;
   const int tiles_x = (int(g.pitch) + CH_TW - 1) / CH_TW;
@@ -2300,6 +2301,10 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     mark(1);
     // seed: runs of u touching near(target) = near^(ra+1)(prev), not yet seeded
     // (a thread whose runs were all seeded at its last select has nothing to do)
+    // seed stamps are returning atomics: a thread reaches the barrier below only
+    // after its stamps were performed at L2, so the arrival after the barrier
+    // can be a relaxed write (a release there costs a full fence every step)
+    uint32_t done = 0;
     if (unseeded) {
       uint32_t n[4];
       ch_vwin4_dyn(Hb, lr0, jw, ra + 1, n);
@@ -2317,8 +2322,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
           if (l != CH_NOL) {
             if (!(lflag[l] & 1)) lflag[l] |= 4;
           } else {
-            atomicMin(a.F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))),
-                      gen);
+            done ^= atomicMin(a.F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))),
+                              gen);
           }
         }
       }
@@ -2333,13 +2338,14 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       if (f & 4) {
         f = uint8_t((f & ~4) | 1);
         lflag[i] = f;
-        if (f & 2) atomicMin(a.F + lroot[i], gen);
+        if (f & 2) done ^= atomicMin(a.F + lroot[i], gen);
       }
       if ((f & 3) == 2) {  // shared and still unseeded: another tile may seed it
         if (f & 8) pend_global = 1;
         else atomicOr(&pend_mask, int(lnbr[i]));
       }
     }
+    if (done == 0x5a5a5a5au) done_sink = done;  // a use, so ptxas keeps ATOM (not RED)
     __syncthreads();
     mark(2);
     // arrive (this tile's seeds of step s are published); then wait for the
@@ -2351,10 +2357,11 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       else if (pend_mask) ++nbr_waits;
     }
     if (tid == 0) {
-      // release: the block barrier above ordered every thread's seed stamps before
-      // this thread's arrival (cumulativity), no full fence needed
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.arrive + s) : "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.tile_arrive + blockIdx.x),
+      // every seed stamp of this step has completed at L2 (returning atomics,
+      // then the block barrier), so a reader that observes these arrivals with
+      // ld.acquire and then loads F through L2 sees the stamps
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.arrive + s) : "memory");
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.tile_arrive + blockIdx.x),
                    "r"(unsigned(s + 1))
                    : "memory");
       auto spin_until = [&](const unsigned* p, unsigned target) {
