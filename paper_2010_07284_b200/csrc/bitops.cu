@@ -9,6 +9,7 @@
 //   near       kernels.cpp:99-124  funnel-shift 3x3 (k-fold: (2k+1)^2) OR
 //   interior   stdlib.imgql:5      same stencil with AND, out-of-image = 1
 //   volume     kernels.cpp:126-136 popcount + warp/block reduce + 1 atomic
+#include <type_traits>
 #include "slcs_internal.h"
 
 namespace slcs {
@@ -433,9 +434,9 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
 #pragma unroll
   for (int e = 0; e < 4; ++e) vm[e] = valid_mask(j0 + e, wpr, lastmask);
 
-  auto hrow = [&](int r, uint32_t (&o)[4]) {
+  // one input row -> its horizontal dilation (erosion) by K bits
+  auto hdil = [&](const uint32_t* row, uint32_t (&o)[4]) {
     uint32_t w[6];
-    const uint32_t* row = row_at(src, r, h, pitch, hl);
     if (!row) {
 #pragma unroll
       for (int e = 0; e < 6; ++e) w[e] = ID;
@@ -460,33 +461,54 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
       o[e] = acc;
     }
   };
-
-  uint32_t ring[2 * K + P][4];
-#pragma unroll
-  for (int i = 0; i < 2 * K; ++i) hrow(r0 - K + i, ring[i]);
-#pragma unroll
-  for (int c = 0; c < S; c += P) {
-#pragma unroll
-    for (int p = 0; p < P; ++p) hrow(r0 + c + K + p, ring[2 * K + p]);
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      if (c + p < rows) {
-        uint32_t o[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint32_t acc = ring[p][e];
-#pragma unroll
-          for (int d = 1; d <= 2 * K; ++d) acc = ERODE ? (acc & ring[p + d][e]) : (acc | ring[p + d][e]);
-          o[e] = acc & vm[e];
-        }
-        dst[size_t(r0 + c + p) * pitch4 + q] = make_uint4(o[0], o[1], o[2], o[3]);
+  // the strip through a (2K + P)-row register ring; FULL: every input row is an
+  // image row and every output row exists, so rows are a pointer walk with no
+  // per-row bounds or halo logic (all strips but the first and last)
+  auto run = [&](auto full) {
+    constexpr bool FULL = decltype(full)::value;
+    const uint32_t* rp = src + size_t(r0 - K) * pitch;
+    uint4* dp = dst + size_t(r0) * pitch4 + q;
+    auto fetch = [&](int r, uint32_t (&o)[4]) {
+      if (FULL) {
+        hdil(rp, o);
+        rp += pitch;
+      } else {
+        hdil(row_at(src, r, h, pitch, hl), o);
       }
+    };
+    uint32_t ring[2 * K + P][4];
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i) fetch(r0 - K + i, ring[i]);
+#pragma unroll
+    for (int c = 0; c < S; c += P) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) fetch(r0 + c + K + p, ring[2 * K + p]);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (FULL || c + p < rows) {
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t acc = ring[p][e];
+#pragma unroll
+            for (int d = 1; d <= 2 * K; ++d)
+              acc = ERODE ? (acc & ring[p + d][e]) : (acc | ring[p + d][e]);
+            o[e] = acc & vm[e];
+          }
+          *dp = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        dp += pitch4;
+      }
+#pragma unroll
+      for (int i = 0; i < 2 * K; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ring[i][e] = ring[i + P][e];
     }
-#pragma unroll
-    for (int i = 0; i < 2 * K; ++i)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) ring[i][e] = ring[i + P][e];
-  }
+  };
+  if (r0 - K >= 0 && r0 + S + K <= h)
+    run(std::true_type{});
+  else
+    run(std::false_type{});
 }
 
 // ---- near / interior for wide images: bulk-async (TMA engine) slabs -----------
@@ -730,19 +752,22 @@ void near_dispatch(const uint32_t* a, uint32_t* out, const Geo& g, int k, cudaSt
 }
 
 // volume: one launch.  8 independent uint4 loads in flight per thread,
-// popcount, warp + block reduction, one u64 atomic per CTA into a per-slice
-// accumulator; the slice's last CTA (done counter) publishes the count (u64
-// and/or double) and resets accumulator and counter to zero, so no memset
-// launch is needed (acc/done must be zero before the first use).
-__global__ void k_volume(const uint4* __restrict__ a, size_t slice4, unsigned long long* acc,
-                         unsigned int* done, unsigned long long* __restrict__ counts,
-                         double* __restrict__ dbl) {
-  slcs_pdl_wait();
-  const uint4* src = a + size_t(blockIdx.y) * slice4;
+// popcount, warp + block reduction, then ONE returning 64-bit atomic per CTA on
+// the slice's accumulator, which packs (count << 20) | CTAs-arrived: the CTA
+// that sees CTAs-arrived == gridDim.x - 1 is the last, and the value it got
+// back already holds every other CTA's count (one location, so the atomic's
+// total order is the synchronisation -- no fences, no second counter).  That
+// CTA publishes the count (u64 and/or double) and resets the accumulator to
+// zero, so no memset launch is needed (acc must be zero before the first use).
+// Counts up to 2^44 px, grids up to 2^20 CTAs per slice.
+__device__ __forceinline__ void vol_body(const uint4* __restrict__ src, size_t n4,
+                                         unsigned long long* acc,
+                                         unsigned long long* __restrict__ counts,
+                                         double* __restrict__ dbl) {
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long local = 0;
-  for (; q + 7 * stride < slice4; q += 8 * stride) {
+  for (; q + 7 * stride < n4; q += 8 * stride) {
     uint4 x[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = __ldg(src + q + u * stride);
@@ -751,10 +776,13 @@ __global__ void k_volume(const uint4* __restrict__ a, size_t slice4, unsigned lo
     for (int u = 0; u < 8; ++u) c += __popc(x[u].x) + __popc(x[u].y) + __popc(x[u].z) + __popc(x[u].w);
     local += c;
   }
-  for (; q < slice4; q += stride) {
+  for (; q < n4; q += stride) {
     const uint4 x = __ldg(src + q);
     local += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
   }
+  // the reads are done: let the next kernel's CTAs launch during the reduction
+  // tail (they still wait for this grid to complete before reading anything)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
   __shared__ unsigned long long part[32];
@@ -766,18 +794,32 @@ __global__ void k_volume(const uint4* __restrict__ a, size_t slice4, unsigned lo
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if (lane == 0) {
-      const int s = blockIdx.y;
-      if (local) atomicAdd(acc + s, local);
-      __threadfence();
-      if (atomicAdd(done + s, 1u) == gridDim.x - 1) {
-        __threadfence();
-        const unsigned long long total = atomicExch(acc + s, 0ull);
-        done[s] = 0u;
-        if (counts) counts[s] = total;
-        if (dbl) dbl[s] = double(total);
+      const unsigned long long old = atomicAdd(acc, (local << 20) | 1ull);
+      if ((old & 0xfffffull) == gridDim.x - 1) {
+        const unsigned long long total = (old >> 20) + local;
+        *acc = 0ull;
+        if (counts) *counts = total;
+        if (dbl) *dbl = double(total);
       }
     }
   }
+}
+
+// one slice per blockIdx.y
+__global__ void k_volume(const uint4* __restrict__ a, size_t slice4, unsigned long long* acc,
+                         unsigned long long* __restrict__ counts, double* __restrict__ dbl) {
+  slcs_pdl_wait();
+  const int s = blockIdx.y;
+  vol_body(a + size_t(s) * slice4, slice4, acc + s, counts ? counts + s : nullptr,
+           dbl ? dbl + s : nullptr);
+}
+
+// independent volumes of different images in one launch, one per blockIdx.y
+// (a device program's adjacent volume steps: one launch instead of n)
+__global__ void k_volume_multi(VolumeJobs jobs) {
+  slcs_pdl_wait();
+  const VolumeJob& j = jobs.job[blockIdx.y];
+  vol_body(reinterpret_cast<const uint4*>(j.a), j.words / 4, j.acc, j.counts, j.dbl);
 }
 
 // randomMask (tests/oracles.cpp:44-49) on device: pixel i of the full image
@@ -953,9 +995,18 @@ int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
   int gx = grid_for(n4, kThreads * 8, 148 * 8);
   if (g.batch > 1) gx = std::max(1, std::min(gx, (148 * 8 + g.batch - 1) / g.batch));
   dim3 grid(unsigned(gx), unsigned(g.batch));
-  unsigned int* done = reinterpret_cast<unsigned int*>(vscratch + g.batch);
-  pdl(k_volume, grid, kThreads, 0, st, reinterpret_cast<const uint4*>(a), n4, vscratch, done,
-      counts, dbl);
+  pdl(k_volume, grid, kThreads, 0, st, reinterpret_cast<const uint4*>(a), n4, vscratch, counts,
+      dbl);
+  return 1;
+}
+
+int launch_volume_multi(const VolumeJobs& jobs, cudaStream_t st) {
+  if (jobs.n < 1 || jobs.n > kVolumeJobsMax) fail(SLCS_ERR_ARG, "volume: bad job count");
+  size_t n4 = 0;
+  for (int i = 0; i < jobs.n; ++i) n4 = std::max(n4, jobs.job[i].words / 4);
+  int gx = grid_for(n4, kThreads * 8, 148 * 8);
+  gx = std::max(1, std::min(gx, (148 * 8 + jobs.n - 1) / jobs.n));
+  pdl(k_volume_multi, dim3(unsigned(gx), unsigned(jobs.n)), kThreads, 0, st, jobs);
   return 1;
 }
 

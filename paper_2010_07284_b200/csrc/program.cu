@@ -1048,6 +1048,17 @@ struct slcs_program {
           }
           if (grp.size() > 1)
             for (int q : grp) lgs[q].group = order[i];
+        } else if (lead.kind == LG_VOLUME && lead.batch == 1) {
+          // adjacent volumes (independent: a volume reads an image, makes a
+          // number): one k_volume_multi launch
+          std::vector<int> grp{order[i]};
+          while (j < order.size() && int(grp.size()) < kVolumeJobsMax &&
+                 lgs[order[j]].kind == LG_VOLUME && lgs[order[j]].batch == 1) {
+            grp.push_back(order[j]);
+            ++j;
+          }
+          if (grp.size() > 1)
+            for (int q : grp) lgs[q].group = order[i];
         }
         i = j;
       }
@@ -1274,7 +1285,7 @@ struct slcs_program {
       ~TimelineMark() {
         if (!p->timeline || q < 0) return;
         const LG& m = p->lgs[size_t(q)];
-        const int lead = (m.kind == LG_EW && m.group >= 0) ? m.group : q;
+        const int lead = m.group >= 0 ? m.group : q;
         if (lead != q && p->tl_step[size_t(lead)] >= 0) {  // emitted with its group lead
           p->tl_step[size_t(q)] = p->tl_step[size_t(lead)];
           return;
@@ -1432,11 +1443,27 @@ struct slcs_program {
                                     static_cast<uint32_t*>(n.ptr), gb, cs, st);
           break;
         }
-        case LG_VOLUME:
-          // d_counts: 2 zeroed u64 per number slot = volume accumulators/counters
+        case LG_VOLUME: {
+          // d_counts: 2 zeroed u64 per number slot (the first: the volume accumulator)
+          if (n.group >= 0) {  // adjacent volumes: one launch
+            if (n.group != int(q)) break;
+            std::vector<int> members = group_members(int(q), bad);
+            if (bad) break;
+            VolumeJobs jobs{};
+            for (const int mq : members) {
+              const LG& m = lgs[size_t(mq)];
+              jobs.job[jobs.n++] = VolumeJob{static_cast<const uint32_t*>(lgs[m.in[0]].ptr),
+                                             bool_geo(m.w, m.h, 1).slice,
+                                             d_counts + 2 * m.num_out, nullptr,
+                                             d_nums + m.num_out};
+            }
+            launches += launch_volume_multi(jobs, st);
+            break;
+          }
           launches += launch_volume(static_cast<const uint32_t*>(lgs[n.in[0]].ptr), nullptr,
                                     d_nums + n.num_out, d_counts + 2 * n.num_out, gb, st);
           break;
+        }
         case LG_ARITH:
           pdl(k_arith, 1, 1, 0, st, d_nums, n.num_a, n.num_b, n.ca, n.cb, n.num_out, n.aop, d_err,
                                    n.k + 1);

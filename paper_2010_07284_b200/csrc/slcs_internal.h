@@ -177,10 +177,26 @@ int launch_near(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erod
 int launch_near_halo(const uint32_t* a, uint32_t* out, const Geo& g, int k, bool erode,
                      const uint32_t* top, int ntop, const uint32_t* bot, int nbot,
                      cudaStream_t st);
-// counts (u64) and/or dbl (double) per slice; vscratch = 2*batch zeroed u64
+// counts (u64) and/or dbl (double) per slice; vscratch = batch zeroed u64
+// accumulators (left zeroed by the launch)
 // (accumulators + done counters), left zeroed by the kernel
 int launch_volume(const uint32_t* a, unsigned long long* counts, double* dbl,
                   unsigned long long* vscratch, const Geo& g, cudaStream_t st);
+// several independent volumes in one launch: image words (a multiple of 4, the
+// slice), a zeroed u64 accumulator each (left zeroed), counts and/or dbl out
+constexpr int kVolumeJobsMax = 8;
+struct VolumeJob {
+  const uint32_t* a;
+  size_t words;
+  unsigned long long* acc;
+  unsigned long long* counts;
+  double* dbl;
+};
+struct VolumeJobs {
+  VolumeJob job[kVolumeJobsMax];
+  int n;
+};
+int launch_volume_multi(const VolumeJobs& jobs, cudaStream_t st);
 // rows [row0, row0 + g.h) of randomMask(g.w x H, density, Rng(seed)) as bits
 int launch_random_mask(uint32_t* bits, const Geo& g, long long row0, unsigned long long seed,
                        double density, cudaStream_t st);

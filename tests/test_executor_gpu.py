@@ -54,6 +54,26 @@ def test_print_formats(dev):
     assert rep.printLines == ["vol=5", "ratio=0.333333", "img=image(4x4,bool)"]
 
 
+@pytest.mark.parametrize("graph", [True, False])
+def test_adjacent_volumes_share_one_launch(dev, graph):
+    """Adjacent volume steps of any shapes run as one k_volume_multi launch; every
+    count (and arithmetic on them) equals the popcount, run after run (the
+    accumulators reset themselves)."""
+    shapes = [(37, 5), (1000, 333), (64, 64), (4097, 129), (1, 1), (31, 2000), (256, 256),
+              (2, 3), (129, 65)]
+    imgs = {f"m{i}.png": O.random_mask(w, h, 0.3 + 0.05 * i, O.Rng(70 + i)) for i, (w, h)
+            in enumerate(shapes)}
+    text = "".join(f'load x{i} = "m{i}.png"\n' for i in range(len(shapes)))
+    text += "".join(f'print "v{i}" volume(x{i})\n' for i in range(len(shapes)))
+    text += 'print "s" volume(x0) + volume(x3)\n'
+    want = [int(np.asarray(imgs[f"m{i}.png"]).sum()) for i in range(len(shapes))]
+    for _ in range(3):
+        rep = run_text(text, imgs, RunOptions(cuda_graph=graph))
+        assert rep.printLines[:len(shapes)] == [f"v{i}={w}" for i, w in enumerate(want)]
+        assert rep.printLines[-1] == f"s={want[0] + want[3]}"
+    assert "[launch group lead]" in rep.plan and "volume" in rep.plan
+
+
 def test_failure_propagation_keeps_independent_branches(dev):
     m = O.random_mask(8, 8, 0.5, O.Rng(1))
     with pytest.raises(RunError, match="cannot open file for reading"):
