@@ -46,6 +46,15 @@ namespace cg = cooperative_groups;
 #ifndef SLCS_TL_QUEUE
 #define SLCS_TL_QUEUE 1
 #endif
+#ifndef SLCS_FIRST_RUN_ALU
+#define SLCS_FIRST_RUN_ALU 1
+#endif
+#ifndef SLCS_TL_FUSED_ROOTS
+#define SLCS_TL_FUSED_ROOTS 1
+#endif
+#ifndef SLCS_CH_SLEEP
+#define SLCS_CH_SLEEP 32  // reach chain: back-off (ns) between halo-record polls
+#endif
 #ifndef SLCS_TL_HINTS
 #define SLCS_TL_HINTS 1
 #endif
@@ -99,10 +108,16 @@ G make_g(const Geo& gb) {
 // ---- run helpers ------------------------------------------------------------
 // the run of x that starts at its lowest set bit
 __device__ __forceinline__ uint32_t first_run(uint32_t x) {
+#if SLCS_FIRST_RUN_ALU
+  // adding the lowest set bit carries through exactly that run (a run ending
+  // at bit 31 carries out): the bits it clears are the run -- ALU ops only
+  return x & ~(x + (x & (0u - x)));
+#else
   const int s = __ffs(x) - 1;
   const uint32_t y = ~x & (FULL << s);
   const uint32_t below = y ? ((y & (0u - y)) - 1u) : FULL;
   return below & (FULL << s);
+#endif
 }
 
 // the run of c containing bit p (bit p must be set)
@@ -572,13 +587,18 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   T tile{par, sT, sB};
   tile.link(u0, Tw, Bw, reinterpret_cast<uint32_t*>(touch), s_qn);
   uint32_t rt[16];
-  tile.roots(u0, Tw, Bw, rt);
+  // FUSED: the roots are found inside the per-run output loop below (one pass
+  // over the runs instead of two); maxvol's sizes alias par, so it keeps the
+  // separate roots() pass
+  constexpr bool FUSED = SLCS_TL_FUSED_ROOTS && MODE != MODE_SIZE;
+  if (!FUSED) tile.roots(u0, Tw, Bw, rt);
   for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x) {
     reinterpret_cast<uint32_t*>(touch)[q] = 0;
     if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
   }
   __syncthreads();
 #else
+  constexpr bool FUSED = false;
   for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x) {
     reinterpret_cast<uint32_t*>(touch)[q] = 0;
     if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
@@ -604,6 +624,11 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
     uint32_t x = Tw | Bw;
     int cs = -1;       // MODE_SIZE: the stretch of runs sharing root slot cs
     uint32_t cn = 0;   // and its pixel count (one shared atomic per stretch)
+    uint32_t last = 0xffffffffu;  // FUSED: the previous run's root (a find hint)
+    if (FUSED) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rt[i] = 0;
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (!x) break;
@@ -611,6 +636,12 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
+        if (FUSED) {  // as roots(): no unions are in flight any more
+          const uint32_t v = T::node(k);
+          const uint32_t p = static_cast<volatile uint32_t*>(par)[T::nslot(v)];
+          last = (p == v || p == last) ? p : tile.find(p);
+          rt[i] = last;
+        }
         const int rs = T::nslot(rt[i]);
         const uint32_t rk = T::bkey(rs);  // the root's block stands for it globally
         Ps[kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask)))] =
@@ -2262,7 +2293,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       unsigned long long v = __ldcg(p);
       for (int spin = 0; (v >> 32) != tag; ++spin) {
         if (spin > (1 << 22)) __trap();  // a producer never arrived: fail, never hang
-        __nanosleep(32);
+        __nanosleep(SLCS_CH_SLEEP);
         v = __ldcg(p);
       }
       stage[hdst[q]] = uint32_t(v);
