@@ -407,50 +407,81 @@ __global__ void __launch_bounds__(128) k_near(const uint32_t* __restrict__ in,
 // k >= 2: a strip of S rows streamed through a (2K+1)-row register ring; P new
 // rows are loaded per step (independent loads in flight) so the 2K halo rows
 // are amortised over a long strip instead of being re-read per short strip.
-template <int K, bool ERODE, int S, int P>
+// A thread owns W consecutive words of the strip (W = 4: one uint4 per row);
+// smaller images use W = 2 or 1 so that the grid still fills the GPU.
+template <int W>
+struct WordVec;
+template <>
+struct WordVec<4> {
+  using V = uint4;
+  __device__ static void load(const uint32_t* p, uint32_t (&o)[4]) {
+    const uint4 c = __ldg(reinterpret_cast<const uint4*>(p));
+    o[0] = c.x, o[1] = c.y, o[2] = c.z, o[3] = c.w;
+  }
+  __device__ static void store(uint32_t* p, const uint32_t (&o)[4]) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+};
+template <>
+struct WordVec<2> {
+  __device__ static void load(const uint32_t* p, uint32_t (&o)[2]) {
+    const uint2 c = __ldg(reinterpret_cast<const uint2*>(p));
+    o[0] = c.x, o[1] = c.y;
+  }
+  __device__ static void store(uint32_t* p, const uint32_t (&o)[2]) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(o[0], o[1]);
+  }
+};
+template <>
+struct WordVec<1> {
+  __device__ static void load(const uint32_t* p, uint32_t (&o)[1]) { o[0] = __ldg(p); }
+  __device__ static void store(uint32_t* p, const uint32_t (&o)[1]) { *p = o[0]; }
+};
+
+template <int K, bool ERODE, int S, int P, int W>
 __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict__ in,
                                                      uint32_t* __restrict__ out, int h, int wpr,
-                                                     uint32_t lastmask, int pitch4, size_t slice,
+                                                     uint32_t lastmask, int groups, size_t slice,
                                                      int nstrips, Halo hl) {
   slcs_pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int s = t / pitch4, q = t - s * pitch4;
+  const int s = t / groups, q = t - s * groups;
   if (s >= nstrips) return;
   const uint32_t* src = in + size_t(blockIdx.y) * slice;
-  uint4* dst = reinterpret_cast<uint4*>(out + size_t(blockIdx.y) * slice);
-  const int r0 = s * S, j0 = 4 * q;
+  uint32_t* dst = out + size_t(blockIdx.y) * slice;
+  const int r0 = s * S, j0 = W * q;
   const int rows = min(S, h - r0);
-  const size_t pitch = size_t(pitch4) * 4;
+  const size_t pitch = size_t(groups) * W;
   if (j0 >= wpr) {
-    for (int i = 0; i < rows; ++i) dst[size_t(r0 + i) * pitch4 + q] = make_uint4(0, 0, 0, 0);
+    const uint32_t z[W] = {};
+    for (int i = 0; i < rows; ++i) WordVec<W>::store(dst + size_t(r0 + i) * pitch + j0, z);
     return;
   }
   constexpr uint32_t ID = ERODE ? 0xffffffffu : 0u;
-  uint32_t pad[5];
+  uint32_t pad[W + 1];
 #pragma unroll
-  for (int e = 0; e < 5; ++e) pad[e] = ERODE ? ~valid_mask(j0 + e, wpr, lastmask) : 0u;
-  const bool has_l = j0 > 0, has_r = j0 + 4 < wpr;
-  uint32_t vm[4];
+  for (int e = 0; e < W + 1; ++e) pad[e] = ERODE ? ~valid_mask(j0 + e, wpr, lastmask) : 0u;
+  const bool has_l = j0 > 0, has_r = j0 + W < wpr;
+  uint32_t vm[W];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) vm[e] = valid_mask(j0 + e, wpr, lastmask);
+  for (int e = 0; e < W; ++e) vm[e] = valid_mask(j0 + e, wpr, lastmask);
 
   // one input row -> its horizontal dilation (erosion) by K bits
-  auto hdil = [&](const uint32_t* row, uint32_t (&o)[4]) {
-    uint32_t w[6];
+  auto hdil = [&](const uint32_t* row, uint32_t (&o)[W]) {
+    uint32_t w[W + 2];
     if (!row) {
 #pragma unroll
-      for (int e = 0; e < 6; ++e) w[e] = ID;
+      for (int e = 0; e < W + 2; ++e) w[e] = ID;
     } else {
-      const uint4 c = __ldg(reinterpret_cast<const uint4*>(row + j0));
+      uint32_t c[W];
+      WordVec<W>::load(row + j0, c);
       w[0] = has_l ? __ldg(row + j0 - 1) : ID;
-      w[1] = c.x | pad[0];
-      w[2] = c.y | pad[1];
-      w[3] = c.z | pad[2];
-      w[4] = c.w | pad[3];
-      w[5] = has_r ? (__ldg(row + j0 + 4) | pad[4]) : ID;
+#pragma unroll
+      for (int e = 0; e < W; ++e) w[e + 1] = c[e] | pad[e];
+      w[W + 1] = has_r ? (__ldg(row + j0 + W) | pad[W]) : ID;
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < W; ++e) {
       uint32_t acc = w[e + 1];
 #pragma unroll
       for (int d = 1; d <= K; ++d) {
@@ -467,8 +498,8 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
   auto run = [&](auto full) {
     constexpr bool FULL = decltype(full)::value;
     const uint32_t* rp = src + size_t(r0 - K) * pitch;
-    uint4* dp = dst + size_t(r0) * pitch4 + q;
-    auto fetch = [&](int r, uint32_t (&o)[4]) {
+    uint32_t* dp = dst + size_t(r0) * pitch + j0;
+    auto fetch = [&](int r, uint32_t (&o)[W]) {
       if (FULL) {
         hdil(rp, o);
         rp += pitch;
@@ -476,7 +507,7 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
         hdil(row_at(src, r, h, pitch, hl), o);
       }
     };
-    uint32_t ring[2 * K + P][4];
+    uint32_t ring[2 * K + P][W];
 #pragma unroll
     for (int i = 0; i < 2 * K; ++i) fetch(r0 - K + i, ring[i]);
 #pragma unroll
@@ -486,23 +517,23 @@ __global__ void __launch_bounds__(128) k_near_stream(const uint32_t* __restrict_
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         if (FULL || c + p < rows) {
-          uint32_t o[4];
+          uint32_t o[W];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
+          for (int e = 0; e < W; ++e) {
             uint32_t acc = ring[p][e];
 #pragma unroll
             for (int d = 1; d <= 2 * K; ++d)
               acc = ERODE ? (acc & ring[p + d][e]) : (acc | ring[p + d][e]);
             o[e] = acc & vm[e];
           }
-          *dp = make_uint4(o[0], o[1], o[2], o[3]);
+          WordVec<W>::store(dp, o);
         }
-        dp += pitch4;
+        dp += pitch;
       }
 #pragma unroll
       for (int i = 0; i < 2 * K; ++i)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) ring[i][e] = ring[i + P][e];
+        for (int e = 0; e < W; ++e) ring[i][e] = ring[i + P][e];
     }
   };
   if (r0 - K >= 0 && r0 + S + K <= h)
@@ -713,25 +744,25 @@ void near_launch(const uint32_t* a, uint32_t* out, const Geo& g, cudaStream_t st
     pdl(k_near<K, ERODE, S>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, pitch4, g.slice,
         nstrips, hl);
   } else {
-    // long strips amortise the 2K halo rows; short images keep >= ~2 waves
+    // long strips amortise the 2K halo rows (32 rows, a uint4 of words per
+    // thread); images too small to fill the GPU that way use 16-row strips of
+    // two words per thread (measured at 16384^2: 16 x 2 = 27 us, 16 x 4 = 27,
+    // 16 x 1 = 29, 32 x 2 = 32, 32 x 4 = 36)
 #ifndef SLCS_NS_P
 #define SLCS_NS_P 4
 #endif
     constexpr int P = SLCS_NS_P;
-    int S = 32;
-    if (size_t(pitch4) * size_t((g.h + S - 1) / S) * g.batch < 148u * 512u) S = 16;
-#ifdef SLCS_NS_S
-    S = SLCS_NS_S;
-#endif
+    const bool big = size_t(g.pitch / 4) * size_t((g.h + 31) / 32) * size_t(g.batch) >= 148u * 2048u;
+    const int S = big ? 32 : 16, W = big ? 4 : 2;
     const int nstrips = (g.h + S - 1) / S;
-    const size_t threads = size_t(pitch4) * size_t(nstrips);
+    const int groups = int(g.pitch / W);
+    const size_t threads = size_t(groups) * size_t(nstrips);
     dim3 grid(unsigned((threads + block - 1) / block), unsigned(g.batch));
-    if (S == 32)
-      pdl(k_near_stream<K, ERODE, 32, P>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask,
-          pitch4, g.slice, nstrips, hl);
-    else
-      pdl(k_near_stream<K, ERODE, 16, P>, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask,
-          pitch4, g.slice, nstrips, hl);
+    auto go = [&](auto kern) {
+      pdl(kern, grid, block, 0, st, a, out, g.h, g.wpr, g.lastmask, groups, g.slice, nstrips, hl);
+    };
+    if (big) go(k_near_stream<K, ERODE, 32, P, 4>);
+    else go(k_near_stream<K, ERODE, 16, P, 2>);
   }
 }
 
