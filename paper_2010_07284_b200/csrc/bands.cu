@@ -285,33 +285,53 @@ __global__ void k_merge_collect_labels(LabelView v, MergeGeo m, int me,
   }
 }
 
-// band labels -> global 64-bit labels: offset + local, or the merged value
+// band labels -> global 64-bit labels: offset + local, or the merged value.
+// Four labels per thread (one 16 B load, two 16 B stores); neighbouring pixels
+// mostly share a label, so a label equal to the previous one reuses its value
+// instead of probing the hash again.
+__device__ __forceinline__ unsigned long long relabel_one(uint32_t l, unsigned long long offset,
+                                                         const unsigned long long* rkeys,
+                                                         const unsigned long long* rvals,
+                                                         uint32_t rmask, int any) {
+  if (!l) return 0ull;
+  if (any) {
+    for (uint32_t h = hash_slot(l, rmask);; h = (h + 1) & rmask) {
+      const unsigned long long k = __ldg(rkeys + h);
+      if (k == l) return __ldg(rvals + h);
+      if (k == EMPTY) break;
+    }
+  }
+  return offset + l;
+}
+
 __global__ void k_relabel_hash(const uint32_t* __restrict__ lab, size_t n,
                                unsigned long long offset, const unsigned long long* rkeys,
                                const unsigned long long* rvals, uint32_t rmask, int any,
-                               unsigned long long* __restrict__ out) {
+                               int vec, unsigned long long* __restrict__ out) {
   slcs_pdl_wait();
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t l = __ldg(lab + i);
-    unsigned long long v = 0;
-    if (l) {
-      v = offset + l;
-      if (any) {
-        uint32_t h = hash_slot(l, rmask);
-        for (;;) {
-          const unsigned long long k = __ldg(rkeys + h);
-          if (k == l) {
-            v = __ldg(rvals + h);
-            break;
-          }
-          if (k == EMPTY) break;
-          h = (h + 1) & rmask;
-        }
-      }
+  const size_t n4 = vec ? n / 4 : 0;  // vec: both buffers 16 B aligned
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  uint32_t pl = 0;
+  unsigned long long pv = 0;
+  auto one = [&](uint32_t l) {
+    if (l != pl) {
+      pv = relabel_one(l, offset, rkeys, rvals, rmask, any);
+      pl = l;
     }
-    out[i] = v;
+    return pv;
+  };
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const uint4 l = __ldcs(reinterpret_cast<const uint4*>(lab) + i);
+    ulonglong2 a, b;
+    a.x = one(l.x);
+    a.y = one(l.y);
+    b.x = one(l.z);
+    b.y = one(l.w);
+    __stcs(reinterpret_cast<ulonglong2*>(out) + 2 * i, a);
+    __stcs(reinterpret_cast<ulonglong2*>(out) + 2 * i + 1, b);
   }
+  for (size_t i = 4 * n4 + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = relabel_one(__ldg(lab + i), offset, rkeys, rvals, rmask, any);
 }
 
 uint32_t pow2_at_least(size_t n) {
@@ -457,9 +477,10 @@ int launch_band_ccl_merge_relabel(int nb, int w, int me, const void* records,
         static_cast<const unsigned long long*>(s.gmax), s.rkeys, s.rvals, s.rc - 1);
     launches = 5;
   }
-  pdl(k_relabel_hash, unsigned(std::min<size_t>((npx + 255) / 256, 148 * 32)), 256, 0, st, labels,
+  const int vec = (reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(out)) % 16 == 0;
+  pdl(k_relabel_hash, unsigned(std::min<size_t>((npx + 1023) / 1024, 148 * 32)), 256, 0, st, labels,
       npx, row0w_host[me], static_cast<const unsigned long long*>(s.rkeys),
-      static_cast<const unsigned long long*>(s.rvals), s.rc - 1, nb > 1 ? 1 : 0, out);
+      static_cast<const unsigned long long*>(s.rvals), s.rc - 1, nb > 1 ? 1 : 0, vec, out);
   return launches + 1;
 }
 
