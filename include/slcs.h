@@ -174,7 +174,8 @@ int slcs_maxvol(slcs_ctx* ctx, const slcs_image* a, slcs_image** out);
  *     target | selected, closed by slcs_near_k_halo;
  *   ccl: band-local labels (slcs_ccl), slcs_ccl_border_record, all-gather,
  *     slcs_band_ccl_relabel -> global 64-bit labels equal to the whole-image
- *     ccl::label (component max index + 1), which 65536^2 needs.
+ *     ccl::label (component max index + 1), which 65536^2 needs; or, with no
+ *     u32 label image, slcs_ccl_band_begin / all-gather / slcs_ccl_band_finish.
  * Halo buffers are packed rows with the band image's row pitch. */
 int slcs_near_k_halo(slcs_ctx* ctx, const slcs_image* a, int k, int erode, const void* top_dev,
                      int top_rows, const void* bot_dev, int bot_rows, slcs_image** out);
@@ -186,6 +187,18 @@ int slcs_ccl_border_record(slcs_ctx* ctx, const slcs_image* labels, void* record
 int slcs_band_ccl_relabel(slcs_ctx* ctx, const slcs_image* labels, int nb, int me,
                           const void* records_dev, const long long* band_heights,
                           uint64_t* out_dev);
+/* The same band CCL without a u32 label image in between: begin runs the
+ * band's union-find and writes its label record (as slcs_ccl_border_record
+ * would from slcs_ccl's labels); after the all-gather, finish writes the
+ * global 64-bit labels straight from the union-find (8 B/px written once,
+ * instead of 4 B/px labels written, read back and relabelled).  A job is
+ * destroyed with slcs_ccl_job_destroy, finished or not. */
+typedef struct slcs_ccl_job slcs_ccl_job;
+int slcs_ccl_band_begin(slcs_ctx* ctx, const slcs_image* band, void* record_dev,
+                        slcs_ccl_job** job);
+int slcs_ccl_band_finish(slcs_ccl_job* job, int nb, int me, const void* records_dev,
+                         const long long* band_heights, uint64_t* out_dev);
+int slcs_ccl_job_destroy(slcs_ccl_job* job);
 /* reach in phases: prepare labels `through` and flags the components holding a
  * seed (through & near(target)); reach_row copies, per pixel of one row, the
  * component's root node and a class byte (0 background, 1 unseeded, 2 seeded)

@@ -59,6 +59,9 @@ _SIGS = {
     "slcs_band_record_bytes": (sz, [i32, i32]),
     "slcs_ccl_border_record": (i32, [vp, vp, vp]),
     "slcs_band_ccl_relabel": (i32, [vp, vp, i32, i32, vp, vp, vp]),
+    "slcs_ccl_band_begin": (i32, [vp, vp, vp, vp]),
+    "slcs_ccl_band_finish": (i32, [vp, i32, i32, vp, vp, vp]),
+    "slcs_ccl_job_destroy": (i32, [vp]),
     "slcs_reach_border_record": (i32, [vp, vp]),
     "slcs_band_reach_merge": (i32, [vp, i32, i32, vp]),
     "slcs_png_decode": (i32, [vp, vp, sz, pvp]),

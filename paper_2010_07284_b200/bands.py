@@ -19,8 +19,11 @@ exchanges stays in device memory:
   every rank resolves the components that cross band borders with one small
   device union-find (``slcs_band_reach_merge``, csrc/bands.cu), flags its newly
   seeded roots, selects ``t | S`` and closes with a halo ``near``;
-* ``ccl::label``: band-local labels, a label border record, all-gather, and a
-  device merge + relabel to global 64-bit labels (``slcs_band_ccl_relabel``).
+* ``ccl::label``: the band's union-find and its label border record
+  (``slcs_ccl_band_begin``: the u32 labels of its first and last row, no label
+  image), all-gather, then a device merge and the global 64-bit labels written
+  straight from the union-find (``slcs_ccl_band_finish``).  With band labels
+  already at hand, ``slcs_ccl_border_record`` + ``slcs_band_ccl_relabel``.
 
 Per step and rank the communication is: near^k 2*k packed rows (k * W/8 bytes
 each way), reach 2 * (5 W + W/4) bytes all-gathered per band plus the closing
@@ -395,21 +398,36 @@ def ccl_banded(comm: Comm, band: DeviceImage, local=None):
     from .pixlog import ccl
     L = _lib.load()
     dev, w, h = band.device, band.width, band.height
-    if local is None:
-        local = ccl.label(band, dev)
     heights = comm.band_heights(h)
     nrec = L.slcs_band_record_bytes(1, w)
-    allrec = None
-    if comm.world > 1:
-        mine = _zeros(nrec, dev)
-        _check(L.slcs_ccl_border_record(dev.handle, local.handle, C.c_void_p(mine.data_ptr())))
-        allrec = _empty(nrec * comm.world, dev)
-        comm.allgather(mine, allrec, dev)
     out = torch.empty((h, w), dtype=torch.int64, device=torch.device("cuda", dev.device))
     hs = (C.c_longlong * comm.world)(*heights)
-    _check(L.slcs_band_ccl_relabel(dev.handle, local.handle, comm.world, comm.rank,
-                                   None if allrec is None else C.c_void_p(allrec.data_ptr()), hs,
-                                   C.c_void_p(out.data_ptr())))
+    mine = _zeros(nrec, dev)
+    if local is None:
+        # no u32 label image: the band's union-find -> record -> 64-bit labels
+        job = C.c_void_p()
+        _check(L.slcs_ccl_band_begin(dev.handle, band.handle, C.c_void_p(mine.data_ptr()),
+                                     C.byref(job)))
+        try:
+            allrec = mine
+            if comm.world > 1:
+                allrec = _empty(nrec * comm.world, dev)
+                comm.allgather(mine, allrec, dev)
+            _check(L.slcs_ccl_band_finish(job, comm.world, comm.rank,
+                                          C.c_void_p(allrec.data_ptr()), hs,
+                                          C.c_void_p(out.data_ptr())))
+        finally:
+            _check(L.slcs_ccl_job_destroy(job))
+    else:
+        allrec = None
+        if comm.world > 1:
+            _check(L.slcs_ccl_border_record(dev.handle, local.handle,
+                                            C.c_void_p(mine.data_ptr())))
+            allrec = _empty(nrec * comm.world, dev)
+            comm.allgather(mine, allrec, dev)
+        _check(L.slcs_band_ccl_relabel(dev.handle, local.handle, comm.world, comm.rank,
+                                       None if allrec is None else C.c_void_p(allrec.data_ptr()),
+                                       hs, C.c_void_p(out.data_ptr())))
     if _streams_differ(dev):
         dev.synchronize()
     return out

@@ -9,6 +9,8 @@
 
 #include "slcs_internal.h"
 
+#include <memory>
+
 namespace slcs {
 int launch_pack_u16_mask(const uint16_t* dense, uint32_t* bits, const Geo& g, cudaStream_t st);
 }
@@ -1204,6 +1206,102 @@ int slcs_band_ccl_relabel(slcs_ctx* ctx, const slcs_image* labels, int nb, int m
         nb, g.w, me, records_dev, row0w.data(), scratch, static_cast<const uint32_t*>(labels->data),
         size_t(g.w) * size_t(g.h), reinterpret_cast<unsigned long long*>(out_dev), ctx->stream);
     ctx->release(scratch);  // stream-ordered; row0w (pageable) was consumed by the enqueue
+  });
+}
+
+// a band's CCL between its border record and its 64-bit labels: the band's
+// union-find (large images), or its u32 labels (images the one-CTA path takes)
+struct slcs_ccl_job {
+  slcs_ctx* ctx = nullptr;
+  slcs_image* band = nullptr;    // bool view of the band (retained)
+  slcs_image* labels = nullptr;  // small path only: the u32 labels
+  void* scratch = nullptr;
+  CclScratch cs;
+};
+
+int slcs_ccl_band_begin(slcs_ctx* ctx, const slcs_image* band, void* record_dev,
+                        slcs_ccl_job** out) {
+  return guard([&] {
+    LOCKED(ctx);
+    if (!out || !record_dev) fail(SLCS_ERR_ARG, "null argument");
+    need_img(band);
+    if (band->kind == SLCS_LABEL)
+      fail(SLCS_ERR_KIND, "component labelling expects a boolean image, got label");
+    Ref b(bool_arg(ctx, band, "ccl"));
+    const Geo& g = b.p->geo;
+    if (g.batch != 1) fail(SLCS_ERR_ARG, "row bands take single images");
+    std::unique_ptr<slcs_ccl_job> job(new slcs_ccl_job);
+    job->ctx = ctx;
+    size_t off[2];
+    band_label_record_offsets(g.w, off);
+    char* rec = static_cast<char*>(record_dev);
+    if (ccl_small_path(g.w, g.h)) {
+      job->labels = op_ccl(ctx, b.p);
+      const size_t rowb = size_t(g.w) * 4;
+      const char* lab = static_cast<const char*>(job->labels->data);
+      cuda_check(cudaMemcpyAsync(rec + off[0], lab, rowb, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "border record");
+      cuda_check(cudaMemcpyAsync(rec + off[1], lab + size_t(g.h - 1) * rowb, rowb,
+                                 cudaMemcpyDeviceToDevice, ctx->stream),
+                 "border record");
+    } else {
+      job->scratch = ctx->alloc(ccl_scratch_bytes_large(g.w, g.h, 1, false, true));
+      ccl_scratch_carve_large(job->scratch, g.w, g.h, 1, false, true, &job->cs);
+      ctx->launches += launch_ccl_prepare(words(b.p), g, job->cs, ctx->stream);
+      ctx->launches += launch_ccl_row_labels(words(b.p), g, job->cs, 0,
+                                             reinterpret_cast<uint32_t*>(rec + off[0]), ctx->stream);
+      ctx->launches += launch_ccl_row_labels(words(b.p), g, job->cs, g.h - 1,
+                                             reinterpret_cast<uint32_t*>(rec + off[1]), ctx->stream);
+    }
+    job->band = b.release();
+    *out = job.release();
+  });
+}
+
+int slcs_ccl_band_finish(slcs_ccl_job* job, int nb, int me, const void* records_dev,
+                         const long long* band_heights, uint64_t* out_dev) {
+  return guard([&] {
+    if (!job) fail(SLCS_ERR_ARG, "null job");
+    slcs_ctx* ctx = job->ctx;
+    LOCKED(ctx);
+    if (nb < 1 || me < 0 || me >= nb || !band_heights || !out_dev || (nb > 1 && !records_dev))
+      fail(SLCS_ERR_ARG, "bad band relabel arguments");
+    const Geo& g = job->band->geo;
+    if (band_heights[me] != g.h) fail(SLCS_ERR_SHAPE, "band height does not match the labels");
+    std::vector<unsigned long long> row0w(static_cast<size_t>(nb));
+    unsigned long long r0 = 0;
+    for (int b = 0; b < nb; ++b) {
+      row0w[size_t(b)] = r0 * (unsigned long long)g.w;
+      r0 += (unsigned long long)band_heights[b];
+    }
+    void* scratch = ctx->alloc(band_merge_scratch_bytes(nb, g.w));
+    auto* out = reinterpret_cast<unsigned long long*>(out_dev);
+    if (job->labels) {
+      ctx->launches += launch_band_ccl_merge_relabel(
+          nb, g.w, me, records_dev, row0w.data(), scratch,
+          static_cast<const uint32_t*>(job->labels->data), size_t(g.w) * size_t(g.h), out,
+          ctx->stream);
+    } else {
+      LabelMap64 map;
+      ctx->launches += launch_band_ccl_merge(nb, g.w, me, records_dev, row0w.data(), scratch,
+                                             &map, ctx->stream);
+      ctx->launches += launch_ccl_labels64(words(job->band), g, job->cs, map, out, ctx->stream);
+    }
+    ctx->release(scratch);  // stream-ordered; row0w (pageable) was consumed by the enqueue
+  });
+}
+
+int slcs_ccl_job_destroy(slcs_ccl_job* job) {
+  return guard([&] {
+    if (!job) return;
+    slcs_ctx* ctx = job->ctx;
+    {
+      LOCKED(ctx);
+      ctx->release(job->scratch);
+    }
+    if (job->labels) slcs_image_release(job->labels);
+    slcs_image_release(job->band);
+    delete job;
   });
 }
 

@@ -34,10 +34,7 @@ constexpr unsigned long long EMPTY = ~0ull;
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 __device__ __forceinline__ uint32_t hash_slot(unsigned long long key, uint32_t mask) {
-  key ^= key >> 33;
-  key *= 0xff51afd7ed558ccdull;
-  key ^= key >> 33;
-  return uint32_t(key) & mask;
+  return band_hash_slot(key, mask);  // the same slots the label writers probe
 }
 
 // insert `key` (absent: EMPTY) and keep the smallest slot id as its representative
@@ -289,24 +286,7 @@ __global__ void k_merge_collect_labels(LabelView v, MergeGeo m, int me,
 // Four labels per thread (one 16 B load, two 16 B stores); neighbouring pixels
 // mostly share a label, so a label equal to the previous one reuses its value
 // instead of probing the hash again.
-__device__ __forceinline__ unsigned long long relabel_one(uint32_t l, unsigned long long offset,
-                                                         const unsigned long long* rkeys,
-                                                         const unsigned long long* rvals,
-                                                         uint32_t rmask, int any) {
-  if (!l) return 0ull;
-  if (any) {
-    for (uint32_t h = hash_slot(l, rmask);; h = (h + 1) & rmask) {
-      const unsigned long long k = __ldg(rkeys + h);
-      if (k == l) return __ldg(rvals + h);
-      if (k == EMPTY) break;
-    }
-  }
-  return offset + l;
-}
-
-__global__ void k_relabel_hash(const uint32_t* __restrict__ lab, size_t n,
-                               unsigned long long offset, const unsigned long long* rkeys,
-                               const unsigned long long* rvals, uint32_t rmask, int any,
+__global__ void k_relabel_hash(const uint32_t* __restrict__ lab, size_t n, LabelMap64 map,
                                int vec, unsigned long long* __restrict__ out) {
   slcs_pdl_wait();
   const size_t n4 = vec ? n / 4 : 0;  // vec: both buffers 16 B aligned
@@ -315,7 +295,7 @@ __global__ void k_relabel_hash(const uint32_t* __restrict__ lab, size_t n,
   unsigned long long pv = 0;
   auto one = [&](uint32_t l) {
     if (l != pl) {
-      pv = relabel_one(l, offset, rkeys, rvals, rmask, any);
+      pv = map_label64(l, map);
       pl = l;
     }
     return pv;
@@ -331,7 +311,7 @@ __global__ void k_relabel_hash(const uint32_t* __restrict__ lab, size_t n,
     __stcs(reinterpret_cast<ulonglong2*>(out) + 2 * i + 1, b);
   }
   for (size_t i = 4 * n4 + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = relabel_one(__ldg(lab + i), offset, rkeys, rvals, rmask, any);
+    out[i] = map_label64(__ldg(lab + i), map);
 }
 
 uint32_t pow2_at_least(size_t n) {
@@ -454,10 +434,9 @@ int launch_band_reach_merge(int nb, int w, size_t pitch_words, int me, const voi
   return 5;
 }
 
-int launch_band_ccl_merge_relabel(int nb, int w, int me, const void* records,
-                                  const unsigned long long* row0w_host, void* scratch,
-                                  const uint32_t* labels, size_t npx, unsigned long long* out,
-                                  cudaStream_t st) {
+int launch_band_ccl_merge(int nb, int w, int me, const void* records,
+                          const unsigned long long* row0w_host, void* scratch, LabelMap64* map,
+                          cudaStream_t st) {
   MergeScratch s = carve(scratch, nb, w);
   const LabelRec off = label_rec(w);
   MergeGeo m = merge_geo(nb, w, off.bytes, s);
@@ -477,10 +456,23 @@ int launch_band_ccl_merge_relabel(int nb, int w, int me, const void* records,
         static_cast<const unsigned long long*>(s.gmax), s.rkeys, s.rvals, s.rc - 1);
     launches = 5;
   }
+  map->offset = row0w_host[me];
+  map->rkeys = s.rkeys;
+  map->rvals = s.rvals;
+  map->rmask = s.rc - 1;
+  map->any = nb > 1 ? 1 : 0;
+  return launches;
+}
+
+int launch_band_ccl_merge_relabel(int nb, int w, int me, const void* records,
+                                  const unsigned long long* row0w_host, void* scratch,
+                                  const uint32_t* labels, size_t npx, unsigned long long* out,
+                                  cudaStream_t st) {
+  LabelMap64 map;
+  const int launches = launch_band_ccl_merge(nb, w, me, records, row0w_host, scratch, &map, st);
   const int vec = (reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(out)) % 16 == 0;
   pdl(k_relabel_hash, unsigned(std::min<size_t>((npx + 1023) / 1024, 148 * 32)), 256, 0, st, labels,
-      npx, row0w_host[me], static_cast<const unsigned long long*>(s.rkeys),
-      static_cast<const unsigned long long*>(s.rvals), s.rc - 1, nb > 1 ? 1 : 0, vec, out);
+      npx, map, vec, out);
   return launches + 1;
 }
 

@@ -1069,23 +1069,28 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&labs)[16], int ri) {
 #ifndef SLCS_TL_WARPS
 #define SLCS_TL_WARPS 8
 #endif
+// OUT = uint32_t: the labels; OUT = u64: a band's global 64-bit labels, each
+// run's label mapped once through `map` (the cross-band merge), so the band
+// CCL writes its 8 B/px output directly instead of a u32 image plus a relabel
 constexpr int TL_WARPS = SLCS_TL_WARPS;
+template <class OUT>
 __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* __restrict__ ubits,
                                                              const uint32_t* __restrict__ P,
                                                              const uint32_t* __restrict__ MKall,
-                                                             uint32_t* __restrict__ L, G g) {
+                                                             OUT* __restrict__ L, G g,
+                                                             LabelMap64 map, int vec_ok) {
   slcs_pdl_wait();
-  __shared__ uint32_t tab[TL_WARPS][32 * 17];
+  __shared__ OUT tab[TL_WARPS][32 * 17];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int slice = blockIdx.y;
   const uint32_t* u = ubits + size_t(slice) * g.slice;
   const uint32_t* Ps = P + size_t(slice) * g.sb;
   const uint32_t* MK = MKall + size_t(slice) * g.sb;
-  uint32_t* Ls = L + size_t(slice) * size_t(g.W) * size_t(g.H);
-  uint32_t* tb = tab[wib];
+  OUT* Ls = L + size_t(slice) * size_t(g.W) * size_t(g.H);
+  OUT* tb = tab[wib];
   const int groups = (g.wpr + 31) / 32;
   const size_t nw = size_t(g.BH) * size_t(groups);
-  const bool vec = (g.W & 3) == 0;
+  const bool vec = (g.W & 3) == 0 && vec_ok;
   for (size_t wg = size_t(blockIdx.x) * TL_WARPS + wib; wg < nw; wg += size_t(gridDim.x) * TL_WARPS) {
     const int k = int(wg / size_t(groups)), gi = int(wg - size_t(k) * groups);
     const int j = gi * 32 + lane;
@@ -1106,18 +1111,27 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
 #pragma unroll
       for (int q = 0; q < 16; ++q)
         lab[q] = (q < nr && (q == 0 || rb[q] != rb[q - 1])) ? MK[rb[q]] : 0u;
+      OUT prev = 0;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         if (q >= nr) break;
-        lab[q] = (q > 0 && rb[q] == rb[q - 1]) ? lab[q - 1] : linear_label(g, lab[q]);
-        tb[lane * 17 + q] = lab[q];
+        OUT v;
+        if (q > 0 && rb[q] == rb[q - 1]) {
+          v = prev;
+        } else if (sizeof(OUT) == 8) {
+          v = OUT(map_label64(linear_label(g, lab[q]), map));
+        } else {
+          v = OUT(linear_label(g, lab[q]));
+        }
+        prev = v;
+        tb[lane * 17 + q] = v;
       }
     }
     __syncwarp();
     const size_t c0 = size_t(gi) * 1024;
     for (int rr = 0; rr < (two ? 2 : 1); ++rr) {
       const uint32_t bits = rr ? B : T;
-      uint32_t* dst = Ls + size_t(2 * k + rr) * g.W + c0;
+      OUT* dst = Ls + size_t(2 * k + rr) * g.W + c0;
       if (vec) {
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
@@ -1126,17 +1140,24 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
           const uint32_t ws = __shfl_sync(0xffffffffu, starts, wi);
           const size_t p = size_t(it) * 128 + size_t(lane) * 4;
           if (c0 + p < size_t(g.W)) {
-            uint32_t v[4];
+            OUT v[4];
             // run index of pixel x0 (runs starting at or before it, minus one), then
             // advanced by the run starts at x0+1 .. x0+3
             const uint32_t sb = ws >> x0, pb = wb >> x0;
-            const uint32_t* trow = tb + wi * 17 + __popc(ws & ((2u << x0) - 1u)) - 1;
+            const OUT* trow = tb + wi * 17 + __popc(ws & ((2u << x0) - 1u)) - 1;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               if (e > 0) trow += (sb >> e) & 1u;
-              v[e] = ((pb >> e) & 1u) ? *trow : 0u;
+              v[e] = ((pb >> e) & 1u) ? *trow : OUT(0);
             }
-            *reinterpret_cast<uint4*>(dst + p) = make_uint4(v[0], v[1], v[2], v[3]);
+            if (sizeof(OUT) == 8) {
+              ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + p);
+              d2[0] = make_ulonglong2(v[0], v[1]);
+              d2[1] = make_ulonglong2(v[2], v[3]);
+            } else {
+              *reinterpret_cast<uint4*>(dst + p) =
+                  make_uint4(uint32_t(v[0]), uint32_t(v[1]), uint32_t(v[2]), uint32_t(v[3]));
+            }
           }
         }
       } else {
@@ -1145,7 +1166,8 @@ __global__ void __launch_bounds__(TL_WARPS * 32) k_tile_labels(const uint32_t* _
           const uint32_t ws = __shfl_sync(0xffffffffu, starts, it);
           const size_t p = size_t(it) * 32 + lane;
           if (c0 + p < size_t(g.W))
-            dst[p] = ((wb >> lane) & 1u) ? tb[it * 17 + __popc(ws & ((2u << lane) - 1u)) - 1] : 0u;
+            dst[p] = ((wb >> lane) & 1u) ? tb[it * 17 + __popc(ws & ((2u << lane) - 1u)) - 1]
+                                         : OUT(0);
         }
       }
     }
@@ -2788,8 +2810,59 @@ int launch_ccl(const uint32_t* bits, uint32_t* labels, const Geo& gb, CclScratch
   const size_t warps = size_t(g.BH) * size_t((g.wpr + 31) / 32);
   dim3 lg(unsigned(std::min<size_t>((warps + TL_WARPS - 1) / TL_WARPS, 148 * 16)),
           unsigned(gb.batch));
-  pdl(k_tile_labels, lg, TL_WARPS * 32, 0, st, bits, s.parent, s.size, labels, g);
+  pdl(k_tile_labels<uint32_t>, lg, TL_WARPS * 32, 0, st, bits, s.parent, s.size, labels, g,
+      LabelMap64{}, 1);
   return launches + 1;
+}
+
+int launch_ccl_prepare(const uint32_t* bits, const Geo& gb, CclScratch& s, cudaStream_t st) {
+  if ((unsigned long long)gb.w * (unsigned long long)gb.h >= 0xfffffffeull)
+    fail(SLCS_ERR_TOO_LARGE, "image too large for packed coordinate labels");
+  if (ccl_small_path(gb.w, gb.h) || gb.batch != 1)
+    fail(SLCS_ERR_ARG, "ccl_prepare: a single image larger than 256x256");
+  check_key_range(gb, "ccl");
+  G g = make_g(gb);
+  int launches = 0;
+  large_local_and_merge(bits, nullptr, g, 1, s, MODE_CCL, st, launches);
+  return launches;
+}
+
+// the u32 labels of one row (a band's border record), from the union-find
+__global__ void k_row_labels(const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ P,
+                             const uint32_t* __restrict__ MK, G g, int row,
+                             uint32_t* __restrict__ out) {
+  slcs_pdl_wait();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= g.wpr) return;
+  const int k = row >> 1;
+  const uint32_t T = __ldg(ubits + size_t(2 * k) * g.pitch + j);
+  const uint32_t B = 2 * k + 1 < g.H ? __ldg(ubits + size_t(2 * k + 1) * g.pitch + j) : 0u;
+  uint32_t rb[16];
+  run_root_blocks(P, g, k, j, T, B, rb);
+  const uint32_t starts = (T | B) & ~((T | B) << 1), bits = (row & 1) ? B : T;
+  for (int x = 0; x < 32 && 32 * j + x < g.W; ++x)
+    out[32 * j + x] = ((bits >> x) & 1u)
+                          ? linear_label(g, MK[pick16(rb, __popc(starts & ((2u << x) - 1u)) - 1)])
+                          : 0u;
+}
+
+int launch_ccl_row_labels(const uint32_t* bits, const Geo& gb, const CclScratch& s, int row,
+                          uint32_t* out, cudaStream_t st) {
+  G g = make_g(gb);
+  pdl(k_row_labels, unsigned((g.wpr + 127) / 128), 128, 0, st, bits, s.parent, s.size, g, row,
+      out);
+  return 1;
+}
+
+int launch_ccl_labels64(const uint32_t* bits, const Geo& gb, const CclScratch& s,
+                        const LabelMap64& map, unsigned long long* out, cudaStream_t st) {
+  G g = make_g(gb);
+  const size_t warps = size_t(g.BH) * size_t((g.wpr + 31) / 32);
+  dim3 lg(unsigned(std::min<size_t>((warps + TL_WARPS - 1) / TL_WARPS, 148 * 16)), 1u);
+  const int vec_ok = reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  pdl(k_tile_labels<unsigned long long>, lg, TL_WARPS * 32, 0, st, bits, s.parent, s.size, out, g,
+      map, vec_ok);
+  return 1;
 }
 
 template <int KOUT, int NB, int TK>

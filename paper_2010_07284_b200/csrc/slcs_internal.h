@@ -322,6 +322,45 @@ int launch_band_ccl_merge_relabel(int nb, int w, int me, const void* records,
                                   const unsigned long long* row0w_host, void* scratch,
                                   const uint32_t* labels, size_t npx, unsigned long long* out,
                                   cudaStream_t st);
+// A band's u32 label -> its global 64-bit label: offset (first row of the band
+// times W) + l, or the merged value of a component that crosses a band border
+// (open-addressed hash rkeys -> rvals, EMPTY = ~0; any = 0: a single band)
+struct LabelMap64 {
+  unsigned long long offset = 0;
+  const unsigned long long* rkeys = nullptr;
+  const unsigned long long* rvals = nullptr;
+  uint32_t rmask = 0;
+  int any = 0;
+};
+__device__ __forceinline__ uint32_t band_hash_slot(unsigned long long key, uint32_t mask) {
+  key ^= key >> 33;
+  key *= 0xff51afd7ed558ccdull;
+  key ^= key >> 33;
+  return uint32_t(key) & mask;
+}
+__device__ __forceinline__ unsigned long long map_label64(uint32_t l, const LabelMap64& m) {
+  if (!l) return 0ull;
+  if (m.any) {
+    for (uint32_t h = band_hash_slot(l, m.rmask);; h = (h + 1) & m.rmask) {
+      const unsigned long long k = __ldg(m.rkeys + h);
+      if (k == l) return __ldg(m.rvals + h);
+      if (k == ~0ull) break;
+    }
+  }
+  return m.offset + l;
+}
+// the cross-band merge alone: fills *map (tables in scratch) for this band
+int launch_band_ccl_merge(int nb, int w, int me, const void* records,
+                          const unsigned long long* row0w_host, void* scratch, LabelMap64* map,
+                          cudaStream_t st);
+// band CCL without a u32 label image: local union-find (P / max keys in s),
+// the u32 labels of rows r0 and r1 (the border record), then the global 64-bit
+// labels written straight from the union-find through `map`
+int launch_ccl_prepare(const uint32_t* bits, const Geo& gb, CclScratch& s, cudaStream_t st);
+int launch_ccl_row_labels(const uint32_t* bits, const Geo& gb, const CclScratch& s, int row,
+                          uint32_t* out, cudaStream_t st);
+int launch_ccl_labels64(const uint32_t* bits, const Geo& gb, const CclScratch& s,
+                        const LabelMap64& map, unsigned long long* out, cudaStream_t st);
 
 // ---- PNG ingest/egress (png.cu) --------------------------------------------------
 struct PngInfo {

@@ -79,6 +79,25 @@ def test_banded_ccl_equals_single_image_labels(dev, world, w, h, ud):
     assert np.array_equal(np.concatenate(got), want)
 
 
+@pytest.mark.parametrize("world", [1, 3])
+@pytest.mark.parametrize("w,h", [(200, 150), (256, 256), (257, 90), (1000, 64)])
+@pytest.mark.parametrize("given_labels", [False, True])
+def test_banded_ccl_both_paths(dev, world, w, h, given_labels):
+    """ccl_banded without labels (slcs_ccl_band_begin/finish: 64-bit labels
+    straight from the union-find; bands the one-CTA path takes keep u32 labels)
+    and with band labels given (slcs_band_ccl_relabel) agree with the whole image."""
+    from paper_2010_07284_b200 import ccl
+    from paper_2010_07284_b200.bands import ccl_banded
+    u = O.random_mask(w, h, 0.45, O.Rng(w * 3 + h + world))
+    ub = split(dev, u, world)
+
+    def one(c, b):
+        local = ccl.label(b, dev) if given_labels else None
+        return ccl_banded(c, b, local).cpu().numpy()
+    got = LocalGroup(world).run(one, ub)
+    assert np.array_equal(np.concatenate(got), O.flood_fill_label(u).astype(np.int64))
+
+
 def test_banded_ccl_blob_and_64bit_offsets(dev):
     # a giant blob component crossing every band; labels of the lower bands exceed
     # the band-local range, exercising the 64-bit global offsets
@@ -138,3 +157,32 @@ def test_banded_c5_scale_equals_whole_image(dev, world):
     for (r0, r1), l64 in zip(spans, labs):
         want = lab[r0 * n:r1 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
         assert torch.equal(l64.view(-1), want), (r0, r1)
+
+
+def test_ccl_band_job_errors_and_early_destroy(dev):
+    """A job can be destroyed without finishing; bad finish arguments are a
+    status code, and the job stays destroyable."""
+    import ctypes as C
+    from paper_2010_07284_b200 import _lib
+    from paper_2010_07284_b200.bands import _zeros
+    L = _lib.load()
+    u = O.random_mask(700, 300, 0.5, O.Rng(5))
+    img = DeviceImage.upload(u, PixelKind.Bool, dev)
+    rec = _zeros(L.slcs_band_record_bytes(1, 700), dev)
+    for finish in (False, True):
+        job = C.c_void_p()
+        assert L.slcs_ccl_band_begin(dev.handle, img.handle, C.c_void_p(rec.data_ptr()),
+                                     C.byref(job)) == 0
+        if finish:
+            hs = (C.c_longlong * 1)(300)
+            rc = L.slcs_ccl_band_finish(job, 1, 3, C.c_void_p(rec.data_ptr()), hs,
+                                        C.c_void_p(rec.data_ptr()))
+            assert rc != 0 and "band" in L.slcs_last_error().decode()
+        assert L.slcs_ccl_job_destroy(job) == 0
+    lab = DeviceImage.upload(u, PixelKind.Bool, dev)
+    job = C.c_void_p()
+    from paper_2010_07284_b200 import ccl
+    labels = ccl.label(lab, dev)
+    rc = L.slcs_ccl_band_begin(dev.handle, labels.handle, C.c_void_p(rec.data_ptr()),
+                               C.byref(job))
+    assert rc != 0 and "expects a boolean image" in L.slcs_last_error().decode()
