@@ -49,6 +49,9 @@ namespace cg = cooperative_groups;
 #ifndef SLCS_FIRST_RUN_ALU
 #define SLCS_FIRST_RUN_ALU 1
 #endif
+#ifndef SLCS_TL_PHASES
+#define SLCS_TL_PHASES 0  // diagnostics: per-phase clock64 of k_tile_local (stderr)
+#endif
 #ifndef SLCS_TL_FUSED_ROOTS
 #define SLCS_TL_FUSED_ROOTS 1
 #endif
@@ -533,6 +536,21 @@ constexpr int LT_LIST = 520;                     // count + <= 512 ring roots
 constexpr int LT_THREADS = LUNITS;
 
 enum { MODE_CCL = 0, MODE_REACH = 1, MODE_SIZE = 2 };
+#if SLCS_TL_PHASES
+__device__ unsigned long long tl_phase_acc[8];
+#define TL_MARK(i)                                                   \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      const long long t_ = clock64();                                \
+      atomicAdd(&tl_phase_acc[i], (unsigned long long)(t_ - tl_t0)); \
+      tl_t0 = t_;                                                    \
+    }                                                                \
+  } while (0)
+#else
+#define TL_MARK(i) \
+  do {             \
+  } while (0)
+#endif
 
 // Tile-local pass.  Per run: P[key block] = local root + 1.  Per local root:
 // F = "holds a seed" (reach) or SZ = local pixel count (maxvol).  Per tile:
@@ -578,14 +596,19 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   }
   sT[u0] = Tw;
   sB[u0] = Bw;
+#if SLCS_TL_PHASES
+  long long tl_t0 = clock64();
+#endif
 #if SLCS_TL_QUEUE
   // touch + fl (16 KB) are free until the roots are known: the link queue
   __shared__ int s_qn[LT_THREADS / 32];
   if (threadIdx.x < LT_THREADS / 32) s_qn[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
+  TL_MARK(0);
   T tile{par, sT, sB};
   tile.link(u0, Tw, Bw, reinterpret_cast<uint32_t*>(touch), s_qn);
+  TL_MARK(1);
   uint32_t rt[16];
   // FUSED: the roots are found inside the per-run output loop below (one pass
   // over the runs instead of two); maxvol's sizes alias par, so it keeps the
@@ -660,8 +683,10 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
     if (MODE == MODE_SIZE && cs >= 0) atomicAdd(lsz + cs, cn);
   }
   __syncthreads();
+  TL_MARK(2);
   uint32_t mk[16];  // MODE_CCL: component max keys (roots are hash-ordered)
   if (MODE == MODE_CCL && SZ) tile.max_keys(u0, Tw, Bw, rt, mk);
+  TL_MARK(3);
   const size_t tile_id = (size_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   uint32_t* L = lists + tile_id * LT_LIST;
   {
@@ -689,6 +714,7 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
     }
   }
   __syncthreads();
+  TL_MARK(4);
   if (threadIdx.x == 0) L[0] = uint32_t(s_cnt);
 }
 
@@ -2602,8 +2628,25 @@ void tile_launch(dim3 grid, const uint32_t* u, const uint32_t* t, CclScratch& s,
                  cudaStream_t st) {
   static PerDevice<int> attr;
   smem_opt_in(attr, k_tile_local<MODE>, tile_smem<MODE>());
+#if SLCS_TL_PHASES
+  {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbolAsync(tl_phase_acc, z, sizeof z, 0, cudaMemcpyHostToDevice, st);
+  }
+#endif
   pdl(k_tile_local<MODE>, grid, LT_THREADS, tile_smem<MODE>(), st, u, t, s.parent, s.flag, s.size,
                                                                  s.lists, g);
+#if SLCS_TL_PHASES
+  {
+    unsigned long long z[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(z, tl_phase_acc, sizeof z);
+    const double n = double(grid.x) * grid.y * grid.z;
+    std::fprintf(stderr, "[tile_local<%d> %0.f tiles, cycles per tile] init %.0f link %.0f "
+                 "roots+out %.0f maxkeys %.0f lists %.0f\n", MODE, n, z[0] / n, z[1] / n,
+                 z[2] / n, z[3] / n, z[4] / n);
+  }
+#endif
 }
 
 static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G& g, int batch,
