@@ -2130,7 +2130,6 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   uint32_t* Ha = reinterpret_cast<uint32_t*>(region + CH_SMEM_STAGE);  // [row][word]
   uint32_t* Hb = Ha + CH_ROWS * CH_TW;
   __shared__ int nl_sh, has_nol, pend_global, pend_mask;
-  __shared__ volatile uint32_t done_sink;
 
   const int tid = threadIdx.x;
   const int tiles_x = (int(g.pitch) + CH_TW - 1) / CH_TW;
@@ -2380,10 +2379,11 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     mark(1);
     // seed: runs of u touching near(target) = near^(ra+1)(prev), not yet seeded
     // (a thread whose runs were all seeded at its last select has nothing to do)
-    // seed stamps are returning atomics: a thread reaches the barrier below only
-    // after its stamps were performed at L2, so the arrival after the barrier
-    // can be a relaxed write (a release there costs a full fence every step)
-    uint32_t done = 0;
+    // A thread that stamped F this step fences before the barrier below, so its
+    // stamps are visible GPU-wide before thread 0's arrival after the barrier:
+    // the arrival itself can be a relaxed write.  (A release on the arrival made
+    // thread 0 pay a full fence every step; stamps are rare, so are these fences.)
+    bool pub = false;
     if (unseeded) {
       uint32_t n[4];
       ch_vwin4_dyn(Hb, lr0, jw, ra + 1, n);
@@ -2401,8 +2401,8 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
           if (l != CH_NOL) {
             if (!(lflag[l] & 1)) lflag[l] |= 4;
           } else {
-            done ^= atomicMin(a.F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))),
-                              gen);
+            atomicMin(a.F + gblk(g, groot(a.P, g, grun(g, k0 + kb0 + q, j, T[q], B[q], m))), gen);
+            pub = true;
           }
         }
       }
@@ -2417,14 +2417,17 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       if (f & 4) {
         f = uint8_t((f & ~4) | 1);
         lflag[i] = f;
-        if (f & 2) done ^= atomicMin(a.F + lroot[i], gen);
+        if (f & 2) {
+          atomicMin(a.F + lroot[i], gen);
+          pub = true;
+        }
       }
       if ((f & 3) == 2) {  // shared and still unseeded: another tile may seed it
         if (f & 8) pend_global = 1;
         else atomicOr(&pend_mask, int(lnbr[i]));
       }
     }
-    if (done == 0x5a5a5a5au) done_sink = done;  // a use, so ptxas keeps ATOM (not RED)
+    if (pub) __threadfence();
     __syncthreads();
     mark(2);
     // arrive (this tile's seeds of step s are published); then wait for the
@@ -2436,9 +2439,9 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       else if (pend_mask) ++nbr_waits;
     }
     if (tid == 0) {
-      // every seed stamp of this step has completed at L2 (returning atomics,
-      // then the block barrier), so a reader that observes these arrivals with
-      // ld.acquire and then loads F through L2 sees the stamps
+      // every seed stamp of this step is visible GPU-wide (its thread fenced
+      // before the block barrier), so a reader that observes these arrivals
+      // with ld.acquire and then loads F sees the stamps
       asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.arrive + s) : "memory");
       asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.tile_arrive + blockIdx.x),
                    "r"(unsigned(s + 1))
