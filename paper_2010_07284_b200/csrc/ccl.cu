@@ -2129,7 +2129,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   uint32_t* stage = reinterpret_cast<uint32_t*>(region);
   uint32_t* Ha = reinterpret_cast<uint32_t*>(region + CH_SMEM_STAGE);  // [row][word]
   uint32_t* Hb = Ha + CH_ROWS * CH_TW;
-  __shared__ int nl_sh, has_nol, pend_global, pend_mask;
+  __shared__ int nl_sh, has_nol, pend_global, pend_mask, pub_any;
 
   const int tid = threadIdx.x;
   const int tiles_x = (int(g.pitch) + CH_TW - 1) / CH_TW;
@@ -2145,6 +2145,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   if (tid == 0) {
     nl_sh = 0;
     has_nol = 0;
+    pub_any = 0;
   }
   uint32_t T[2], B[2];
 #pragma unroll
@@ -2379,10 +2380,9 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     mark(1);
     // seed: runs of u touching near(target) = near^(ra+1)(prev), not yet seeded
     // (a thread whose runs were all seeded at its last select has nothing to do)
-    // A thread that stamped F this step fences before the barrier below, so its
-    // stamps are visible GPU-wide before thread 0's arrival after the barrier:
-    // the arrival itself can be a relaxed write.  (A release on the arrival made
-    // thread 0 pay a full fence every step; stamps are rare, so are these fences.)
+    // Stamping F sets pub_any; thread 0 then makes its arrival a release (fence +
+    // relaxed write) only in steps where this tile stamped something.  A release
+    // on every arrival made thread 0 pay a full fence every step; stamps are rare.
     bool pub = false;
     if (unseeded) {
       uint32_t n[4];
@@ -2427,7 +2427,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
         else atomicOr(&pend_mask, int(lnbr[i]));
       }
     }
-    if (pub) __threadfence();
+    if (pub) pub_any = 1;
     __syncthreads();
     mark(2);
     // arrive (this tile's seeds of step s are published); then wait for the
@@ -2439,9 +2439,13 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       else if (pend_mask) ++nbr_waits;
     }
     if (tid == 0) {
-      // every seed stamp of this step is visible GPU-wide (its thread fenced
-      // before the block barrier), so a reader that observes these arrivals
-      // with ld.acquire and then loads F sees the stamps
+      // release pattern when stamps were made (fence.acq_rel.gpu, cumulative
+      // over the block barrier, then the relaxed writes): a reader that observes
+      // these arrivals with ld.acquire sees this step's stamps
+      if (pub_any) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        pub_any = 0;
+      }
       asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.arrive + s) : "memory");
       asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.tile_arrive + blockIdx.x),
                    "r"(unsigned(s + 1))
