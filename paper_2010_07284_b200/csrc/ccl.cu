@@ -2113,6 +2113,17 @@ __device__ __forceinline__ void ch_vwin4_dyn(const uint32_t* H, int r0, int c, i
   }
 }
 
+// halo records: one 64-bit word carries (step tag, data), so each is written and
+// read with a single-copy-atomic relaxed gpu-scope access and validates itself
+__device__ __forceinline__ void ch_rec_store(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ch_rec_load(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint32_t ch_hash(uint32_t key) { return (key * 0x9E3779B1u) >> 20; }
 
 __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g) {
@@ -2338,11 +2349,11 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     for (int q = 0; q < 2; ++q) {
       if (!hsrc[q]) continue;
       const unsigned long long* p = hsrc[q] + (tag & 1) * halo_bank;
-      unsigned long long v = __ldcg(p);
+      unsigned long long v = ch_rec_load(p);
       for (int spin = 0; (v >> 32) != tag; ++spin) {
         if (spin > (1 << 22)) __trap();  // a producer never arrived: fail, never hang
         __nanosleep(SLCS_CH_SLEEP);
-        v = __ldcg(p);
+        v = ch_rec_load(p);
       }
       stage[hdst[q]] = uint32_t(v);
     }
@@ -2524,10 +2535,11 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       for (int i = 0; i < 4; ++i) {
         const int row = 2 * kb0 + i;  // tile-relative
         const unsigned long long v = tag | uo_keep[i];
-        if (row < 3) __stcg(my_halo + CH_H_TOP + row * CH_TW + jw, v);
-        if (row >= 2 * CH_TB - 3) __stcg(my_halo + CH_H_BOT + (row - (2 * CH_TB - 3)) * CH_TW + jw, v);
-        if (jw == 0) __stcg(my_halo + CH_H_LEFT + row, v);
-        if (jw == CH_TW - 1) __stcg(my_halo + CH_H_RIGHT + row, v);
+        if (row < 3) ch_rec_store(my_halo + CH_H_TOP + row * CH_TW + jw, v);
+        if (row >= 2 * CH_TB - 3)
+          ch_rec_store(my_halo + CH_H_BOT + (row - (2 * CH_TB - 3)) * CH_TW + jw, v);
+        if (jw == 0) ch_rec_store(my_halo + CH_H_LEFT + row, v);
+        if (jw == CH_TW - 1) ch_rec_store(my_halo + CH_H_RIGHT + row, v);
       }
     }
     __syncthreads();
