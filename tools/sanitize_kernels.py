@@ -51,5 +51,29 @@ for (w, h, d) in [(256, 256, 0.5), (1024, 1024, 0.41), (1000, 700, 0.5), (2100, 
         assert np.array_equal(np.concatenate(got), O.flood_fill_label(u).astype(np.int64)), \
             (w, h, "banded ccl")
         n_ok += 3
+# the persistent reach chain (k_reach_chain: halo records, arrivals, flag stamps)
+# and a program's adjacent volumes (k_volume_multi)
+from paper_2010_07284_b200 import synth as S  # noqa: E402
+from paper_2010_07284_b200.executor import Program  # noqa: E402
+from paper_2010_07284_b200.imgql import compile_text  # noqa: E402
+w, h, depth = 900, 700, 12
+img = O.blob_noise(w, h, 5)
+graph = compile_text(S.near_reach_chain(depth) + 'print "v1" volume(b)\nprint "v2" volume(x0)\n')
+out_task = [i for i, t in enumerate(graph.nodes) if t.opcode == "save"][0]
+prog = Program(graph, dev)
+prog.set_input_host("img.png", img, PixelKind.U16)
+prog.run()
+assert "chain of" in prog.plan, prog.plan
+out = np.zeros((h, w), np.uint8)
+prog.download(out_task, out)
+b, x = O.threshold(0, img, 56360), O.threshold(0, img, 62258)
+xs = [x]
+for k in range(depth):
+    x = O.dilate(x) if k % 2 == 0 else O.reach(x, b)
+    xs.append(x)
+assert np.array_equal(out, x), "reach chain"
+vols = [prog.download(i) for i, t in enumerate(graph.nodes) if t.opcode == "volume"]
+assert sorted(vols) == sorted([float(b.sum()), float(xs[0].sum())]), "volumes"
+n_ok += 2
 dev.synchronize()
 print(f"sanitize workload ok: {n_ok} checks, {dev.launches} launches")
