@@ -186,3 +186,33 @@ def test_ccl_band_job_errors_and_early_destroy(dev):
     rc = L.slcs_ccl_band_begin(dev.handle, labels.handle, C.c_void_p(rec.data_ptr()),
                                C.byref(job))
     assert rc != 0 and "expects a boolean image" in L.slcs_last_error().decode()
+
+
+@pytest.mark.parametrize("use_job", [False, True])
+def test_band_labels_to_unaligned_output(dev, use_job):
+    """64-bit label output that is 8- but not 16-byte aligned takes the scalar
+    store path of k_relabel_hash / k_tile_labels<u64>; the labels are the same."""
+    import ctypes as C
+    import torch
+    from paper_2010_07284_b200 import _lib, ccl
+    from paper_2010_07284_b200.bands import _zeros
+    L = _lib.load()
+    w, h = 777, 300
+    u = O.random_mask(w, h, 0.5, O.Rng(9))
+    img = DeviceImage.upload(u, PixelKind.Bool, dev)
+    rec = _zeros(L.slcs_band_record_bytes(1, w), dev)
+    buf = torch.zeros(w * h + 1, dtype=torch.int64, device=torch.device("cuda", dev.device))
+    out_ptr = C.c_void_p(buf.data_ptr() + 8)
+    hs = (C.c_longlong * 1)(h)
+    if use_job:
+        job = C.c_void_p()
+        assert L.slcs_ccl_band_begin(dev.handle, img.handle, C.c_void_p(rec.data_ptr()),
+                                     C.byref(job)) == 0
+        assert L.slcs_ccl_band_finish(job, 1, 0, C.c_void_p(rec.data_ptr()), hs, out_ptr) == 0
+        assert L.slcs_ccl_job_destroy(job) == 0
+    else:
+        lab = ccl.label(img, dev)
+        assert L.slcs_band_ccl_relabel(dev.handle, lab.handle, 1, 0, None, hs, out_ptr) == 0
+    dev.synchronize()
+    got = buf[1:].cpu().numpy().reshape(h, w)
+    assert np.array_equal(got, O.flood_fill_label(u).astype(np.int64))
