@@ -46,9 +46,6 @@ namespace cg = cooperative_groups;
 #ifndef SLCS_TL_QUEUE
 #define SLCS_TL_QUEUE 1
 #endif
-#ifndef SLCS_FIRST_RUN_ALU
-#define SLCS_FIRST_RUN_ALU 1
-#endif
 #ifndef SLCS_TL_PHASES
 #define SLCS_TL_PHASES 0  // diagnostics: per-phase clock64 of k_tile_local (stderr)
 #endif
@@ -111,16 +108,10 @@ G make_g(const Geo& gb) {
 // ---- run helpers ------------------------------------------------------------
 // the run of x that starts at its lowest set bit
 __device__ __forceinline__ uint32_t first_run(uint32_t x) {
-#if SLCS_FIRST_RUN_ALU
   // adding the lowest set bit carries through exactly that run (a run ending
   // at bit 31 carries out): the bits it clears are the run -- ALU ops only
+  // (no FLO/BREV: 3 % faster CCL and reach than an __ffs-based mask)
   return x & ~(x + (x & (0u - x)));
-#else
-  const int s = __ffs(x) - 1;
-  const uint32_t y = ~x & (FULL << s);
-  const uint32_t below = y ? ((y & (0u - y)) - 1u) : FULL;
-  return below & (FULL << s);
-#endif
 }
 
 // the run of c containing bit p (bit p must be set)
