@@ -520,7 +520,10 @@ struct RunTile {
 // Large-image path: 128x256-px tiles (64 bands x 8 words = 512 threads, 4 CTAs per SM).
 constexpr int LKW = 8;
 constexpr int LTWW = 8;
-constexpr int LTNB = 64;
+#ifndef SLCS_LTNB
+#define SLCS_LTNB 64
+#endif
+constexpr int LTNB = SLCS_LTNB;
 constexpr int LUNITS = LTNB * LTWW;              // 512
 constexpr int LSLOTS = LTNB * (1 << (LKW - 1));  // 8192 blocks per tile
 constexpr int LT_LIST = 520;                     // count + <= 512 ring roots
