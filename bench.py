@@ -644,30 +644,32 @@ def c5_result(args, ws, rank, local, dev, stream, n=65536):
     import torch
 
     from paper_2010_07284_b200.bands import (LocalGroup, SoloComm, TorchComm, band_rows,
-                                             ccl_banded, near_banded, reach_banded,
-                                             volume_banded)
+                                             near_banded, reach_ccl_banded, volume_banded)
     from paper_2010_07284_b200.pixlog import random_mask_device
 
     r0, r1 = band_rows(n, ws, rank)
     mask = random_mask_device(n, r1 - r0, 0.5, 1, r0, dev)
     target = random_mask_device(n, r1 - r0, 0.05, 2, r0, dev)
     comm = TorchComm() if ws > 1 else SoloComm()
+    # reach(target, mask) and ccl::label(mask) share one labelling of the band
+    # (reach_ccl_banded); at N=1, 65536^2 labels do not fit 32-bit keys, so both
+    # run as two in-process bands
     if ws == 1 and n * n >= 0xFFFFFFFE:
-        halves = [random_mask_device(n, b - a, 0.5, 1, a, dev)
+        halves = [(random_mask_device(n, b - a, 0.05, 2, a, dev),
+                   random_mask_device(n, b - a, 0.5, 1, a, dev))
                   for a, b in (band_rows(n, 2, 0), band_rows(n, 2, 1))]
 
-        def labels():
-            return LocalGroup(2).run(ccl_banded, halves)
+        def reach_labels():
+            return LocalGroup(2).run(lambda c, b: reach_ccl_banded(c, b[0], b[1]), halves)
     else:
-        def labels():
-            return ccl_banded(comm, mask)
+        def reach_labels():
+            return reach_ccl_banded(comm, target, mask)
 
     def step():
         x = near_banded(comm, mask, 4)
         v = volume_banded(comm, x)
-        r = reach_banded(comm, target, mask)
-        lab = labels()
-        return v, r, lab
+        rl = reach_labels()
+        return v, rl
 
     vol = None
     for _ in range(max(3, args.warmup)):
@@ -705,6 +707,8 @@ def c5_result(args, ws, rank, local, dev, stream, n=65536):
                    "exchange": "near^4: 4 packed rows each way per neighbour (NCCL send/recv);"
                                " volume: 8 B all-reduce; reach/ccl: border records "
                                "all-gathered (NCCL), device union-find",
+                   "labelling": "reach and ccl::label of the mask share one band "
+                                "union-find (reach_ccl_banded)",
                    "timing": "CUDA events on the bands' stream around the K steps "
                              "(exchanges included), max over ranks",
                    "l2": "no flush: each step's working set (mask, target, 64-bit labels) "

@@ -194,8 +194,13 @@ int slcs_band_ccl_relabel(slcs_ctx* ctx, const slcs_image* labels, int nb, int m
  * instead of 4 B/px labels written, read back and relabelled).  A job is
  * destroyed with slcs_ccl_job_destroy, finished or not. */
 typedef struct slcs_ccl_job slcs_ccl_job;
+typedef struct slcs_reach_state slcs_reach_state;
 int slcs_ccl_band_begin(slcs_ctx* ctx, const slcs_image* band, void* record_dev,
                         slcs_ccl_job** job);
+/* The band's ccl::label from the labelling of a band reach on the same image
+ * (slcs_reach_prepare_labels: reach's `through` is the ccl input): no second
+ * union-find.  The reach state must outlive the job. */
+int slcs_ccl_band_begin_reach(slcs_reach_state* st, void* record_dev, slcs_ccl_job** job);
 int slcs_ccl_band_finish(slcs_ccl_job* job, int nb, int me, const void* records_dev,
                          const long long* band_heights, uint64_t* out_dev);
 int slcs_ccl_job_destroy(slcs_ccl_job* job);
@@ -204,9 +209,12 @@ int slcs_ccl_job_destroy(slcs_ccl_job* job);
  * component's root node and a class byte (0 background, 1 unseeded, 2 seeded)
  * to the host; reach_set_flags seeds host-listed roots; finish writes
  * near^k_out(target | selected components) (k_out = 0: no closing near). */
-typedef struct slcs_reach_state slcs_reach_state;
 int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
                        slcs_reach_state** out);
+/* slcs_reach_prepare whose labelling also keeps each component's max key, for
+ * slcs_ccl_band_begin_reach (ccl::label of `through` at no second labelling). */
+int slcs_reach_prepare_labels(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+                              slcs_reach_state** out);
 int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls);
 int slcs_reach_set_flags(slcs_reach_state* st, int n, const uint32_t* roots);
 int slcs_reach_border_record(slcs_reach_state* st, void* record_dev);

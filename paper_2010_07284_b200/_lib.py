@@ -60,6 +60,8 @@ _SIGS = {
     "slcs_ccl_border_record": (i32, [vp, vp, vp]),
     "slcs_band_ccl_relabel": (i32, [vp, vp, i32, i32, vp, vp, vp]),
     "slcs_ccl_band_begin": (i32, [vp, vp, vp, vp]),
+    "slcs_ccl_band_begin_reach": (i32, [vp, vp, vp]),
+    "slcs_reach_prepare_labels": (i32, [vp, vp, vp, vp]),
     "slcs_ccl_band_finish": (i32, [vp, i32, i32, vp, vp, vp]),
     "slcs_ccl_job_destroy": (i32, [vp]),
     "slcs_reach_border_record": (i32, [vp, vp]),

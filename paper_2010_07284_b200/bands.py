@@ -23,7 +23,9 @@ exchanges stays in device memory:
   (``slcs_ccl_band_begin``: the u32 labels of its first and last row, no label
   image), all-gather, then a device merge and the global 64-bit labels written
   straight from the union-find (``slcs_ccl_band_finish``).  With band labels
-  already at hand, ``slcs_ccl_border_record`` + ``slcs_band_ccl_relabel``.
+  already at hand, ``slcs_ccl_border_record`` + ``slcs_band_ccl_relabel``;
+  with a reach on the same image, ``reach_ccl_banded`` labels the band once for
+  both.
 
 Per step and rank the communication is: near^k 2*k packed rows (k * W/8 bytes
 each way), reach 2 * (5 W + W/4) bytes all-gathered per band plus the closing
@@ -384,6 +386,52 @@ def reach_banded(comm: Comm, target: DeviceImage, through: DeviceImage) -> Devic
     finally:
         L.slcs_reach_state_destroy(st)
     return near_banded(comm, sel_band, 1)  # reach = near(t | S)
+
+
+def reach_ccl_banded(comm: Comm, target: DeviceImage, through: DeviceImage):
+    """(reach(target, through), ccl::label(through)) of the full image,
+    restricted to this band, from ONE labelling of the band's `through`
+    (slcs_reach_prepare_labels + slcs_ccl_band_begin_reach): the reach's
+    border-record merge and the labels' merge run as in reach_banded and
+    ccl_banded, the band union-find only once."""
+    import torch
+    L = _lib.load()
+    dev, w, h = target.device, target.width, target.height
+    heights = comm.band_heights(h)
+    hs = (C.c_longlong * comm.world)(*heights)
+    st = C.c_void_p()
+    _check(L.slcs_reach_prepare_labels(dev.handle, target.handle, through.handle, C.byref(st)))
+    try:
+        nrec_l = L.slcs_band_record_bytes(1, w)
+        lrec = _zeros(nrec_l, dev)
+        job = C.c_void_p()
+        _check(L.slcs_ccl_band_begin_reach(st, C.c_void_p(lrec.data_ptr()), C.byref(job)))
+        try:
+            lall = lrec
+            if comm.world > 1:
+                nrec = L.slcs_band_record_bytes(0, w)
+                mine = _zeros(nrec, dev)
+                _check(L.slcs_reach_border_record(st, C.c_void_p(mine.data_ptr())))
+                allrec = _empty(nrec * comm.world, dev)
+                comm.allgather(mine, allrec, dev)
+                _check(L.slcs_band_reach_merge(st, comm.world, comm.rank,
+                                               C.c_void_p(allrec.data_ptr())))
+                lall = _empty(nrec_l * comm.world, dev)
+                comm.allgather(lrec, lall, dev)
+            sel = C.c_void_p()
+            _check(L.slcs_reach_finish(st, 0, C.byref(sel)))
+            sel_band = DeviceImage(sel, dev)
+            out = torch.empty((h, w), dtype=torch.int64, device=torch.device("cuda", dev.device))
+            _check(L.slcs_ccl_band_finish(job, comm.world, comm.rank,
+                                          C.c_void_p(lall.data_ptr()), hs,
+                                          C.c_void_p(out.data_ptr())))
+            if _streams_differ(dev):
+                dev.synchronize()
+        finally:
+            _check(L.slcs_ccl_job_destroy(job))
+    finally:
+        L.slcs_reach_state_destroy(st)
+    return near_banded(comm, sel_band, 1), out
 
 
 def ccl_banded(comm: Comm, band: DeviceImage, local=None):

@@ -823,6 +823,7 @@ int slcs_image_vstack(slcs_ctx* ctx, int n, const slcs_image* const* imgs, slcs_
 
 struct slcs_reach_state {
   slcs_ctx* ctx = nullptr;
+  bool max_keys = false;  // the labelling also holds max keys (slcs_reach_prepare_labels)
   slcs_image* t = nullptr;
   slcs_image* u = nullptr;
   void* scratch = nullptr;
@@ -837,8 +838,8 @@ struct slcs_reach_state {
 
 extern "C" {
 
-int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
-                       slcs_reach_state** out) {
+static int reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+                         slcs_reach_state** out, bool max_keys) {
   return guard([&] {
     LOCKED(ctx);
     if (!out) fail(SLCS_ERR_ARG, "null output");
@@ -847,17 +848,34 @@ int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image
     same_shape(t.p, u.p, "reach");
     if (t.p->geo.batch != 1) fail(SLCS_ERR_ARG, "banded reach takes single images");
     const Geo& g = t.p->geo;
-    auto* st = new slcs_reach_state;
+    std::unique_ptr<slcs_reach_state> st(new slcs_reach_state);
     st->ctx = ctx;
-    size_t sb = ccl_scratch_bytes_large(g.w, g.h, 1, true, false);
+    st->max_keys = max_keys;
+    size_t sb = ccl_scratch_bytes_large(g.w, g.h, 1, true, max_keys);
     st->scratch = ctx->alloc(sb + g.slice * 4);
-    ccl_scratch_carve_large(st->scratch, g.w, g.h, 1, true, false, &st->cs);
+    ccl_scratch_carve_large(st->scratch, g.w, g.h, 1, true, max_keys, &st->cs);
     st->tmp = reinterpret_cast<uint32_t*>(static_cast<char*>(st->scratch) + sb);
-    ctx->launches += launch_reach_prepare(words(t.p), words(u.p), g, st->cs, ctx->stream);
+    try {
+      ctx->launches += launch_reach_prepare(words(t.p), words(u.p), g, st->cs, ctx->stream,
+                                            max_keys);
+    } catch (...) {
+      ctx->release(st->scratch);
+      throw;
+    }
     st->t = t.release();
     st->u = u.release();
-    *out = st;
+    *out = st.release();
   });
+}
+
+int slcs_reach_prepare(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+                       slcs_reach_state** out) {
+  return reach_prepare(ctx, target, through, out, false);
+}
+
+int slcs_reach_prepare_labels(slcs_ctx* ctx, const slcs_image* target, const slcs_image* through,
+                              slcs_reach_state** out) {
+  return reach_prepare(ctx, target, through, out, true);
 }
 
 int slcs_reach_row(slcs_reach_state* st, int row, uint32_t* roots, uint8_t* cls) {
@@ -1215,7 +1233,7 @@ struct slcs_ccl_job {
   slcs_ctx* ctx = nullptr;
   slcs_image* band = nullptr;    // bool view of the band (retained)
   slcs_image* labels = nullptr;  // small path only: the u32 labels
-  void* scratch = nullptr;
+  void* scratch = nullptr;       // owned (null when the labelling is a reach state's)
   CclScratch cs;
 };
 
@@ -1254,6 +1272,30 @@ int slcs_ccl_band_begin(slcs_ctx* ctx, const slcs_image* band, void* record_dev,
                                              reinterpret_cast<uint32_t*>(rec + off[1]), ctx->stream);
     }
     job->band = b.release();
+    *out = job.release();
+  });
+}
+
+int slcs_ccl_band_begin_reach(slcs_reach_state* rs, void* record_dev, slcs_ccl_job** out) {
+  return guard([&] {
+    if (!rs || !out || !record_dev) fail(SLCS_ERR_ARG, "null argument");
+    if (!rs->max_keys)
+      fail(SLCS_ERR_ARG, "the reach state carries no max keys (use slcs_reach_prepare_labels)");
+    slcs_ctx* ctx = rs->ctx;
+    LOCKED(ctx);
+    const Geo& g = rs->u->geo;
+    std::unique_ptr<slcs_ccl_job> job(new slcs_ccl_job);
+    job->ctx = ctx;
+    job->cs = rs->cs;  // borrowed: the reach state must outlive the job
+    size_t off[2];
+    band_label_record_offsets(g.w, off);
+    char* rec = static_cast<char*>(record_dev);
+    ctx->launches += launch_ccl_row_labels(words(rs->u), g, job->cs, 0,
+                                           reinterpret_cast<uint32_t*>(rec + off[0]), ctx->stream);
+    ctx->launches += launch_ccl_row_labels(words(rs->u), g, job->cs, g.h - 1,
+                                           reinterpret_cast<uint32_t*>(rec + off[1]), ctx->stream);
+    rs->u->refs.fetch_add(1);
+    job->band = rs->u;
     *out = job.release();
   });
 }

@@ -529,7 +529,9 @@ constexpr int LSLOTS = LTNB * (1 << (LKW - 1));  // 8192 blocks per tile
 constexpr int LT_LIST = 520;                     // count + <= 512 ring roots
 constexpr int LT_THREADS = LUNITS;
 
-enum { MODE_CCL = 0, MODE_REACH = 1, MODE_SIZE = 2 };
+// MODE_BOTH: reach's seed flags (F) and the labels' max keys (SZ as MK) from one
+// labelling -- a band's reach and ccl::label of the same image share it
+enum { MODE_CCL = 0, MODE_REACH = 1, MODE_SIZE = 2, MODE_BOTH = 3 };
 #if SLCS_TL_PHASES
 __device__ unsigned long long tl_phase_acc[8];
 #define TL_MARK(i)                                                   \
@@ -583,7 +585,9 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
   const uint32_t Bw = (in && r + 1 < g.H) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
   uint32_t ntT = 0, ntB = 0;
-  if (MODE == MODE_REACH && (Tw | Bw)) {
+  constexpr bool SEEDS = MODE == MODE_REACH || MODE == MODE_BOTH;
+  constexpr bool MAXK = MODE == MODE_CCL || MODE == MODE_BOTH;
+  if (SEEDS && (Tw | Bw)) {
     const uint32_t* t = tbits + size_t(slice) * g.slice;
     ntT = near_word(t, g, r, j);
     ntB = r + 1 < g.H ? near_word(t, g, r + 1, j) : 0u;
@@ -611,14 +615,14 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   if (!FUSED) tile.roots(u0, Tw, Bw, rt);
   for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x) {
     reinterpret_cast<uint32_t*>(touch)[q] = 0;
-    if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
+    if (SEEDS) reinterpret_cast<uint32_t*>(fl)[q] = 0;
   }
   __syncthreads();
 #else
   constexpr bool FUSED = false;
   for (int q = threadIdx.x; q < LSLOTS / 4; q += blockDim.x) {
     reinterpret_cast<uint32_t*>(touch)[q] = 0;
-    if (MODE == MODE_REACH) reinterpret_cast<uint32_t*>(fl)[q] = 0;
+    if (SEEDS) reinterpret_cast<uint32_t*>(fl)[q] = 0;
   }
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
             gnode(g, R0 + int(rk >> LKW), C0 + int(rk & lmask));
         if (band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31)))
           touch[rs] = 1;
-        if (MODE == MODE_REACH && (((Tw & ntT) | (Bw & ntB)) & m)) fl[rs] = 1;
+        if (SEEDS && (((Tw & ntT) | (Bw & ntB)) & m)) fl[rs] = 1;
         if (MODE == MODE_SIZE) {
           const uint32_t n = uint32_t(__popc(Tw & m) + __popc(Bw & m));
           if (rs != cs && cs >= 0) atomicAdd(lsz + cs, cn);
@@ -679,7 +683,7 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   __syncthreads();
   TL_MARK(2);
   uint32_t mk[16];  // MODE_CCL: component max keys (roots are hash-ordered)
-  if (MODE == MODE_CCL && SZ) tile.max_keys(u0, Tw, Bw, rt, mk);
+  if (MAXK && SZ) tile.max_keys(u0, Tw, Bw, rt, mk);
   TL_MARK(3);
   const size_t tile_id = (size_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   uint32_t* L = lists + tile_id * LT_LIST;
@@ -697,9 +701,9 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
           const uint32_t bk = T::bkey(ks);
           const uint32_t gk = gkey(g, R0 + int(bk >> LKW), C0 + int(bk & lmask));
           const uint32_t b = kblk(g, gk);
-          if (MODE == MODE_REACH) F[size_t(slice) * g.sb + b] = fl[ks];
+          if (SEEDS) F[size_t(slice) * g.sb + b] = fl[ks];
           if (MODE == MODE_SIZE) SZ[size_t(slice) * g.sb + b] = lsz[ks];
-          if (MODE == MODE_CCL && SZ)  // component max key (MK)
+          if (MAXK && SZ)  // component max key (MK)
             SZ[size_t(slice) * g.sb + b] =
                 gkey(g, R0 + int(mk[i] >> LKW), C0 + int(mk[i] & lmask));
           if (touch[ks]) L[1 + atomicAdd(&s_cnt, 1)] = hnode(gk);
@@ -866,11 +870,12 @@ __global__ void __launch_bounds__(256) k_root_flatten(uint32_t* P, uint8_t* F, u
   if (!moved) return;
   const unsigned grp = __match_any_sync(part, R);
   const bool leader = (threadIdx.x & 31) == __ffs(grp) - 1;
-  if (mode == MODE_REACH) {
+  if (mode == MODE_REACH || mode == MODE_BOTH) {
     uint8_t* Fs = F + size_t(slice) * g.sb;
     const unsigned any = __ballot_sync(part, Fs[gblk(g, rv)] != 0) & grp;
     if (leader && any) Fs[gblk(g, R)] = 1;
-  } else {
+  }
+  if (mode != MODE_REACH && SZ) {
     uint32_t* Ss = SZ + size_t(slice) * g.sb;
     const uint32_t v = Ss[gblk(g, rv)];
     if (mode == MODE_SIZE) {
@@ -2668,6 +2673,8 @@ static void large_local_and_merge(const uint32_t* u, const uint32_t* t, const G&
             unsigned(batch));
   if (mode == MODE_REACH)
     tile_launch<MODE_REACH>(grid, u, t, s, g, st);
+  else if (mode == MODE_BOTH)
+    tile_launch<MODE_BOTH>(grid, u, t, s, g, st);
   else if (mode == MODE_SIZE)
     tile_launch<MODE_SIZE>(grid, u, t, s, g, st);
   else
@@ -2813,11 +2820,14 @@ int launch_reach_labeled(const uint32_t* target, const uint32_t* through, const 
 // reach split in phases for row bands: prepare (labels + seed flags), export a
 // row's roots/classes, import resolved flags, finish (select [+ closing near])
 int launch_reach_prepare(const uint32_t* target, const uint32_t* through, const Geo& gb,
-                         CclScratch& s, cudaStream_t st) {
+                         CclScratch& s, cudaStream_t st, bool max_keys) {
   check_key_range(gb, "reach");
+  if (max_keys && (unsigned long long)gb.w * (unsigned long long)gb.h >= 0xfffffffeull)
+    fail(SLCS_ERR_TOO_LARGE, "image too large for packed coordinate labels");
   G g = make_g(gb);
   int launches = 0;
-  large_local_and_merge(through, target, g, gb.batch, s, MODE_REACH, st, launches);
+  large_local_and_merge(through, target, g, gb.batch, s, max_keys ? MODE_BOTH : MODE_REACH, st,
+                        launches);
   return launches;
 }
 

@@ -273,9 +273,10 @@ int launch_reach(const uint32_t* target, const uint32_t* through, uint32_t* out,
 // (the fused kernel may then read it before its programmatic-launch wait)
 int launch_maxvol(const uint32_t* bits, uint32_t* out, const Geo& gb, CclScratch& s,
                   cudaStream_t st);
-// row bands: reach in phases (large path always)
+// row bands: reach in phases (large path always); max_keys: the labelling also
+// carries each component's max key (s.size), so ccl::label can reuse it
 int launch_reach_prepare(const uint32_t* target, const uint32_t* through, const Geo& gb,
-                         CclScratch& s, cudaStream_t st);
+                         CclScratch& s, cudaStream_t st, bool max_keys = false);
 int launch_reach_row(const uint32_t* through, const CclScratch& s, const Geo& gb, int row,
                      uint32_t* roots, uint8_t* cls, cudaStream_t st);
 int launch_reach_set_flags(const CclScratch& s, const Geo& gb, const uint32_t* roots, int n,

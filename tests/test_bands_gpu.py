@@ -157,6 +157,14 @@ def test_banded_c5_scale_equals_whole_image(dev, world):
     for (r0, r1), l64 in zip(spans, labs):
         want = lab[r0 * n:r1 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
         assert torch.equal(l64.view(-1), want), (r0, r1)
+    del labs
+    # reach + ccl from one labelling (the C5 bench step)
+    from paper_2010_07284_b200.bands import reach_ccl_banded
+    both = grp.run(lambda c, b: reach_ccl_banded(c, b[0], b[1]), list(zip(tgts, masks)))
+    same_rows([x[0] for x in both], reach(whole_t, whole_m, dev))
+    for (r0, r1), (_, l64) in zip(spans, both):
+        want = lab[r0 * n:r1 * n].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(l64.view(-1), want), (r0, r1)
 
 
 def test_ccl_band_job_errors_and_early_destroy(dev):
@@ -216,3 +224,22 @@ def test_band_labels_to_unaligned_output(dev, use_job):
     dev.synchronize()
     got = buf[1:].cpu().numpy().reshape(h, w)
     assert np.array_equal(got, O.flood_fill_label(u).astype(np.int64))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("w,h,ud", [(600, 517, 0.5), (1000, 700, 0.41), (200, 150, 0.45)])
+def test_reach_ccl_banded_shares_one_labelling(dev, world, w, h, ud):
+    """reach_ccl_banded: reach and 64-bit ccl::label of the same band from one
+    union-find equal the whole-image reach and the reference labels."""
+    from paper_2010_07284_b200.bands import reach_ccl_banded
+    rng = O.Rng(w + 11 * world)
+    u = O.random_mask(w, h, ud, rng)
+    t = O.random_mask(w, h, 0.03, rng)
+    ub, tb = split(dev, u, world), split(dev, t, world)
+    got = LocalGroup(world).run(
+        lambda c, b: tuple(x.numpy() if hasattr(x, "numpy") and not hasattr(x, "cpu")
+                           else x.cpu().numpy() for x in reach_ccl_banded(c, b[0], b[1])),
+        list(zip(tb, ub)))
+    assert np.array_equal(np.concatenate([g[0] for g in got]), O.reach(t, u))
+    assert np.array_equal(np.concatenate([g[1] for g in got]),
+                          O.flood_fill_label(u).astype(np.int64))
