@@ -199,7 +199,8 @@ int slcs_ccl_band_begin(slcs_ctx* ctx, const slcs_image* band, void* record_dev,
                         slcs_ccl_job** job);
 /* The band's ccl::label from the labelling of a band reach on the same image
  * (slcs_reach_prepare_labels: reach's `through` is the ccl input): no second
- * union-find.  The reach state must outlive the job. */
+ * union-find.  The job keeps the reach state's labelling alive: the two may
+ * be destroyed in either order. */
 int slcs_ccl_band_begin_reach(slcs_reach_state* st, void* record_dev, slcs_ccl_job** job);
 int slcs_ccl_band_finish(slcs_ccl_job* job, int nb, int me, const void* records_dev,
                          const long long* band_heights, uint64_t* out_dev);

@@ -823,6 +823,7 @@ int slcs_image_vstack(slcs_ctx* ctx, int n, const slcs_image* const* imgs, slcs_
 
 struct slcs_reach_state {
   slcs_ctx* ctx = nullptr;
+  std::atomic<int> refs{1};  // the caller's + one per ccl job borrowing the labelling
   bool max_keys = false;  // the labelling also holds max keys (slcs_reach_prepare_labels)
   slcs_image* t = nullptr;
   slcs_image* u = nullptr;
@@ -974,20 +975,27 @@ int slcs_reach_finish(slcs_reach_state* st, int k_out, slcs_image** out) {
   });
 }
 
+// the state is freed when its last holder lets go (the caller's destroy, or the
+// last ccl job that borrows its labelling)
+static void reach_state_unref(slcs_reach_state* st) {
+  if (st->refs.fetch_sub(1) != 1) return;
+  slcs_ctx* ctx = st->ctx;
+  {
+    LOCKED(ctx);
+    ctx->release(st->scratch);
+    ctx->release(st->d_roots);
+    ctx->release(st->d_cls);
+    ctx->release(st->merge);
+  }
+  slcs_image_release(st->t);
+  slcs_image_release(st->u);
+  delete st;
+}
+
 int slcs_reach_state_destroy(slcs_reach_state* st) {
   return guard([&] {
     if (!st) return;
-    slcs_ctx* ctx = st->ctx;
-    {
-      LOCKED(ctx);
-      ctx->release(st->scratch);
-      ctx->release(st->d_roots);
-      ctx->release(st->d_cls);
-      ctx->release(st->merge);
-    }
-    slcs_image_release(st->t);
-    slcs_image_release(st->u);
-    delete st;
+    reach_state_unref(st);
   });
 }
 
@@ -1234,6 +1242,7 @@ struct slcs_ccl_job {
   slcs_image* band = nullptr;    // bool view of the band (retained)
   slcs_image* labels = nullptr;  // small path only: the u32 labels
   void* scratch = nullptr;       // owned (null when the labelling is a reach state's)
+  slcs_reach_state* reach = nullptr;  // the reach state whose labelling this borrows (ref)
   CclScratch cs;
 };
 
@@ -1286,7 +1295,7 @@ int slcs_ccl_band_begin_reach(slcs_reach_state* rs, void* record_dev, slcs_ccl_j
     const Geo& g = rs->u->geo;
     std::unique_ptr<slcs_ccl_job> job(new slcs_ccl_job);
     job->ctx = ctx;
-    job->cs = rs->cs;  // borrowed: the reach state must outlive the job
+    job->cs = rs->cs;  // borrowed: the job holds a reference to the reach state
     size_t off[2];
     band_label_record_offsets(g.w, off);
     char* rec = static_cast<char*>(record_dev);
@@ -1296,6 +1305,8 @@ int slcs_ccl_band_begin_reach(slcs_reach_state* rs, void* record_dev, slcs_ccl_j
                                            reinterpret_cast<uint32_t*>(rec + off[1]), ctx->stream);
     rs->u->refs.fetch_add(1);
     job->band = rs->u;
+    rs->refs.fetch_add(1);
+    job->reach = rs;
     *out = job.release();
   });
 }
@@ -1343,6 +1354,7 @@ int slcs_ccl_job_destroy(slcs_ccl_job* job) {
     }
     if (job->labels) slcs_image_release(job->labels);
     slcs_image_release(job->band);
+    if (job->reach) reach_state_unref(job->reach);
     delete job;
   });
 }

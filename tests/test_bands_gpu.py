@@ -243,3 +243,33 @@ def test_reach_ccl_banded_shares_one_labelling(dev, world, w, h, ud):
     assert np.array_equal(np.concatenate([g[0] for g in got]), O.reach(t, u))
     assert np.array_equal(np.concatenate([g[1] for g in got]),
                           O.flood_fill_label(u).astype(np.int64))
+
+
+def test_ccl_job_keeps_reach_labelling_alive(dev):
+    """A ccl job borrowed from a reach state stays valid after the reach state is
+    destroyed first (the job holds a reference); labels are still exact."""
+    import ctypes as C
+    import torch
+    from paper_2010_07284_b200 import _lib
+    from paper_2010_07284_b200.bands import _zeros
+    L = _lib.load()
+    w, h = 640, 300
+    rng = O.Rng(21)
+    u, t = O.random_mask(w, h, 0.5, rng), O.random_mask(w, h, 0.03, rng)
+    du, dt = (DeviceImage.upload(x, PixelKind.Bool, dev) for x in (u, t))
+    st, job = C.c_void_p(), C.c_void_p()
+    assert L.slcs_reach_prepare(dev.handle, dt.handle, du.handle, C.byref(st)) == 0
+    rec = _zeros(L.slcs_band_record_bytes(1, w), dev)
+    rc = L.slcs_ccl_band_begin_reach(st, C.c_void_p(rec.data_ptr()), C.byref(job))
+    assert rc != 0 and "max keys" in L.slcs_last_error().decode()
+    assert L.slcs_reach_state_destroy(st) == 0
+    assert L.slcs_reach_prepare_labels(dev.handle, dt.handle, du.handle, C.byref(st)) == 0
+    assert L.slcs_ccl_band_begin_reach(st, C.c_void_p(rec.data_ptr()), C.byref(job)) == 0
+    assert L.slcs_reach_state_destroy(st) == 0  # before the job: the job keeps it alive
+    out = torch.zeros((h, w), dtype=torch.int64, device=torch.device("cuda", dev.device))
+    hs = (C.c_longlong * 1)(h)
+    assert L.slcs_ccl_band_finish(job, 1, 0, C.c_void_p(rec.data_ptr()), hs,
+                                  C.c_void_p(out.data_ptr())) == 0
+    assert L.slcs_ccl_job_destroy(job) == 0
+    dev.synchronize()
+    assert np.array_equal(out.cpu().numpy(), O.flood_fill_label(u).astype(np.int64))
