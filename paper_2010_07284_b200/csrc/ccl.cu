@@ -2027,14 +2027,29 @@ __global__ void __launch_bounds__(NB * LTWW, 2048 / (NB * LTWW)) k_reach_fused(c
 // lookup (correct, slower).  Flags are the label-CSE stamps (gen = reach
 // index + 1; the labelling step zeroes them once per run).
 constexpr int CH_TW = 8;     // words per tile row (256 px)
-constexpr int CH_TB = 56;    // bands per tile (112 rows): 4096^2 -> 16 x 37 = 592 tiles = 4 per SM
+// Tile = 32 bands (64 rows) x 8 words (256 px), 128 threads: 4096^2 -> 16 x 64 =
+// 1024 tiles, 7 co-resident per SM.  Smaller tiles hide the per-step latency better
+// (measured C2: 56 bands / 4 per SM 2.50 ms, 32 / 7 2.30 ms, 16 / 14 2.43 ms,
+// 28 / 8 with a partial warp 2.53 ms).
+#ifndef SLCS_CH_TB
+#define SLCS_CH_TB 32
+#endif
+#ifndef SLCS_CH_MAXL
+#define SLCS_CH_MAXL 1024
+#endif
+#ifndef SLCS_CH_MINB
+#define SLCS_CH_MINB 7
+#endif
+constexpr int CH_TB = SLCS_CH_TB;  // bands per tile
 constexpr int CH_THREADS = CH_TW * CH_TB / 2;  // a thread owns two stacked bands of one word
 constexpr int CH_R = 3;                       // max stencil radius
 constexpr int CH_ROWS = 2 * CH_TB + 2 * CH_R;  // staged rows
 constexpr int CH_SW = 16;     // staged row stride: halo word, 8 words (16 B aligned), halo word
 constexpr int CH_C0 = 4;      // column of the tile's first word in a staged row
-constexpr int CH_MAXL = 2048;  // distinct roots with a local id
-constexpr int CH_HASH = 4096;
+constexpr int CH_MAXL = SLCS_CH_MAXL;  // distinct roots with a local id
+constexpr int CH_HASH = 2 * CH_MAXL;
+constexpr int CH_HASH_BITS = CH_HASH == 4096 ? 12 : (CH_HASH == 2048 ? 11 : (CH_HASH == 1024 ? 10 : 13));
+static_assert((1 << CH_HASH_BITS) == CH_HASH, "CH_HASH must be 1024 .. 8192");
 constexpr uint16_t CH_NOL = 0xffffu;
 constexpr size_t CH_SMEM_LIDS = size_t(CH_TW) * CH_TB * 16 * 2;
 constexpr size_t CH_SMEM_ROOTS = size_t(CH_MAXL) * 4;
@@ -2123,9 +2138,11 @@ __device__ __forceinline__ unsigned long long ch_rec_load(const unsigned long lo
   return v;
 }
 
-__device__ __forceinline__ uint32_t ch_hash(uint32_t key) { return (key * 0x9E3779B1u) >> 20; }
+__device__ __forceinline__ uint32_t ch_hash(uint32_t key) {
+  return (key * 0x9E3779B1u) >> (32 - CH_HASH_BITS);
+}
 
-__global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g) {
+__global__ void __launch_bounds__(CH_THREADS, SLCS_CH_MINB) k_reach_chain(ChainArgs a, G g) {
   slcs_pdl_wait();
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
@@ -2177,10 +2194,18 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
       x &= ~m;
       const uint32_t rb = gblk(g, groot(a.P, g, grun(g, k, j, T[q], B[q], m)));
       uint32_t h = ch_hash(rb);
+      bool stored = false;
       for (int probe = 0; probe < CH_HASH; ++probe, h = (h + 1) & (CH_HASH - 1)) {
         const uint32_t old = atomicCAS(hkeys + h, EMPTYK, rb);
-        if (old == EMPTYK || old == rb) break;
+        if (old == EMPTYK || old == rb) {
+          stored = true;
+          break;
+        }
       }
+      // a full table: the root goes without a local id, but still counts as held
+      // here (possibly more than once -- an over-count only makes the other
+      // holders treat it as shared, i.e. wait for it)
+      if (!stored) atomicAdd(a.tilecnt + rb, 1u);
     }
   }
   __syncthreads();
@@ -2188,6 +2213,9 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
     if (hkeys[i] == EMPTYK) continue;
     const int l = atomicAdd(&nl_sh, 1);
     hlid[i] = l < CH_MAXL ? uint16_t(l) : CH_NOL;
+    // a root beyond the local ids is seeded here through F (global stamps): the
+    // other tiles that hold it must count this tile as a holder too
+    if (l >= CH_MAXL) atomicAdd(a.tilecnt + hkeys[i], 1u);
     if (l < CH_MAXL) lroot[l] = hkeys[i];
   }
   __syncthreads();
@@ -2303,6 +2331,7 @@ __global__ void __launch_bounds__(CH_THREADS, 4) k_reach_chain(ChainArgs a, G g)
   // is fixed for the whole chain, so it is resolved once.  Words outside the
   // image stay the zeros the first full staging wrote.
   constexpr int CH_NHALO = 6 * (CH_TW + 2) + 2 * 2 * CH_TB;
+  static_assert(CH_NHALO <= 2 * CH_THREADS, "each thread stages at most two halo words");
   const unsigned long long* hsrc[2] = {nullptr, nullptr};
   int hdst[2] = {0, 0};
 #pragma unroll

@@ -183,6 +183,29 @@ def test_near_reach_chain_small(dev):
     assert np.array_equal(out_of(rep, "o.png"), x)
 
 
+@pytest.mark.parametrize("thr", [45875, 52428, 58982])
+def test_reach_chain_many_components_per_tile(dev, thr):
+    """A random `through` of density 0.3 / 0.2 / 0.1 puts more distinct components in a
+    chain tile than it has local ids (CH_MAXL): those runs take the global-root
+    path and the tile waits on the global arrival count.  Exact vs the oracle."""
+    from paper_2010_07284_b200 import synth as S
+    w, h, depth = 2048, 1024, 8
+    rng = np.random.default_rng(thr)
+    img = rng.integers(0, 65536, size=(h, w), dtype=np.uint16)
+    graph = compile_text(S.near_reach_chain(depth, through_thr=thr, target_thr=65000))
+    out_task = [i for i, t in enumerate(graph.nodes) if t.opcode == "save"][0]
+    prog = Program(graph, dev)
+    prog.set_input_host("img.png", img, PixelKind.U16)
+    prog.run()
+    assert "chain of" in prog.plan, prog.plan
+    out = np.zeros((h, w), np.uint8)
+    prog.download(out_task, out)
+    b, x = O.threshold(0, img, thr), O.threshold(0, img, 65000)
+    for k in range(depth):
+        x = O.dilate(x) if k % 2 == 0 else O.reach(x, b)
+    assert np.array_equal(out, x)
+
+
 @pytest.mark.parametrize("cse", [True, False])
 @pytest.mark.parametrize("graph", [True, False])
 def test_near_reach_chain_large_path_label_cse(dev, cse, graph):
