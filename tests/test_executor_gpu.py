@@ -443,6 +443,39 @@ def test_nan_and_inf_prints_match_reference_executor(dev):
     assert rep.printLines == want
 
 
+@pytest.mark.parametrize("nears,tail", [(0, 1), (2, 3), (1, 2), (2, 0)])
+def test_reach_chain_radii(dev, nears, tail):
+    """Chains whose reaches are separated by 0, 1 or 2 nears (the chain kernel's
+    kmid) and end with 0..3 closing nears (klast), against the oracle."""
+    w, h, n = 1500, 900, 7
+    img = O.blob_noise(w, h, 17)
+    lines = ['load img = "img.png"', "let b = img >. 56360", "let x0 = img >. 62258"]
+    for k in range(n):
+        t = f"x{k}"
+        for _ in range(nears):
+            t = f"near({t})"
+        lines.append(f"let x{k + 1} = reach({t}, b)")
+    res = f"x{n}"
+    for _ in range(tail):
+        res = f"near({res})"
+    lines.append(f'save "out.png" {res}')
+    graph = compile_text("\n".join(lines) + "\n")
+    out_task = [i for i, t in enumerate(graph.nodes) if t.opcode == "save"][0]
+    prog = Program(graph, dev)
+    prog.set_input_host("img.png", img, PixelKind.U16)
+    prog.run()
+    out = np.zeros((h, w), np.uint8)
+    prog.download(out_task, out)
+    b, x = O.threshold(0, img, 56360), O.threshold(0, img, 62258)
+    for _ in range(n):
+        for _ in range(nears):
+            x = O.dilate(x)
+        x = O.reach(x, b)
+    for _ in range(tail):
+        x = O.dilate(x)
+    assert np.array_equal(out, x), prog.plan
+
+
 @pytest.mark.parametrize("w,h,depth", [(700, 500, 20), (1000, 1001, 12), (4100, 37, 9),
                                        (300, 2600, 30), (2048, 2048, 41)])
 def test_reach_chain_one_launch_matches_oracle(dev, w, h, depth):
