@@ -1008,9 +1008,11 @@ def main():
         roofline = {
             "bound": "hbm", "kernel": "k_reach_chain (all 500 reaches of the chain in ONE "
                                       "persistent cooperative launch on a shared labelling of "
-                                      "`through`; per reach: staged window + stencils, seed "
-                                      "flags, one grid barrier, flag pull, select, step-tagged "
-                                      "halo exchange between neighbouring tiles)",
+                                      "`through`; 64x256-px tiles, 7 per SM; per reach: "
+                                      "staged window + stencils, sticky seed flags, an arrival "
+                                      "(a tile waits only for the tiles that can still seed one "
+                                      "of its shared roots), select, step-tagged halo records "
+                                      "to the neighbouring tiles)",
             "achieved": BYTES_PER_PX["reach"] * px * units / launch_s / 1e9, "peak": peak,
             "unit": "GB/s",
             "frac": BYTES_PER_PX["reach"] * px * units / launch_s / 1e9 / peak,
@@ -1023,8 +1025,9 @@ def main():
             "note": "frac >> 1 is not HBM evidence: SURVEY 8(d)'s 8.375 B/px per reach assume a "
                     "u32 labelling materialised per reach; here `through` is labelled once per "
                     "formula and every reach works on L2-resident bit images (DRAM `traffic` "
-                    "per launch).  The kernel is bound by cross-SM latency: per reach one grid "
-                    "barrier + two L2 round trips (flag pull, halo records)",
+                    "per launch).  The kernel is bound by cross-SM latency: per reach the "
+                    "neighbours' halo records (an L2 round trip) plus the window / seed / "
+                    "select work of the slowest tiles; no grid barrier is paid",
             "latency_model": {
                 "per_reach_us": chain_us / units,
                 "grid_barrier_floor_us": 1.64,
