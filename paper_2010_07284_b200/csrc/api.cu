@@ -111,8 +111,23 @@ void stage_fence(int i, int dev, cudaStream_t st) {
   cuda_check(cudaEventRecord(x.ev, st), "event");
   x.pending = true;
 }
-// host source -> pinned staging copy (or the source itself when too big)
+// Page-locked host memory (cudaHostAlloc / cudaHostRegister, e.g. a torch
+// pin_memory() tensor) is a DMA source/target already: copies go straight to and
+// from it at full link speed instead of through a staging memcpy.  Pageable
+// memory (the reference's std::vector-backed ImageBuffer) keeps the staging path.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // an unregistered pointer is not an error here
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// host source -> pinned staging copy (or the source itself when it is pinned
+// already or too big to stage)
 const void* stage_in(int i, const void* src, size_t n) {
+  if (host_pinned(src)) return src;
   void* p = stage_slot(i, n);
   if (!p) return src;
   std::memcpy(p, src, n);
@@ -132,7 +147,7 @@ struct HostOut {
     slot = i;
     dst = host;
     n = bytes;
-    void* p = stage_slot(i, bytes);
+    void* p = host_pinned(host) ? nullptr : stage_slot(i, bytes);
     staged = p != nullptr;
     cuda_check(cudaMemcpyAsync(staged ? p : host, dev_src, bytes, cudaMemcpyDeviceToHost, st),
                what);
@@ -625,9 +640,24 @@ int slcs_image_upload(slcs_ctx* ctx, slcs_kind kind, int w, int h, int batch, co
     if (!host) fail(SLCS_ERR_ARG, "null source buffer");
     check_dims(w, h, batch);
     const void* src = stage_in(0, host, host_bytes(kind, w, h, batch));
-    LOCKED(ctx);
-    *out = upload(ctx, kind, w, h, batch, src, false);
-    if (src != host) stage_fence(0, ctx->device, ctx->stream);
+    cudaEvent_t done = nullptr;
+    {
+      LOCKED(ctx);
+      *out = upload(ctx, kind, w, h, batch, src, false);
+      if (src != host) {
+        stage_fence(0, ctx->device, ctx->stream);
+      } else if (host_pinned(host)) {
+        // a pinned source is read by the DMA after this call would return: the
+        // caller may reuse its buffer only once the copy is done
+        cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(done, ctx->stream), "event");
+      }
+    }
+    if (done) {
+      const cudaError_t e = cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+      cuda_check(e, "upload wait");
+    }
   });
 }
 

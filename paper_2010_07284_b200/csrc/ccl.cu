@@ -332,9 +332,9 @@ struct RunTile {
     }
   }
   // After roots(): the max key of each run's component into the root's slot
-  // (par is free again); returns this thread's per-run component max keys.
-  __device__ void max_keys(int u, uint32_t T, uint32_t B, const uint32_t (&r)[16],
-                           uint32_t (&mk)[16]) const {
+  // (par is free again).  Afterwards par[nslot(r[i])] is run i's component max
+  // key (read it there: a per-run register copy spills at 32 registers).
+  __device__ void max_keys_only(int u, uint32_t T, uint32_t B, const uint32_t (&r)[16]) const {
     const int band = u / TWW, w = u % TWW;
     uint32_t x = T | B;
 #pragma unroll
@@ -361,6 +361,11 @@ struct RunTile {
     }
     if (T | B) atomicMax(par + nslot(cr), ck);
     __syncthreads();
+  }
+  // max_keys_only, then this thread's per-run component max keys in registers
+  __device__ void max_keys(int u, uint32_t T, uint32_t B, const uint32_t (&r)[16],
+                           uint32_t (&mk)[16]) const {
+    max_keys_only(u, T, B, r);
 #pragma unroll
     for (int i = 0; i < 16; ++i) mk[i] = par[nslot(r[i])];
   }
@@ -584,13 +589,14 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   const bool in = kb < g.BH && j < g.wpr;
   const uint32_t Tw = in ? __ldg(u + size_t(r) * g.pitch + j) : 0u;
   const uint32_t Bw = (in && r + 1 < g.H) ? __ldg(u + size_t(r + 1) * g.pitch + j) : 0u;
-  uint32_t ntT = 0, ntB = 0;
+  // the word's seed pixels: through & near(target), both rows folded into one
+  // column mask (a run is seeded iff it meets it; one live register across link)
+  uint32_t sdw = 0;
   constexpr bool SEEDS = MODE == MODE_REACH || MODE == MODE_BOTH;
   constexpr bool MAXK = MODE == MODE_CCL || MODE == MODE_BOTH;
   if (SEEDS && (Tw | Bw)) {
     const uint32_t* t = tbits + size_t(slice) * g.slice;
-    ntT = near_word(t, g, r, j);
-    ntB = r + 1 < g.H ? near_word(t, g, r + 1, j) : 0u;
+    sdw = (Tw & near_word(t, g, r, j)) | (r + 1 < g.H ? Bw & near_word(t, g, r + 1, j) : 0u);
   }
   sT[u0] = Tw;
   sB[u0] = Bw;
@@ -669,7 +675,7 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
             gnode(g, R0 + int(rk >> LKW), C0 + int(rk & lmask));
         if (band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31)))
           touch[rs] = 1;
-        if (SEEDS && (((Tw & ntT) | (Bw & ntB)) & m)) fl[rs] = 1;
+        if (SEEDS && (sdw & m)) fl[rs] = 1;
         if (MODE == MODE_SIZE) {
           const uint32_t n = uint32_t(__popc(Tw & m) + __popc(Bw & m));
           if (rs != cs && cs >= 0) atomicAdd(lsz + cs, cn);
@@ -682,8 +688,9 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
   }
   __syncthreads();
   TL_MARK(2);
-  uint32_t mk[16];  // MODE_CCL: component max keys (roots are hash-ordered)
-  if (MAXK && SZ) tile.max_keys(u0, Tw, Bw, rt, mk);
+  // MODE_CCL: component max keys (roots are hash-ordered) land in par at the
+  // roots' slots
+  if (MAXK && SZ) tile.max_keys_only(u0, Tw, Bw, rt);
   TL_MARK(3);
   const size_t tile_id = (size_t(slice) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   uint32_t* L = lists + tile_id * LT_LIST;
@@ -703,9 +710,10 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
           const uint32_t b = kblk(g, gk);
           if (SEEDS) F[size_t(slice) * g.sb + b] = fl[ks];
           if (MODE == MODE_SIZE) SZ[size_t(slice) * g.sb + b] = lsz[ks];
-          if (MAXK && SZ)  // component max key (MK)
-            SZ[size_t(slice) * g.sb + b] =
-                gkey(g, R0 + int(mk[i] >> LKW), C0 + int(mk[i] & lmask));
+          if (MAXK && SZ) {  // component max key (MK)
+            const uint32_t mk = par[ks];
+            SZ[size_t(slice) * g.sb + b] = gkey(g, R0 + int(mk >> LKW), C0 + int(mk & lmask));
+          }
           if (touch[ks]) L[1 + atomicAdd(&s_cnt, 1)] = hnode(gk);
         }
       }
