@@ -670,9 +670,6 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
           rt[i] = last;
         }
         const int rs = T::nslot(rt[i]);
-        const uint32_t rk = T::bkey(rs);  // the root's block stands for it globally
-        Ps[kblk(g, gkey(g, R0 + int(k >> LKW), C0 + int(k & lmask)))] =
-            gnode(g, R0 + int(rk >> LKW), C0 + int(rk & lmask));
         if (band == 0 || band == LTNB - 1 || (w == 0 && (m & 1u)) || (w == LTWW - 1 && (m >> 31)))
           touch[rs] = 1;
         if (SEEDS && (sdw & m)) fl[rs] = 1;
@@ -703,8 +700,17 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
         const uint32_t m = first_run(x);
         x &= ~m;
         const uint32_t k = T::key(band, w, Tw, Bw, m);
+        const int ks = T::slot(k);
+        // P (run key block -> local root node) is staged in par, whose LSLOTS
+        // slots are exactly the tile's 2x2 blocks, and leaves below as whole
+        // 512 B band rows (scattered 4 B stores left partial sectors that L2
+        // refilled from DRAM: ~1 B/px of reads).  A slot is the key block of one
+        // run only, so this thread is its only reader (a root's size / max key)
+        // and writer from here on; slots without a run key keep stale values,
+        // which nothing reads.
+        const uint32_t rk = T::bkey(T::nslot(rt[i]));  // the root's block stands for it globally
+        const uint32_t pv = gnode(g, R0 + int(rk >> LKW), C0 + int(rk & lmask));
         if (rt[i] == T::node(k)) {  // local root
-          const int ks = T::slot(k);
           const uint32_t bk = T::bkey(ks);
           const uint32_t gk = gkey(g, R0 + int(bk >> LKW), C0 + int(bk & lmask));
           const uint32_t b = kblk(g, gk);
@@ -716,12 +722,31 @@ __global__ void __launch_bounds__(LT_THREADS, SLCS_TL_MINB) k_tile_local(const u
           }
           if (touch[ks]) L[1 + atomicAdd(&s_cnt, 1)] = hnode(gk);
         }
+        par[ks] = pv;
       }
     }
   }
   __syncthreads();
   TL_MARK(4);
   if (threadIdx.x == 0) L[0] = uint32_t(s_cnt);
+  {
+    constexpr int BPR = 1 << (LKW - 1);  // blocks per tile band row (128)
+    const int bx0 = blockIdx.x * BPR, nbx = min(BPR, g.BW - bx0);
+    const int kb0 = blockIdx.y * LTNB, nkb = min(LTNB, g.BH - kb0);
+    if ((g.BW & 3) == 0) {
+      for (int e = threadIdx.x; e < nkb * (BPR / 4); e += blockDim.x) {
+        const int bi = e / (BPR / 4), q = e % (BPR / 4);
+        if (4 * q < nbx)
+          *reinterpret_cast<uint4*>(Ps + size_t(kb0 + bi) * size_t(g.BW) + bx0 + 4 * q) =
+              *reinterpret_cast<const uint4*>(par + bi * BPR + 4 * q);
+      }
+    } else {
+      for (int e = threadIdx.x; e < nkb * BPR; e += blockDim.x) {
+        const int bi = e / BPR, c = e % BPR;
+        if (c < nbx) Ps[size_t(kb0 + bi) * size_t(g.BW) + bx0 + c] = par[e];
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ void load_unit(const uint32_t* u, const G& g, int k, int j,
