@@ -198,37 +198,6 @@ __device__ void gunite(uint32_t* P, const G& g, uint32_t a, uint32_t b) {
 }
 
 
-// Border links are emitted per word; along a tile border consecutive lanes
-// usually link the same pair of local roots.  A lane skips its union when the
-// previous lane of the warp linked the identical (local root, local root)
-// pair -- checked with one shuffle, so a straight border costs one union.
-__device__ __forceinline__ void gunite_dedup(uint32_t* P, const G& g, uint32_t a, uint32_t b,
-                                             bool active) {
-  const uint32_t la = active ? __ldcg(P + gblk(g, a)) : 0u;
-  const uint32_t lb = active ? __ldcg(P + gblk(g, b)) : 0u;
-  const uint32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
-  const unsigned mask = __activemask();
-  const int lane = threadIdx.x & 31;
-  const uint32_t plo = __shfl_up_sync(mask, lo, 1), phi = __shfl_up_sync(mask, hi, 1);
-  const bool prev_active = lane > 0 && ((mask >> (lane - 1)) & 1u);
-  if (!active) return;
-  if (prev_active && plo == lo && phi == hi) return;
-  if (la != lb) gunite(P, g, la, lb);
-}
-
-// gunite_dedup for a pair of already-looked-up ancestors (la, lb)
-__device__ __forceinline__ void unite_dedup_pair(uint32_t* P, const G& g, uint32_t la, uint32_t lb,
-                                                 bool active) {
-  const uint32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
-  const unsigned mask = __activemask();
-  const int lane = threadIdx.x & 31;
-  const uint32_t plo = __shfl_up_sync(mask, lo, 1), phi = __shfl_up_sync(mask, hi, 1);
-  const bool prev_active = lane > 0 && ((mask >> (lane - 1)) & 1u);
-  if (!active) return;
-  if (prev_active && plo == lo && phi == hi) return;
-  if (la != lb) gunite(P, g, la, lb);
-}
-
 // read-only find (concurrent writers only ever store final roots)
 __device__ __forceinline__ uint32_t gfind_ro(const uint32_t* P, const G& g, uint32_t v) {
   uint32_t q = __ldcg(P + gblk(g, v));
@@ -782,9 +751,16 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
   if ((threadIdx.x & 31) == 0) s_qn[mw] = 0;
   __syncwarp();
 #endif
-  // units [0, nA): horizontal tile borders; [nA, nA + nB): vertical ones
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nA + nB;
-       i += gridDim.x * blockDim.x) {
+  // units [0, nA): horizontal tile borders; [nA, nA + nB): vertical ones.  The
+  // loop is warp-uniform so the vertical-border lanes of a warp can dedupe their
+  // unions together.
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < nA + nB;
+       base += gridDim.x * blockDim.x) {
+    const uint32_t i = base + uint32_t(lane);
+    const unsigned maskA = __ballot_sync(FULL, i < nA);
+    const unsigned maskB = __ballot_sync(FULL, i < nA + nB && i >= nA);
+    if (i >= nA + nB) continue;
     if (i < nA) {
       const int t = int(i / uint32_t(g.wpr)), j = int(i - uint32_t(t) * uint32_t(g.wpr));
       const int k = (t + 1) * LTNB;
@@ -839,7 +815,14 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
         if ((td & 1u) && (Bl >> 31)) link(grun(g, k - 1, j - 1, Tl, Bl, run_at(Tl | Bl, 31)));
         if ((td >> 31) && (Br & 1u)) link(grun(g, k - 1, j + 1, Tr, Br, run_at(Tr | Br, 0)));
       }
-      unite_dedup_pair(Ps, g, fa, fb, !first);
+      {
+        // each lane's first pair: one union per distinct pair of the warp
+        const uint32_t lo = min(fa, fb), hi = max(fa, fb);
+        const bool need = !first && lo != hi;
+        const unsigned long long key = (static_cast<unsigned long long>(hi) << 32) | lo;
+        const unsigned grp = __match_any_sync(maskA, need ? key : 0ull);
+        if (need && lane == __ffs(grp) - 1) gunite(Ps, g, fa, fb);
+      }
     } else {
       const uint32_t i2 = i - nA;
       const int t = int(i2 / uint32_t(g.BH)), k = int(i2 - uint32_t(t) * uint32_t(g.BH));
@@ -848,21 +831,41 @@ __global__ void k_tile_merge(const uint32_t* __restrict__ ubits, uint32_t* P, G 
       load_unit(u, g, k, jl, Tl, Bl);
       load_unit(u, g, k, jr, Tr, Br);
       const uint32_t cl = Tl | Bl, cr = Tr | Br;
-      // consecutive lanes walk down one border: dedupe the horizontal link
-      const bool hlink = (cl >> 31) && (cr & 1u);
-      const uint32_t va = hlink ? grun(g, k, jl, Tl, Bl, run_at(cl, 31)) : 0u;
-      const uint32_t vb = hlink ? grun(g, k, jr, Tr, Br, run_at(cr, 0)) : 0u;
-      gunite_dedup(Ps, g, va, vb, hlink);
+      // Up to three links per band: the horizontal one and the two diagonals into
+      // the band above (when that band is in the same tile row and the pixel
+      // straight above is clear).  Each is taken between the endpoints' current
+      // ancestors (local roots or above).  Down one border the links mostly join
+      // the same two pieces, so the warp's lanes match their pairs and one lane
+      // per distinct pair unites: a dense border costs a union per warp, not per
+      // band.
+      uint32_t pa[3] = {0u, 0u, 0u}, pb[3] = {0u, 0u, 0u};
+      if ((cl >> 31) && (cr & 1u)) {
+        pa[0] = __ldcg(Ps + gblk(g, grun(g, k, jl, Tl, Bl, run_at(cl, 31))));
+        pb[0] = __ldcg(Ps + gblk(g, grun(g, k, jr, Tr, Br, run_at(cr, 0))));
+      }
       if (k % LTNB != 0 && ((Tr & 1u) || (Tl >> 31))) {
         uint32_t Tul, Bul, Tur, Bur;
         load_unit(u, g, k - 1, jl, Tul, Bul);
         load_unit(u, g, k - 1, jr, Tur, Bur);
-        if ((Tr & 1u) && (Bul >> 31) && !(Bur & 1u))
-          gunite(Ps, g, grun(g, k, jr, Tr, Br, run_at(cr, 0)),
-                 grun(g, k - 1, jl, Tul, Bul, run_at(Tul | Bul, 31)));
-        if ((Tl >> 31) && (Bur & 1u) && !(Bul >> 31))
-          gunite(Ps, g, grun(g, k, jl, Tl, Bl, run_at(cl, 31)),
-                 grun(g, k - 1, jr, Tur, Bur, run_at(Tur | Bur, 0)));
+        if ((Tr & 1u) && (Bul >> 31) && !(Bur & 1u)) {
+          pa[1] = __ldcg(Ps + gblk(g, grun(g, k, jr, Tr, Br, run_at(cr, 0))));
+          pb[1] = __ldcg(Ps + gblk(g, grun(g, k - 1, jl, Tul, Bul, run_at(Tul | Bul, 31))));
+        }
+        if ((Tl >> 31) && (Bur & 1u) && !(Bul >> 31)) {
+          pa[2] = __ldcg(Ps + gblk(g, grun(g, k, jl, Tl, Bl, run_at(cl, 31))));
+          pb[2] = __ldcg(Ps + gblk(g, grun(g, k - 1, jr, Tur, Bur, run_at(Tur | Bur, 0))));
+        }
+      }
+      unsigned long long prev[2] = {0ull, 0ull};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const uint32_t lo = min(pa[q], pb[q]), hi = max(pa[q], pb[q]);
+        const unsigned long long key = (static_cast<unsigned long long>(hi) << 32) | lo;
+        // absent or already-joined pairs (lo == hi) and a lane's repeats drop out
+        const bool need = lo != hi && (q < 1 || key != prev[0]) && (q < 2 || key != prev[1]);
+        if (q < 2) prev[q] = key;
+        const unsigned grp = __match_any_sync(maskB, need ? key : 0ull);
+        if (need && lane == __ffs(grp) - 1) gunite(Ps, g, pa[q], pb[q]);
       }
     }
   }
