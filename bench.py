@@ -1033,7 +1033,7 @@ def main():
                 "grid_barrier_floor_us": 1.64,
                 "barrier_source": "tools/ubench_barrier.cu, 592 co-resident CTAs "
                                   "(profiles/r02_ubench_barrier.txt)",
-                "phase_timeline": "profiles/r02i_chain_phases.txt (SLCS_PHASE_TIMING=1)"},
+                "phase_timeline": "profiles/r02j_chain_phases.txt (SLCS_PHASE_TIMING=1)"},
             "compulsory_bytes_per_px": 0.375,
             "compulsory_frac": 0.375 * px * units / launch_s / 1e9 / peak,
         }
