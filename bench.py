@@ -630,7 +630,12 @@ def c4_result(args, ws, rank, local, dev, stream, n=16384):
                                                    "labels)",
                          "achieved": 4.125 * px / tc / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": 4.125 * px / tc / 1e9 / peak, "traffic": ccl_traffic,
-                         "traffic_source": ccl_src, "peak_source": pk},
+                         "traffic_source": ccl_src, "peak_source": pk,
+                         "note": "not HBM-bound: k_tile_local (~70 % of the ccl) is issue-bound "
+                                 "(~84 % of issue slots busy at 13.8 active threads per warp "
+                                 "instruction, 305 MB DRAM per launch; "
+                                 "profiles/r02i_ncu_tile_local_full.txt); the union count per "
+                                 "run is near its floor (DESIGN.md section 12)"},
             "checksum_ok": checks or None, "e2e": e2e, "cpu_baseline": cpu})
 
 
