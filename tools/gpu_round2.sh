@@ -14,6 +14,7 @@ fi
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"; tail -c 300 $O/bench.json; tail -3 $O/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2>&1; echo "ref rc=$?"; tail -c 300 $O/bench_ref.json
 SLCS_PHASE_TIMING=1 timeout 120 python tools/prof_chain.py 1000 3 2> $O/chain_phases.txt > /dev/null; tail -1 $O/chain_phases.txt
+[ -x tools/ubench_barrier ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_barrier tools/ubench_barrier.cu
 timeout 60 ./tools/ubench_barrier > $O/ubench_barrier.txt 2>&1; tail -3 $O/ubench_barrier.txt
 if [ "${SKIP_NCU:-0}" = "0" ]; then
 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/launches_bench.csv \
